@@ -1,0 +1,89 @@
+/*
+ * avion_b200.h -- C ABI of the B200-native AVION training hot path.
+ *
+ * One shared library, paper_2309_16669_b200/libavion_b200.so, built for
+ * sm_100a only.  Every entry point:
+ *   - takes plain device pointers + sizes/strides (no torch types),
+ *   - launches asynchronously on the caller's CUDA stream (`stream` is a
+ *     cudaStream_t passed as void*; NULL = legacy default stream),
+ *   - never synchronises and never allocates device memory the caller
+ *     did not pass in, except the per-process cached TMA descriptors,
+ *   - returns AVB_OK (0) or an AVB_E_* code; avb_last_error() gives text.
+ * The host-side argument checks run before any launch, so a bad call leaves
+ * the output untouched (the reference raises InputError "before any decode",
+ * pkg/src/vidpipe/decoder.py:116-119).
+ *
+ * Reference interfaces replaced (file:line under /root/reference):
+ *   avb_rrc_normalize  <- _codec.yuv_to_rgb(y,u,v,hflip,tw,th)
+ *                           pkg/src/vidpipe/_codec/codec.cpp:250-275 (binding :806-807)
+ *                         VideoReader.current_rgb(x,y,w,h,hflip,tw,th)
+ *                           codec.cpp:452-467 (binding :823-825)
+ *                         and the Python step that calls them per frame,
+ *                           decoder.py:257-271 (crop_planes :282-292),
+ *                         extended with the GPU normalize + cast the reference
+ *                         defers.
+ *   avb_rrc_taps       <- (test hook) the tap table the scaler derives from
+ *                         (crop, target); codec.cpp:233-241.
+ *   everything else    <- no reference code: the encoder / attention / loss
+ *                         the reference only names (README.md:159-161,
+ *                         models.py:34-74,127-145).
+ */
+#ifndef AVION_B200_H
+#define AVION_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---- */
+#define AVB_OK             0
+#define AVB_E_ARG          1  /* bad dims / strides / dtype / null pointer   */
+#define AVB_E_BOX          2  /* crop box not contained in the frame         */
+#define AVB_E_UNSUPPORTED  3  /* valid but outside the kernel's envelope     */
+#define AVB_E_CUDA         4  /* CUDA runtime / launch error                 */
+
+/* ---- enums ---- */
+#define AVB_DTYPE_BF16     0
+#define AVB_DTYPE_F32      1
+
+#define AVB_LAYOUT_CTHW    0  /* dst [B,3,T,Ht,Wt]  (encoder input)            */
+#define AVB_LAYOUT_TCHW    1  /* dst [B,T,3,Ht,Wt]  (reference Batch.frames)   */
+
+const char* avb_last_error(void);
+int avb_version(void);
+int avb_device_sm_count(void);
+
+/*
+ * K1: fused crop -> hflip -> antialiased bilinear -> normalize -> cast.
+ *   src        uint8 frames, element (b,t,y,x,c) at
+ *              src[b*s_clip + t*s_t + y*s_h + x*s_w + c*s_c]   (byte strides)
+ *              Fast path: s_c == 1 && s_w == 3 (interleaved RGB, THWC).
+ *              Any other strides (e.g. the reference's [B,T,3,H,W]) take the
+ *              generic path.
+ *   boxes_dev  int32 [B,4] device, CropRect order (x, y, crop_w, crop_h)
+ *   hflip_dev  uint8 [B] device (nullable = no flip)
+ *   boxes_host optional host copy of boxes; when given, every box is checked
+ *              against (W,H) and AVB_E_BOX returned before launch.  The kernel
+ *              re-checks on device and leaves invalid clips untouched.
+ *   mean3, inv_std3  host float[3]; y = (v/255 - mean[c]) * inv_std[c]
+ *   dst        device, layout per out_layout, dtype per out_dtype
+ */
+int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, int W,
+                      int64_t s_clip, int64_t s_t, int64_t s_h, int64_t s_w, int64_t s_c,
+                      const int32_t* boxes_dev, const uint8_t* hflip_dev,
+                      const int32_t* boxes_host, int Ht, int Wt,
+                      const float* mean3, const float* inv_std3,
+                      int out_dtype, int out_layout, void* dst, void* stream);
+
+/* Test hook: the device-computed tap table for one (crop, target) pair:
+ * lo[tgt], hi[tgt] int32 device, weights[tgt*max_taps] float device. */
+int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_dev,
+                 int max_taps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AVION_B200_H */

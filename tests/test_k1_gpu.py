@@ -1,0 +1,132 @@
+"""K1 parity on the GPU: CUDA kernel vs the float64 numpy oracle on identical inputs + boxes.
+
+Tolerances (BASELINE.json north_star / SURVEY.md 8(c)):
+  * tap index ranges: bit-exact; gather at identity scale: exact;
+  * fp32 output: <= 1e-3 absolute;
+  * bf16 output: <= 1 bf16 ulp of the oracle value.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import transform_oracle as O
+from paper_2309_16669_b200 import transform as T
+from paper_2309_16669_b200.errors import InputError
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rrc_golden.json")))
+CFG2 = np.asarray(GOLD["config2_568x320"], dtype=np.int32)
+
+
+def frames_u8(B, Tn, H, W, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, 256, (B, Tn, H, W, 3), generator=g, dtype=torch.uint8)
+
+
+def bf16_ulp(x):
+    a = np.abs(x).astype(np.float64)
+    e = np.floor(np.log2(np.maximum(a, 1e-30)))
+    return np.where(a > 0, 2.0 ** (e - 7), 2.0 ** -133)
+
+
+@pytest.mark.parametrize("crop,tgt", [(303, 224), (392, 224), (427, 224), (448, 224), (100, 224), (224, 224),
+                                      (7, 3), (5, 9), (568, 224), (1, 224)])
+def test_device_taps_bit_exact(crop, tgt):
+    lo, hi, w = T.device_taps(crop, tgt)
+    elo, ehi = O.tap_ranges(crop, tgt)
+    assert np.array_equal(lo.cpu().numpy(), elo)
+    assert np.array_equal(hi.cpu().numpy(), ehi)
+    m = O.weight_matrix(crop, tgt)
+    wd = w.cpu().numpy()
+    for i in range(tgt):
+        n = ehi[i] - elo[i]
+        assert np.allclose(wd[i, :n], m[i, elo[i]:ehi[i]], atol=1e-7, rtol=0)
+
+
+def test_identity_gather_exact():
+    fr = frames_u8(2, 3, 64, 80, seed=1)
+    boxes = np.asarray([[0, 0, 80, 64], [0, 0, 80, 64]], dtype=np.int32)
+    out = T.transform(fr.cuda(), boxes, [0, 1], (64, 80), mean=(0, 0, 0), std=(1, 1, 1), out_dtype=torch.float32)
+    ref = fr.numpy().transpose(0, 4, 1, 2, 3).astype(np.float64) / 255.0
+    ref[1] = ref[1][..., ::-1]
+    assert np.abs(out.cpu().numpy() - ref).max() < 1e-6
+    # byte-exact gather: recover the source bytes
+    back = np.rint(out.cpu().numpy() * 255.0)
+    assert np.array_equal(back[0], fr.numpy()[0].transpose(3, 0, 1, 2))
+
+
+@pytest.mark.parametrize("layout", ["cthw", "tchw"])
+def test_config2_boxes_fp32_and_bf16(layout):
+    B, Tn = 6, 4
+    fr = frames_u8(B, Tn, 320, 568, seed=2)
+    boxes, flips = CFG2[:B, :4], CFG2[:B, 4]
+    ref = O.transform_batch(fr.numpy(), boxes, flips)                     # [B,3,T,224,224]
+    if layout == "tchw":
+        ref = ref.transpose(0, 2, 1, 3, 4)
+    d = fr.cuda()
+    o32 = T.transform(d, boxes, flips, out_dtype=torch.float32, layout=layout).cpu().numpy()
+    assert np.abs(o32 - ref).max() <= 1e-3
+    o16 = T.transform(d, boxes, flips, out_dtype=torch.bfloat16, layout=layout).float().cpu().numpy()
+    assert np.all(np.abs(o16 - ref) <= bf16_ulp(ref) + 1e-6)
+
+
+def test_generic_strides_reference_batch_layout():
+    """[B,T,3,H,W] planar (reference Batch.frames) takes the generic-stride path."""
+    B, Tn = 3, 2
+    fr = frames_u8(B, Tn, 120, 200, seed=3)
+    planar = fr.permute(0, 1, 4, 2, 3).contiguous().cuda()               # [B,T,3,H,W]
+    boxes = np.asarray([[3, 5, 150, 101], [0, 0, 200, 120], [50, 19, 77, 99]], dtype=np.int32)
+    flips = np.asarray([1, 0, 1])
+    out = T.transform(planar, boxes, flips, (64, 96), channels_last=False, out_dtype=torch.float32)
+    ref = O.transform_batch(fr.numpy(), boxes, flips, (64, 96))
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+
+
+@pytest.mark.parametrize("H,W,Ht,Wt,box", [(40, 50, 97, 131, (3, 2, 41, 33)),   # upscale, odd Wt
+                                           (33, 47, 33, 47, (0, 0, 47, 33)),    # identity, odd
+                                           (9, 9, 1, 1, (0, 0, 9, 9)),          # to 1 pixel
+                                           (600, 1000, 224, 224, (10, 20, 980, 570))])  # 4.4x down
+def test_edge_shapes(H, W, Ht, Wt, box):
+    fr = frames_u8(1, 2, H, W, seed=4)
+    out = T.transform(fr.cuda(), np.asarray([box], dtype=np.int32), [1], (Ht, Wt), out_dtype=torch.float32)
+    ref = O.transform_batch(fr.numpy(), np.asarray([box]), np.asarray([1]), (Ht, Wt))
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+
+
+def test_out_buffer_and_errors():
+    fr = frames_u8(2, 2, 50, 60).cuda()
+    boxes = np.asarray([[0, 0, 60, 50], [10, 10, 50, 40]], dtype=np.int32)
+    buf = torch.full((2, 3, 2, 32, 32), 7.0, dtype=torch.bfloat16, device="cuda")
+    r = T.transform(fr, boxes, None, (32, 32), out=buf)
+    assert r.data_ptr() == buf.data_ptr()
+    with pytest.raises(InputError):
+        T.transform(fr, boxes, None, (32, 31), out=buf)                     # shape mismatch
+    bad = np.asarray([[0, 0, 60, 50], [11, 10, 50, 40]], dtype=np.int32)  # x + w = 61 > 60
+    before = buf.clone()
+    with pytest.raises(InputError):
+        T.transform(fr, bad, None, (32, 32), out=buf)
+    torch.cuda.synchronize()
+    assert torch.equal(before, buf)                                          # untouched on error
+    with pytest.raises(InputError):
+        T.transform(fr.cpu(), boxes, None, (32, 32))                        # no CPU path
+
+
+def test_full_config2_size_properties():
+    """B=64, T=16, 568x320 -> 224^2 bf16: spot-check clips vs oracle + flip/mirror property."""
+    B, Tn = 64, 16
+    g = torch.Generator(device="cuda").manual_seed(0)
+    fr = torch.randint(0, 256, (B, Tn, 320, 568, 3), generator=g, dtype=torch.uint8, device="cuda")
+    boxes, flips = CFG2[:B, :4], CFG2[:B, 4]
+    out = T.transform(fr, boxes, flips)
+    assert out.shape == (B, 3, Tn, 224, 224) and torch.isfinite(out.float()).all()
+    for b in (0, 1, 37, 63):
+        ref = O.transform_clip(fr[b, :4].cpu().numpy(), boxes[b], bool(flips[b]))
+        o = out[b, :, :4].float().cpu().numpy()
+        assert np.all(np.abs(o - ref) <= bf16_ulp(ref) + 1e-6)
+    # flipping the flip bit mirrors the output columns (up to bf16 rounding of equal values)
+    out2 = T.transform(fr, boxes, 1 - flips)
+    assert (out2.float() - out.float().flip(-1)).abs().max().item() <= 0.02
