@@ -52,6 +52,13 @@ extern "C" {
 #define AVB_LAYOUT_CTHW    0  /* dst [B,3,T,Ht,Wt]  (encoder input)            */
 #define AVB_LAYOUT_TCHW    1  /* dst [B,T,3,Ht,Wt]  (reference Batch.frames)   */
 
+/* GEMM epilogues (avb_gemm) */
+#define AVB_EPI_BF16       0  /* C bf16 = alpha*acc (+bias) (+aux residual)                 */
+#define AVB_EPI_BIAS_GELU  1  /* aux_out bf16 = alpha*acc+bias; C bf16 = QuickGELU(aux_out)   */
+#define AVB_EPI_DGELU      2  /* C bf16 = alpha*acc * QuickGELU'(aux)                       */
+#define AVB_EPI_F32        3  /* C fp32 = alpha*acc (+bias)                                 */
+#define AVB_EPI_F32_ACCUM  4  /* C fp32 += alpha*acc (red.add; allows split_k > 1)          */
+
 const char* avb_last_error(void);
 int avb_version(void);
 int avb_device_sm_count(void);
@@ -82,6 +89,20 @@ int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, int W,
  * lo[tgt], hi[tgt] int32 device, weights[tgt*max_taps] float device. */
 int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_dev,
                  int max_taps, void* stream);
+
+/*
+ * K2/K3: C[M,N] = epilogue(alpha * sum_k A[m,k] B[n,k]) on tcgen05 (TMEM accumulators, TMA
+ * 128B-swizzled operands, persistent warp-specialised, 1 CTA per SM).
+ *   A: a_major 0 -> row-major [M,K] (lda >= K);  1 -> row-major [K,M] (lda >= M)
+ *   B: b_major 0 -> row-major [N,K] (ldb >= K);  1 -> row-major [K,N] (ldb >= N)
+ *   bf16 operands, 16-byte aligned, leading dims multiples of 8 elements.
+ *   bias: fp32 [N] or NULL.  aux/aux_out: bf16 [M, ldaux] (see AVB_EPI_*).
+ * Used for patch-embed (K2), QKV / out-proj / fc1 / fc2 forward, dgrad (A K-major, B MN-major)
+ * and wgrad (both MN-major, EPI_F32_ACCUM, split_k over the token dimension).
+ */
+int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, int64_t ldb, int b_major,
+             void* C, int64_t ldc, int M, int N, int K, int epilogue, const float* bias,
+             const void* aux, int64_t ldaux, void* aux_out, float alpha, int split_k, void* stream);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,8 @@ EXPORTS: dict[str, tuple] = {
     "avb_rrc_normalize": (_i32, [_vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64,
                                  _vp, _vp, _vp, _i32, _i32, _f32p, _f32p, _i32, _i32, _vp, _vp]),
     "avb_rrc_taps": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32, _vp]),
+    "avb_gemm": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp,
+                        C.c_float, _i32, _vp]),
 }
 
 _lock = threading.Lock()

@@ -1,0 +1,438 @@
+// K2/K3: persistent warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+//   C[M,N] = epilogue( sum_k A[m,k] * B[n,k] )
+//
+// Operands are bf16, fed by TMA (128B swizzle) through an mbarrier ring into UMMA
+// (tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16), accumulating in TMEM
+// (two BN-column accumulators so the epilogue of tile i overlaps the MMAs of tile i+1).
+// Each operand may be K-major (A:[M,K], B:[N,K]) or MN-major (A:[K,M], B:[K,N]) so
+// forward (X W^T), dgrad (dY W) and wgrad (dY^T X) all run without transposes.
+//
+// Warp roles (256 threads, 1 CTA/SM):
+//   warp 0     TMA producer (one lane)
+//   warp 1     MMA issuer   (one lane)
+//   warp 2     TMEM allocator
+//   warps 4-7  epilogue: tcgen05.ld 32 lanes x 32 columns -> bias / QuickGELU / residual /
+//              dGELU / fp32 split-K reduction -> global.
+//
+// No reference code exists for this (absent in the reference,
+// restated from PAPER.md:258-260,727).
+#include "tc_common.cuh"
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+struct GemmArgs {
+  void* C;
+  int64_t ldc;
+  int M, N, K;
+  int epi;
+  const float* bias;     // [N] fp32 or null
+  const void* aux;       // bf16 [M, ldaux]: residual (EPI_BF16) or GELU pre-activation (EPI_DGELU)
+  int64_t ldaux;
+  void* aux_out;         // bf16 [M, ldaux]: pre-activation out (EPI_BIAS_GELU)
+  int num_m, num_n, splits, kb_per_split, num_kb;
+  int vec_ok;            // 16B-aligned rows for vector epilogue stores
+  float alpha;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;               // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;               // 32 KB (BN=256)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+};
+
+__device__ __forceinline__ void store_row_chunk(const GemmArgs& a, int row, int col, float (&v)[32]) {
+  // v: 32 consecutive columns [col, col+32) of `row`, epilogue already applied
+  if (row >= a.M) return;
+  const bool full = (col + 32 <= a.N) && a.vec_ok;
+  if (a.epi == AVB_EPI_F32_ACCUM) {
+    float* c = reinterpret_cast<float*>(a.C) + (int64_t)row * a.ldc + col;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(c + j), "f"(v[j]), "f"(v[j + 1]),
+                     "f"(v[j + 2]), "f"(v[j + 3])
+                     : "memory");
+    } else {
+      for (int j = 0; j < 32 && col + j < a.N; ++j) atomicAdd(c + j, v[j]);
+    }
+    return;
+  }
+  if (a.epi == AVB_EPI_F32) {
+    float* c = reinterpret_cast<float*>(a.C) + (int64_t)row * a.ldc + col;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+      for (int j = 0; j < 32 && col + j < a.N; ++j) c[j] = v[j];
+    }
+    return;
+  }
+  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(a.C) + (int64_t)row * a.ldc + col;
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 q;
+      q.x = pack_bf16x2(v[j], v[j + 1]);
+      q.y = pack_bf16x2(v[j + 2], v[j + 3]);
+      q.z = pack_bf16x2(v[j + 4], v[j + 5]);
+      q.w = pack_bf16x2(v[j + 6], v[j + 7]);
+      *reinterpret_cast<uint4*>(c + j) = q;
+    }
+  } else {
+    for (int j = 0; j < 32 && col + j < a.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+__device__ __forceinline__ void load_aux_chunk(const GemmArgs& a, const void* base, int row, int col, float (&o)[32]) {
+  const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(base) + (int64_t)row * a.ldaux + col;
+  if (row < a.M && col + 32 <= a.N && a.vec_ok) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 q = *reinterpret_cast<const uint4*>(p + j);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(h[e]);
+        o[j + 2 * e] = f.x;
+        o[j + 2 * e + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = (row < a.M && col + j < a.N) ? __bfloat162float(p[j]) : 0.f;
+  }
+}
+
+__device__ __forceinline__ void store_aux_chunk(const GemmArgs& a, int row, int col, const float (&v)[32]) {
+  if (row >= a.M) return;
+  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(a.aux_out) + (int64_t)row * a.ldaux + col;
+  if (col + 32 <= a.N && a.vec_ok) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 q;
+      q.x = pack_bf16x2(v[j], v[j + 1]);
+      q.y = pack_bf16x2(v[j + 2], v[j + 3]);
+      q.z = pack_bf16x2(v[j + 4], v[j + 5]);
+      q.w = pack_bf16x2(v[j + 6], v[j + 7]);
+      *reinterpret_cast<uint4*>(c + j) = q;
+    }
+  } else {
+    for (int j = 0; j < 32 && col + j < a.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs a) {
+  using C = Cfg<BN, A_MN, B_MN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = a.num_m * a.num_n * a.splits;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mn = t % (a.num_m * a.num_n);
+        const int split = t / (a.num_m * a.num_n);
+        const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN;
+        const int kb0 = split * a.kb_per_split;
+        const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tc::tma_load_2d(sa + j * 8192, &tmA, &full[stage], m0 + 64 * j, k0);
+          } else {
+            tc::tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tc::tma_load_2d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+          } else {
+            tc::tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const int split = t / (a.num_m * a.num_n);
+        const int kb0 = split * a.kb_per_split;
+        const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = A_MN ? tc::sdesc_sw128(sa + k * 2048, 8192, 1024) : tc::sdesc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t db = B_MN ? tc::sdesc_sw128(sb + k * 2048, 8192, 1024) : tc::sdesc_sw128(sb + k * 32, 16, 1024);
+            tc::umma_f16_ss(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc::umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue
+    const int ew = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const int mn = t % (a.num_m * a.num_n);
+      const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::tc_fence_after();
+      const int row = m0 + ew * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col = n0 + c * 32;
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tmem + acc * BN + ((uint32_t)(ew * 32) << 16) + c * 32, r);
+        tc::tmem_ld_wait();
+        if (col >= a.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * a.alpha;
+        if (a.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += (col + j < a.N) ? __ldg(a.bias + col + j) : 0.f;
+        }
+        if (a.epi == AVB_EPI_BF16) {
+          if (a.aux) {
+            float rr[32];
+            load_aux_chunk(a, a.aux, row, col, rr);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += rr[j];
+          }
+        } else if (a.epi == AVB_EPI_BIAS_GELU) {
+          store_aux_chunk(a, row, col, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = tc::quick_gelu(v[j]);
+        } else if (a.epi == AVB_EPI_DGELU) {
+          float h[32];
+          load_aux_chunk(a, a.aux, row, col, h);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= tc::quick_gelu_grad(h[j]);
+        }
+        store_row_chunk(a, row, col, v);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t st) {
+  using C = Cfg<BN, A_MN, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return avb::cuda_status(e, "gemm: set smem attribute");
+    attr = true;
+  }
+  const int total = a.num_m * a.num_n * a.splits;
+  const int grid = total < avb::sm_count() ? total : avb::sm_count();
+  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::SMEM, st>>>(ta, tb, a);
+  return avb::launch_status("avb_gemm");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ tensor maps
+namespace avb {
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encode() {
+  if (g_encode) return AVB_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return AVB_E_CUDA;
+  }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return AVB_OK;
+}
+
+int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                      uint32_t box_inner, uint32_t box_outer) {
+  int s = get_encode();
+  if (s) return s;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu box=%u,%u", (int)r,
+              (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)ld_elems, box_inner, box_outer);
+    return AVB_E_ARG;
+  }
+  return AVB_OK;
+}
+
+int make_tmap_3d_bf16(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_elems,
+                      uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2) {
+  int s = get_encode();
+  if (s) return s;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1_elems * 2, s2_elems * 2};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(3d) failed (%d)", (int)r);
+    return AVB_E_ARG;
+  }
+  return AVB_OK;
+}
+}  // namespace avb
+
+extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, int64_t ldb, int b_major, void* C,
+                        int64_t ldc, int M, int N, int K, int epilogue, const float* bias, const void* aux,
+                        int64_t ldaux, void* aux_out, float alpha, int split_k, void* stream) {
+  AVB_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "negative GEMM dims");
+  if (M == 0 || N == 0) return AVB_OK;
+  AVB_CHECK_ARG(K >= 1, "K must be >= 1");
+  AVB_CHECK_ARG(A && B && C, "null operand");
+  AVB_CHECK_ARG(a_major == 0 || a_major == 1, "a_major must be 0 (K-major) or 1 (MN-major)");
+  AVB_CHECK_ARG(b_major == 0 || b_major == 1, "b_major must be 0 (K-major) or 1 (MN-major)");
+  AVB_CHECK_ARG(epilogue >= AVB_EPI_BF16 && epilogue <= AVB_EPI_F32_ACCUM, "bad epilogue %d", epilogue);
+  AVB_CHECK_ARG((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
+                "A/B must be 16-byte aligned");
+  AVB_CHECK_ARG((lda * 2) % 16 == 0 && (ldb * 2) % 16 == 0, "lda/ldb must be multiples of 8 elements");
+  AVB_CHECK_ARG(lda >= (a_major ? M : K) && ldb >= (b_major ? N : K), "leading dimension too small");
+  AVB_CHECK_ARG(ldc >= N, "ldc < N");
+  AVB_CHECK_ARG(epilogue != AVB_EPI_BIAS_GELU || aux_out, "BIAS_GELU needs aux_out");
+  AVB_CHECK_ARG(epilogue != AVB_EPI_DGELU || aux, "DGELU needs aux (pre-activation)");
+  AVB_CHECK_ARG(split_k >= 1, "split_k must be >= 1");
+  AVB_CHECK_ARG(split_k == 1 || epilogue == AVB_EPI_F32_ACCUM, "split_k > 1 needs EPI_F32_ACCUM");
+
+  const int BN = (N <= 128) ? 128 : 256;
+  CUtensorMap ta, tb;
+  int s;
+  if (a_major == 0)
+    s = avb::make_tmap_2d_bf16(&ta, A, K, M, lda, 64, 128);
+  else
+    s = avb::make_tmap_2d_bf16(&ta, A, M, K, lda, 64, 64);
+  if (s) return s;
+  if (b_major == 0)
+    s = avb::make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, BN);
+  else
+    s = avb::make_tmap_2d_bf16(&tb, B, N, K, ldb, 64, 64);
+  if (s) return s;
+
+  GemmArgs g;
+  g.C = C;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.epi = epilogue;
+  g.bias = bias;
+  g.aux = aux;
+  g.ldaux = ldaux;
+  g.aux_out = aux_out;
+  g.alpha = alpha;
+  g.num_m = (M + BM - 1) / BM;
+  g.num_n = (N + BN - 1) / BN;
+  g.num_kb = (K + BK - 1) / BK;
+  int splits = split_k;
+  if (splits > g.num_kb) splits = g.num_kb;
+  g.kb_per_split = (g.num_kb + splits - 1) / splits;
+  g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;
+  const int esz = (epilogue == AVB_EPI_F32 || epilogue == AVB_EPI_F32_ACCUM) ? 4 : 2;
+  g.vec_ok = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc * esz) % 16 == 0) &&
+             (!aux || (((reinterpret_cast<uintptr_t>(aux) & 15) == 0) && (ldaux * 2) % 16 == 0)) &&
+             (!aux_out || (((reinterpret_cast<uintptr_t>(aux_out) & 15) == 0) && (ldaux * 2) % 16 == 0));
+  cudaStream_t st = avb::as_stream(stream);
+  const int key = (BN == 256 ? 4 : 0) | (a_major << 1) | b_major;
+  switch (key) {
+    case 0: return launch<128, false, false>(ta, tb, g, st);
+    case 1: return launch<128, false, true>(ta, tb, g, st);
+    case 2: return launch<128, true, false>(ta, tb, g, st);
+    case 3: return launch<128, true, true>(ta, tb, g, st);
+    case 4: return launch<256, false, false>(ta, tb, g, st);
+    case 5: return launch<256, false, true>(ta, tb, g, st);
+    case 6: return launch<256, true, false>(ta, tb, g, st);
+    default: return launch<256, true, true>(ta, tb, g, st);
+  }
+}
