@@ -104,6 +104,27 @@ int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, int64_t ldb
              void* C, int64_t ldc, int M, int N, int K, int epilogue, const float* bias,
              const void* aux, int64_t ldaux, void* aux_out, float alpha, int split_k, void* stream);
 
+/*
+ * K4: blockwise attention forward, head_dim 64, fp32 online softmax, O(N) memory.
+ *   q,k,v: bf16 [B, N, H, 64] views: element (b,n,h,d) at p[b*sb + n*ld + h*64 + d]
+ *          (the packed QKV GEMM output works directly: q=qkv, k=qkv+H*64, v=qkv+2*H*64)
+ *   o:     bf16, same form with (ld_o, sb_o)
+ *   lse:   fp32 [B*H, Npad] natural-log row log-sum-exp, Npad = roundup(N,128)
+ */
+int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb,
+                 void* o, int64_t ld_o, int64_t sb_o, float* lse, int B, int H, int N,
+                 int head_dim, float softmax_scale, int causal, void* stream);
+
+/*
+ * K5: blockwise attention backward (recomputes P from lse; no N x N storage).
+ *   o, dout share (ld_o, sb_o); dq, dk, dv share (ld_g, sb_g).
+ *   delta:  fp32 scratch [B*H, Npad];  dq_acc: fp32 scratch [B, N, H, 64].
+ */
+int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb,
+                 const void* o, const void* dout, int64_t ld_o, int64_t sb_o, const float* lse,
+                 float* delta, float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g,
+                 int B, int H, int N, int head_dim, float softmax_scale, int causal, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

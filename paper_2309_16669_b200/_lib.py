@@ -33,6 +33,10 @@ EXPORTS: dict[str, tuple] = {
     "avb_rrc_taps": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32, _vp]),
     "avb_gemm": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp,
                         C.c_float, _i32, _vp]),
+    "avb_attn_fwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _i32, C.c_float,
+                            _i32, _vp]),
+    "avb_attn_bwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
+                            _i64, _i32, _i32, _i32, _i32, C.c_float, _i32, _vp]),
 }
 
 _lock = threading.Lock()

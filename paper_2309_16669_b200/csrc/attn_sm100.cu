@@ -1,0 +1,690 @@
+// K4/K5: blockwise (Flash-style) attention forward/backward on tcgen05, head_dim 64.
+//
+// PAPER.md:265-272, :350-357 (O(N) memory: no N x N tensor is stored; the memory
+// contract the reference models at models.py:137-140 -- O plus per-row statistics).
+// No reference code exists for the kernels themselves.
+//
+// Layout: Q/K/V/O are [B, N, H, 64] bf16 views with row stride `ld` and batch stride `sb`
+// (elements), e.g. the packed QKV GEMM output [B*N, 3*H*64] with q=qkv, k=qkv+D, v=qkv+2D.
+// LSE / delta are fp32 [B*H, Npad], Npad = roundup(N, 128).
+//
+// Forward, one CTA per (128-query tile, head, clip), 2 CTAs per SM (112 KB smem, 256 TMEM cols):
+//   warp 4  TMA: Q once, then K_j/V_j through a 2-stage ring
+//   warp 5  MMA: S = Q K_j^T (M128 N128 K64) -> TMEM; O_j = P_j V_j (M128 N64 K128, V MN-major)
+//   warps 0-3 softmax, thread = query row: two TMEM passes over S (row max, then exp2 + sum +
+//           bf16 pack into the 128B-swizzled P tile in smem), O_j folded into registers with the
+//           online-softmax rescale.
+// Backward, one CTA per (128-key tile, head, clip), 1 CTA per SM:
+//   S^T = K Q_i^T and dP^T = V dO_i^T into TMEM; warps 0-3 (thread = key row) form
+//   P^T = exp2(S^T*scale*log2e - LSE*log2e) and dS^T = scale * P^T (dP^T - delta) in smem;
+//   dV += P^T dO_i, dK += dS^T Q_i accumulate in TMEM across query tiles; dQ_i = dS_i K
+//   (dS^T's smem tile re-read as an MN-major A operand) is drained from TMEM with
+//   red.global.add.v4.f32 into an fp32 accumulator, converted to bf16 by a tiny kernel.
+#include "tc_common.cuh"
+
+namespace {
+
+constexpr int HD = 64;
+constexpr int BT = 128;  // tile rows (queries or keys)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// write 8 consecutive bf16 (one 16B unit) of row `row` into a K-major SW128 tile set
+// (tiles of [128 rows][64 cols], 16 KB each); col8 = column / 8 (0..15)
+__device__ __forceinline__ void st_sw128(uint8_t* base, int row, int col8, uint4 v) {
+  const int tile = col8 >> 3, u = col8 & 7;
+  *reinterpret_cast<uint4*>(base + tile * 16384 + row * 128 + ((u ^ (row & 7)) << 4)) = v;
+}
+
+struct FwdArgs {
+  int B, H, N, Npad;
+  float scale_log2;
+  __nv_bfloat16* o;
+  int64_t ld_o, sb_o;
+  float* lse;
+  int causal;
+};
+
+constexpr int F_SQ = 0, F_SKV = 16384, F_SP = F_SKV + 2 * 32768, F_TILES = F_SP + 32768;
+// barriers live in the first 128 B of the dynamic window, tiles start at the next 1 KB boundary;
+// 115712 B = (228 KB - 2 x 1 KB reserved) / 2 keeps two CTAs per SM.
+constexpr int F_SMEM = F_TILES + 1024;
+static_assert(F_SMEM <= 115712, "attn fwd must fit two CTAs per SM");
+
+__global__ void __launch_bounds__(192, 2)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 128 + 1023) & ~uintptr_t(1023));
+  if (smem + F_TILES > smem_raw + F_SMEM) __trap();  // dynamic smem base not 1 KB aligned
+  uint8_t* sQ = smem + F_SQ;
+  uint8_t* sKV = smem + F_SKV;
+  uint8_t* sP = smem + F_SP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* o_full = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qt * BT;
+  const int nkv_all = (a.N + BT - 1) / BT;
+  const int nkv = a.causal ? min(nkv_all, qt + 1) : nkv_all;
+
+  if (warp == 4 && lane == 0) {
+    tc::tma_prefetch(&tmQ);
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmV);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&kv_full[s], 1);
+      tc::mbar_init(&kv_empty[s], 1);
+    }
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(o_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 5) tc::tmem_alloc(tmem_slot, 256);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + 128;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(q_full, 16384);
+      tc::tma_load_3d(sQ, &tmQ, q_full, h * HD, q0, b);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        tc::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&kv_full[st], 32768);
+        tc::tma_load_3d(sKV + st * 32768, &tmK, &kv_full[st], h * HD, j * BT, b);
+        tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idO = tc::idesc_bf16_f32(128, 64, 0, 1);
+      const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
+      tc::mbar_wait(q_full, 0);
+      for (int j = 0; j <= nkv; ++j) {
+        if (j < nkv) {
+          const int st = j & 1;
+          tc::mbar_wait(&kv_full[st], (j >> 1) & 1);
+          if (j > 0) tc::mbar_wait(p_full, (j - 1) & 1);
+          tc::tc_fence_after();
+          const uint32_t aK = smem_u32(sKV + st * 32768);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::umma_f16_ss(tS, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024), idS,
+                            kk > 0);
+          tc::umma_commit(s_full);
+        } else {
+          tc::mbar_wait(p_full, (j - 1) & 1);
+          tc::tc_fence_after();
+        }
+        if (j > 0) {
+          const int ps = (j - 1) & 1;
+          const uint32_t aV = smem_u32(sKV + ps * 32768 + 16384);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            tc::umma_f16_ss(tO, tc::sdesc_sw128(aP + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                            tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO, kk > 0);
+          tc::umma_commit(o_full);
+          tc::umma_commit(&kv_empty[ps]);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax warps
+    const int row = warp * 32 + lane;
+    const int qi = q0 + row;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    float o[HD];
+#pragma unroll
+    for (int e = 0; e < HD; ++e) o[e] = 0.f;
+
+    for (int j = 0; j < nkv; ++j) {
+      tc::mbar_wait(s_full, j & 1);
+      tc::tc_fence_after();
+      const int kv0 = j * BT;
+      int lim = a.N - kv0;                       // valid key columns in this tile
+      if (a.causal) lim = min(lim, qi - kv0 + 1);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tS + lane_off + c * 32, r);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (c * 32 + e < lim) mx = fmaxf(mx, __uint_as_float(r[e]));
+      }
+      const float m_new = fmaxf(m, mx * a.scale_log2);
+      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+      const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_use);
+      if (j > 0) {
+        tc::mbar_wait(o_full, (j - 1) & 1);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[c * 32 + e] = fmaf(o[c * 32 + e], alpha_prev, __uint_as_float(r[e]));
+        }
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tS + lane_off + c * 32, r);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float p[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = c * 32 + u * 8 + e;
+            const float pe = (col < lim) ? ex2(fmaf(__uint_as_float(r[u * 8 + e]), a.scale_log2, -m_use)) : 0.f;
+            p[e] = pe;
+            sum += pe;
+          }
+          uint4 v;
+          v.x = pack_bf16x2(p[0], p[1]);
+          v.y = pack_bf16x2(p[2], p[3]);
+          v.z = pack_bf16x2(p[4], p[5]);
+          v.w = pack_bf16x2(p[6], p[7]);
+          st_sw128(sP, row, c * 4 + u, v);
+        }
+      }
+      l = fmaf(l, alpha, sum);
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_full);
+      alpha_prev = alpha;
+      m = m_new;
+    }
+    tc::mbar_wait(o_full, (nkv - 1) & 1);
+    tc::tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t r[32];
+      tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[c * 32 + e] = fmaf(o[c * 32 + e], alpha_prev, __uint_as_float(r[e]));
+    }
+    if (qi < a.N) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* dst = a.o + (int64_t)b * a.sb_o + (int64_t)qi * a.ld_o + h * HD;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint4 v;
+        v.x = pack_bf16x2(o[u * 8 + 0] * inv, o[u * 8 + 1] * inv);
+        v.y = pack_bf16x2(o[u * 8 + 2] * inv, o[u * 8 + 3] * inv);
+        v.z = pack_bf16x2(o[u * 8 + 4] * inv, o[u * 8 + 5] * inv);
+        v.w = pack_bf16x2(o[u * 8 + 6] * inv, o[u * 8 + 7] * inv);
+        reinterpret_cast<uint4*>(dst)[u] = v;
+      }
+      a.lse[(int64_t)(b * a.H + h) * a.Npad + qi] = (l > 0.f) ? (m + __log2f(l)) * kLn2 : -INFINITY;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 256);
+  }
+}
+
+// ---------------------------------------------------------------------------------- backward
+struct BwdArgs {
+  int B, H, N, Npad;
+  float scale, scale_log2;
+  const float* lse;
+  const float* delta;
+  float* dq_acc;          // [B, N, H, 64] fp32
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  int64_t ld_g, sb_g;     // strides of dk/dv
+  int causal;
+};
+
+constexpr int B_SK = 0, B_SV = 16384, B_SQD = 32768;      // 2 stages x (Q 16K + dO 16K)
+constexpr int B_SPT = B_SQD + 2 * 32768, B_SDS = B_SPT + 32768;
+constexpr int B_SLD = B_SDS + 32768;                      // 2 stages x (lse 512 + delta 512)
+constexpr int B_BAR = B_SLD + 2 * 1024;
+constexpr int B_SMEM = B_BAR + 256 + 1024;
+
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                    const BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + B_SK;
+  uint8_t* sV = smem + B_SV;
+  uint8_t* sQD = smem + B_SQD;
+  uint8_t* sPT = smem + B_SPT;
+  uint8_t* sDS = smem + B_SDS;
+  float* sLD = reinterpret_cast<float*>(smem + B_SLD);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ds_ready = bars + 6;
+  uint64_t* mma_done = bars + 7;
+  uint64_t* dq_free = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kv0 = kt * BT;
+  const int nq_all = (a.N + BT - 1) / BT;
+  const int i0 = a.causal ? kt : 0;  // first query tile that sees this key tile
+  const int nq = nq_all - i0;
+
+  if (warp == 4 && lane == 0) {
+    tc::tma_prefetch(&tmQ);
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmV);
+    tc::tma_prefetch(&tmdO);
+    tc::mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&qd_full[s], 1);
+      tc::mbar_init(&qd_empty[s], 1);
+    }
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(ds_ready, 4);
+    tc::mbar_init(mma_done, 1);
+    tc::mbar_init(dq_free, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 5) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384;
+  const int64_t bh = (int64_t)b * a.H + h;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(kv_full, 32768);
+      tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
+      tc::tma_load_3d(sV, &tmV, kv_full, h * HD, kv0, b);
+      for (int ii = 0; ii < nq; ++ii) {
+        const int i = i0 + ii, st = ii & 1;
+        tc::mbar_wait(&qd_empty[st], ((ii >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
+        tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
+        tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
+        const float* gl = a.lse + bh * a.Npad + i * BT;
+        const float* gd = a.delta + bh * a.Npad + i * BT;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                         smem_u32(sLD + st * 256)),
+                     "l"(gl), "r"(smem_u32(&qd_full[st]))
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                         smem_u32(sLD + st * 256 + 128)),
+                     "l"(gd), "r"(smem_u32(&qd_full[st]))
+                     : "memory");
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
+      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: B (dO / Q) MN-major
+      constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aPT = smem_u32(sPT), aDS = smem_u32(sDS);
+      tc::mbar_wait(kv_full, 0);
+      for (int ii = 0; ii <= nq; ++ii) {
+        if (ii < nq) {
+          const int st = ii & 1;
+          tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);
+          if (ii > 0) tc::mbar_wait(ds_ready, (ii - 1) & 1);
+          tc::tc_fence_after();
+          const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::umma_f16_ss(tST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
+                            idSS, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::umma_f16_ss(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
+                            idSS, kk > 0);
+          tc::umma_commit(s_full);
+        } else {
+          tc::mbar_wait(ds_ready, (ii - 1) & 1);
+          tc::tc_fence_after();
+        }
+        if (ii > 0) {
+          const int ps = (ii - 1) & 1;
+          const uint32_t aQ = smem_u32(sQD + ps * 32768), aDO = aQ + 16384;
+          if (ii > 1) tc::mbar_wait(dq_free, (ii - 2) & 1);
+          tc::tc_fence_after();
+          const uint32_t acc = (ii > 1) ? 1u : 0u;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t dP = tc::sdesc_sw128(aPT + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+            tc::umma_f16_ss(tDV, dP, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t dS = tc::sdesc_sw128(aDS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+            tc::umma_f16_ss(tDK, dS, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
+            // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
+            const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
+            tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
+          }
+          tc::umma_commit(mma_done);
+          tc::umma_commit(&qd_empty[ps]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ compute warps (thread = key row)
+    const int row = warp * 32 + lane;
+    const int kvi = kv0 + row;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    for (int ii = 0; ii < nq; ++ii) {
+      const int i = i0 + ii, st = ii & 1;
+      const int q0 = i * BT;
+      tc::mbar_wait(s_full, ii & 1);
+      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // lse/delta landed (already complete for the MMA)
+      tc::tc_fence_after();
+      if (ii > 0) {
+        // drain dQ_{i-1} (thread = query row of tile i-1) and free P^T/dS^T
+        tc::mbar_wait(mma_done, (ii - 1) & 1);
+        tc::tc_fence_after();
+        const int qrow = q0 - BT + row;
+        float* dst = a.dq_acc + (((int64_t)b * a.N + qrow) * a.H + h) * HD;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(tDQ + lane_off + c * 32, r);
+          tc::tmem_ld_wait();
+          if (qrow < a.N) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c * 32 + e),
+                           "f"(__uint_as_float(r[e])), "f"(__uint_as_float(r[e + 1])), "f"(__uint_as_float(r[e + 2])),
+                           "f"(__uint_as_float(r[e + 3]))
+                           : "memory");
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(dq_free);
+      }
+      const float* sl = sLD + st * 256;
+      const float* sd = sl + 128;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rp[32];
+        tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
+        tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+        tc::tmem_ld_wait();
+        float p[32], ds[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int qc = c * 32 + e;
+          const int qi = q0 + qc;
+          const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+          const float lse2 = sl[qc] * kLog2e;
+          const float pe = ok ? ex2(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
+          p[e] = pe;
+          ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[e]) - sd[qc]) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 v, w;
+          v.x = pack_bf16x2(p[u * 8 + 0], p[u * 8 + 1]);
+          v.y = pack_bf16x2(p[u * 8 + 2], p[u * 8 + 3]);
+          v.z = pack_bf16x2(p[u * 8 + 4], p[u * 8 + 5]);
+          v.w = pack_bf16x2(p[u * 8 + 6], p[u * 8 + 7]);
+          w.x = pack_bf16x2(ds[u * 8 + 0], ds[u * 8 + 1]);
+          w.y = pack_bf16x2(ds[u * 8 + 2], ds[u * 8 + 3]);
+          w.z = pack_bf16x2(ds[u * 8 + 4], ds[u * 8 + 5]);
+          w.w = pack_bf16x2(ds[u * 8 + 6], ds[u * 8 + 7]);
+          st_sw128(sPT, row, c * 4 + u, v);
+          st_sw128(sDS, row, c * 4 + u, w);
+        }
+      }
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(ds_ready);
+    }
+    // last dQ + dK/dV out
+    tc::mbar_wait(mma_done, (nq - 1) & 1);
+    tc::tc_fence_after();
+    {
+      const int qrow = (i0 + nq - 1) * BT + row;
+      float* dst = a.dq_acc + (((int64_t)b * a.N + qrow) * a.H + h) * HD;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tDQ + lane_off + c * 32, r);
+        tc::tmem_ld_wait();
+        if (qrow < a.N) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c * 32 + e),
+                         "f"(__uint_as_float(r[e])), "f"(__uint_as_float(r[e + 1])), "f"(__uint_as_float(r[e + 2])),
+                         "f"(__uint_as_float(r[e + 3]))
+                         : "memory");
+        }
+      }
+    }
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tsrc = which ? tDK : tDV;
+      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tsrc + lane_off + c * 32, r);
+        tc::tmem_ld_wait();
+        if (kvi < a.N) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+            v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+            v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+            v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+            reinterpret_cast<uint4*>(g + c * 32)[u] = v;
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+// delta[b,h,n] = sum_d dO*O (fp32, padded rows); also zeroes the dQ accumulator rows.
+__global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o, int64_t sb_o,
+                                    const __nv_bfloat16* __restrict__ dout, int64_t ld_do, int64_t sb_do,
+                                    float* __restrict__ delta, float* __restrict__ dq_acc, int B, int H, int N, int Npad) {
+  // 8 threads per (b, n, h) row of 64 elements
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t item = gid >> 3;
+  const int sub = gid & 7;
+  const int64_t total = (int64_t)B * N * H;
+  if (item >= total) return;
+  const int h = item % H;
+  const int64_t bn = item / H;
+  const int n = bn % N;
+  const int b = bn / N;
+  const uint4 ov = *reinterpret_cast<const uint4*>(o + b * sb_o + (int64_t)n * ld_o + h * HD + sub * 8);
+  const uint4 dv = *reinterpret_cast<const uint4*>(dout + b * sb_do + (int64_t)n * ld_do + h * HD + sub * 8);
+  const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+  const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 a = __bfloat1622float2(o2[e]), c = __bfloat1622float2(d2[e]);
+    s = fmaf(a.x, c.x, fmaf(a.y, c.y, s));
+  }
+  s += __shfl_xor_sync(0xffffffff, s, 1);
+  s += __shfl_xor_sync(0xffffffff, s, 2);
+  s += __shfl_xor_sync(0xffffffff, s, 4);
+  if (sub == 0) delta[((int64_t)b * H + h) * Npad + n] = s;
+  float4* z = reinterpret_cast<float4*>(dq_acc + item * HD + sub * 8);
+  z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int64_t ld,
+                                       int64_t sb, int B, int H, int N) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one thread per 8 elements
+  const int64_t total = (int64_t)B * N * H * 8;
+  if (gid >= total) return;
+  const int sub = gid & 7;
+  const int64_t item = gid >> 3;
+  const int h = item % H;
+  const int64_t bn = item / H;
+  const int n = bn % N;
+  const int b = bn / N;
+  const float4* s = reinterpret_cast<const float4*>(dq_acc + item * HD + sub * 8);
+  const float4 x = s[0], y = s[1];
+  uint4 v;
+  v.x = pack_bf16x2(x.x, x.y);
+  v.y = pack_bf16x2(x.z, x.w);
+  v.z = pack_bf16x2(y.x, y.y);
+  v.w = pack_bf16x2(y.z, y.w);
+  *reinterpret_cast<uint4*>(dq + b * sb + (int64_t)n * ld + h * HD + sub * 8) = v;
+}
+
+int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, int64_t sb) {
+  return avb::make_tmap_3d_bf16(m, p, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)ld, (uint64_t)sb, 64, 128, 1);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb, void* o, int64_t ld_o,
+                            int64_t sb_o, float* lse, int B, int H, int N, int head_dim, float softmax_scale,
+                            int causal, void* stream) {
+  AVB_CHECK_ARG(head_dim == HD, "head_dim must be 64 (got %d)", head_dim);
+  AVB_CHECK_ARG(B >= 0 && H >= 1 && N >= 0, "bad attention dims");
+  if (B == 0 || N == 0) return AVB_OK;
+  AVB_CHECK_ARG(q && k && v && o && lse, "null pointer");
+  AVB_CHECK_ARG(aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o), "q/k/v/o must be 16-byte aligned");
+  AVB_CHECK_ARG(ld % 8 == 0 && sb % 8 == 0 && ld_o % 8 == 0, "strides must be multiples of 8 elements");
+  AVB_CHECK_ARG(ld >= (int64_t)H * HD && ld_o >= (int64_t)H * HD, "row stride smaller than H*64");
+  AVB_CHECK_ARG(B <= 65535 && H <= 65535, "B/H too large");
+  CUtensorMap mq, mk, mv;
+  int s;
+  if ((s = make_maps(&mq, q, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
+  FwdArgs a;
+  a.B = B;
+  a.H = H;
+  a.N = N;
+  a.Npad = (N + BT - 1) / BT * BT;
+  a.scale_log2 = softmax_scale * kLog2e;
+  a.o = reinterpret_cast<__nv_bfloat16*>(o);
+  a.ld_o = ld_o;
+  a.sb_o = sb_o;
+  a.lse = lse;
+  a.causal = causal;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+    if (e != cudaSuccess) return avb::cuda_status(e, "attn_fwd smem attr");
+    attr = true;
+  }
+  dim3 grid((N + BT - 1) / BT, H, B);
+  attn_fwd_kernel<<<grid, 192, F_SMEM, avb::as_stream(stream)>>>(mq, mk, mv, a);
+  return avb::launch_status("avb_attn_fwd");
+}
+
+extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb, const void* o,
+                            const void* dout, int64_t ld_o, int64_t sb_o, const float* lse, float* delta,
+                            float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g, int B, int H,
+                            int N, int head_dim, float softmax_scale, int causal, void* stream) {
+  AVB_CHECK_ARG(head_dim == HD, "head_dim must be 64 (got %d)", head_dim);
+  AVB_CHECK_ARG(B >= 0 && H >= 1 && N >= 0, "bad attention dims");
+  if (B == 0 || N == 0) return AVB_OK;
+  AVB_CHECK_ARG(q && k && v && o && dout && lse && delta && dq_acc && dq && dk && dv, "null pointer");
+  AVB_CHECK_ARG(aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && aligned16(dout) && aligned16(dq) &&
+                    aligned16(dk) && aligned16(dv) && aligned16(lse) && aligned16(delta) && aligned16(dq_acc),
+                "pointers must be 16-byte aligned");
+  AVB_CHECK_ARG(ld % 8 == 0 && sb % 8 == 0 && ld_o % 8 == 0 && sb_o % 8 == 0 && ld_g % 8 == 0 && sb_g % 8 == 0,
+                "strides must be multiples of 8 elements");
+  cudaStream_t st = avb::as_stream(stream);
+  const int Npad = (N + BT - 1) / BT * BT;
+  {
+    const int64_t threads = (int64_t)B * N * H * 8;
+    attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(o), ld_o, sb_o, reinterpret_cast<const __nv_bfloat16*>(dout), ld_o,
+        sb_o, delta, dq_acc, B, H, N, Npad);
+    int s = avb::launch_status("attn_bwd_pre");
+    if (s) return s;
+  }
+  CUtensorMap mq, mk, mv, mdo;
+  int s;
+  if ((s = make_maps(&mq, q, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mdo, dout, B, H, N, ld_o, sb_o))) return s;
+  BwdArgs a;
+  a.B = B;
+  a.H = H;
+  a.N = N;
+  a.Npad = Npad;
+  a.scale = softmax_scale;
+  a.scale_log2 = softmax_scale * kLog2e;
+  a.lse = lse;
+  a.delta = delta;
+  a.dq_acc = dq_acc;
+  a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+  a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+  a.ld_g = ld_g;
+  a.sb_g = sb_g;
+  a.causal = causal;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
+    if (e != cudaSuccess) return avb::cuda_status(e, "attn_bwd smem attr");
+    attr = true;
+  }
+  dim3 grid((N + BT - 1) / BT, H, B);
+  attn_bwd_kernel<<<grid, 192, B_SMEM, st>>>(mq, mk, mv, mdo, a);
+  if ((s = avb::launch_status("avb_attn_bwd"))) return s;
+  const int64_t threads = (int64_t)B * N * H * 8;
+  attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+      dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N);
+  return avb::launch_status("attn_dq_convert");
+}

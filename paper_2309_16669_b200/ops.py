@@ -66,3 +66,61 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
                       _lib.stream_ptr())
     _lib.check(st, "gemm")
     return out
+
+
+# ----------------------------------------------------------------------------- attention
+def _bnhd(t: torch.Tensor, name: str, H: int):
+    """Validate a [B, N, H*64] (or [B, N, H, 64]) bf16 view; return (B, N, ld, sb)."""
+    if t.dtype != torch.bfloat16 or not t.is_cuda:
+        raise InputError(f"{name} must be a bf16 CUDA tensor")
+    if t.dim() == 4:
+        if t.shape[2] != H or t.shape[3] != 64 or t.stride(3) != 1 or t.stride(2) != 64:
+            raise InputError(f"{name} must be [B,N,H,64] with contiguous heads")
+        return t.shape[0], t.shape[1], t.stride(1), t.stride(0)
+    if t.dim() != 3 or t.shape[2] != H * 64 or t.stride(2) != 1:
+        raise InputError(f"{name} must be [B,N,H*64] with unit last stride")
+    return t.shape[0], t.shape[1], t.stride(1), t.stride(0)
+
+
+def npad(N: int) -> int:
+    return (N + 127) // 128 * 128
+
+
+def attn_fwd(q, k, v, H: int, *, scale: float | None = None, causal: bool = False, out=None, lse=None):
+    """O, LSE = blockwise attention over [B,N,H,64] views (q/k/v may be slices of packed QKV)."""
+    B, N, ld, sb = _bnhd(q, "q", H)
+    for t, nm in ((k, "k"), (v, "v")):
+        if _bnhd(t, nm, H) != (B, N, ld, sb):
+            raise InputError("q, k, v must share shape and strides")
+    if out is None:
+        out = torch.empty((B, N, H * 64), dtype=torch.bfloat16, device=q.device)
+    _, _, ld_o, sb_o = _bnhd(out, "out", H)
+    if lse is None:
+        lse = torch.empty((B * H, npad(N)), dtype=torch.float32, device=q.device)
+    scale = 64 ** -0.5 if scale is None else float(scale)
+    st = _lib.load().avb_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, out.data_ptr(), ld_o, sb_o,
+                                  lse.data_ptr(), B, H, N, 64, scale, int(causal), _lib.stream_ptr())
+    _lib.check(st, "attn_fwd")
+    return out, lse
+
+
+def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causal: bool = False,
+             dq=None, dk=None, dv=None):
+    """dQ, dK, dV of blockwise attention (dq/dk/dv may be slices of one packed [B,N,3*H*64] buffer)."""
+    B, N, ld, sb = _bnhd(q, "q", H)
+    _, _, ld_o, sb_o = _bnhd(o, "o", H)
+    if _bnhd(dout, "dout", H)[2:] != (ld_o, sb_o):
+        raise InputError("o and dout must share strides")
+    if dq is None:
+        g = torch.empty((B, N, 3, H * 64), dtype=torch.bfloat16, device=q.device)
+        dq, dk, dv = g[:, :, 0], g[:, :, 1], g[:, :, 2]
+    _, _, ld_g, sb_g = _bnhd(dq, "dq", H)
+    delta = torch.empty((B * H, npad(N)), dtype=torch.float32, device=q.device)
+    dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device)
+    scale = 64 ** -0.5 if scale is None else float(scale)
+    st = _lib.load().avb_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(),
+                                  ld_o, sb_o, lse.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dq.data_ptr(),
+                                  dk.data_ptr(), dv.data_ptr(), ld_g, sb_g, B, H, N, 64, scale, int(causal),
+                                  _lib.stream_ptr())
+    _lib.check(st, "attn_bwd")
+    return dq, dk, dv

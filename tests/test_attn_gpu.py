@@ -1,0 +1,77 @@
+"""Blockwise attention (K4/K5) vs a torch fp32 reference of the same op on identical bf16 inputs.
+
+Tolerance (north_star): bf16 outputs/gradients within 2e-2 norm-relative of fp32; LSE within 1e-3 abs.
+"""
+
+import math
+
+import pytest
+import torch
+
+from paper_2309_16669_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+def ref_attn(q, k, v, scale, causal):
+    # q,k,v [B,N,H,64] -> fp32 math
+    qf, kf, vf = (t.float().permute(0, 2, 1, 3) for t in (q, k, v))
+    s = qf @ kf.transpose(-1, -2) * scale
+    if causal:
+        N = s.shape[-1]
+        s = s.masked_fill(torch.ones(N, N, dtype=torch.bool, device=s.device).triu(1), float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ vf
+    return o.permute(0, 2, 1, 3), lse
+
+
+def packed(B, N, H, seed=0, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(B, N, 3, H, 64, generator=g, device="cuda") * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("B,N,H", [(1, 128, 1), (2, 197, 3), (2, 785, 2), (1, 1569, 2), (1, 2049, 1), (3, 77, 2),
+                                   (1, 1, 1)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fwd(B, N, H, causal):
+    qkv = packed(B, N, H, seed=N + H)
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    o, lse = ops.attn_fwd(q.reshape(B, N, H * 64), k.reshape(B, N, H * 64), v.reshape(B, N, H * 64), H,
+                          causal=causal)
+    ro, rlse = ref_attn(q, k, v, 0.125, causal)
+    assert rel(o.view(B, N, H, 64), ro) < 2e-2
+    got = lse.view(B, H, -1)[:, :, :N]
+    assert (got - rlse).abs().max().item() < 1e-3
+
+
+def test_fwd_packed_qkv_view():
+    # q/k/v as strided slices of the QKV GEMM output [B*N, 3*H*64]
+    B, N, H = 2, 1569, 12
+    D = H * 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = torch.randn(B, N, 3 * D, generator=g, device="cuda").to(torch.bfloat16)
+    o, _ = ops.attn_fwd(qkv[:, :, :D], qkv[:, :, D:2 * D], qkv[:, :, 2 * D:], H)
+    q, k, v = (qkv[:, :, i * D:(i + 1) * D].reshape(B, N, H, 64) for i in range(3))
+    ro, _ = ref_attn(q, k, v, 0.125, False)
+    assert rel(o.view(B, N, H, 64), ro) < 2e-2
+
+
+@pytest.mark.parametrize("B,N,H", [(1, 128, 1), (2, 197, 3), (1, 785, 2), (1, 1569, 2), (2, 300, 1)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_bwd(B, N, H, causal):
+    qkv = packed(B, N, H, seed=7 + N)
+    q, k, v = (qkv[:, :, i].contiguous() for i in range(3))
+    D = H * 64
+    o, lse = ops.attn_fwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), H, causal=causal)
+    g = torch.Generator(device="cuda").manual_seed(99)
+    do = torch.randn(B, N, D, generator=g, device="cuda").to(torch.bfloat16)
+    dq, dk, dv = ops.attn_bwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), o, do, lse, H, causal=causal)
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    ro, _ = ref_attn(qf, kf, vf, 0.125, causal)
+    ro.backward(do.float().view(B, N, H, 64))
+    for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
+        assert rel(got.reshape(B, N, H, 64), ref) < 2e-2
