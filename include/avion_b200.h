@@ -51,6 +51,7 @@ extern "C" {
 
 #define AVB_LAYOUT_CTHW    0  /* dst [B,3,T,Ht,Wt]  (encoder input)            */
 #define AVB_LAYOUT_TCHW    1  /* dst [B,T,3,Ht,Wt]  (reference Batch.frames)   */
+#define AVB_LAYOUT_TUBELET 2  /* dst [B*Np, 3*tt*ph*pw] patch-embed GEMM rows     */
 
 /* GEMM epilogues (avb_gemm) */
 #define AVB_EPI_BF16       0  /* C bf16 = alpha*acc (+bias) (+aux residual)                 */
@@ -84,6 +85,16 @@ int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, int W,
                       const int32_t* boxes_host, int Ht, int Wt,
                       const float* mean3, const float* inv_std3,
                       int out_dtype, int out_layout, void* dst, void* stream);
+
+/* K1 writing straight into the tubelet patch-embed operand: row n' = ((t/tt)*(Ht/ph) + y/ph)*(Wt/pw)
+ * + x/pw of clip b, feature ((c*tt + t%tt)*ph + y%ph)*pw + x%pw (Conv3d weight flattening), so the
+ * K2 GEMM reads it with no im2col pass.  tub_w must be even. */
+int avb_rrc_normalize_tubelet(const uint8_t* src, int64_t B, int T, int H, int W,
+                              int64_t s_clip, int64_t s_t, int64_t s_h, int64_t s_w, int64_t s_c,
+                              const int32_t* boxes_dev, const uint8_t* hflip_dev,
+                              const int32_t* boxes_host, int Ht, int Wt,
+                              const float* mean3, const float* inv_std3, int out_dtype,
+                              int tub_t, int tub_h, int tub_w, void* dst, void* stream);
 
 /* Test hook: the device-computed tap table for one (crop, target) pair:
  * lo[tgt], hi[tgt] int32 device, weights[tgt*max_taps] float device. */
@@ -124,6 +135,34 @@ int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_
                  const void* o, const void* dout, int64_t ld_o, int64_t sb_o, const float* lse,
                  float* delta, float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g,
                  int B, int H, int N, int head_dim, float softmax_scale, int causal, void* stream);
+
+/* K6: LayerNorm over rows of D (<= 1024, multiple of 8) bf16 elements, fp32 gamma/beta/stats. */
+int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma, const float* beta, void* y,
+                      int64_t ldy, float* mean, float* rstd, int M, int D, float eps, void* stream);
+/* dx (=|+=) LN'(dy); dgamma/dbeta (nullable) += column reductions. */
+int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, int64_t ldx, const float* gamma,
+                      const float* mean, const float* rstd, void* dx, int64_t lddx, float* dgamma,
+                      float* dbeta, int M, int D, int accumulate, void* stream);
+
+/* out[n] += sum_m X[m,n] (bias gradients); X bf16 [M, ldx]. */
+int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void* stream);
+
+/* tokens: x[b,0] = cls + pos[0]; x[b,1+n] = pe[b*Np+n] + pos[1+n]   (bf16 x, fp32 cls/pos) */
+int avb_tokens_fwd(const void* pe, const float* cls, const float* pos, void* x, int B, int Np, int D,
+                   void* stream);
+/* dpe = dx[:,1:] (nullable); dpos += sum_b dx; dcls += sum_b dx[:,0] */
+int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos, int B, int Np, int D, void* stream);
+
+/* softmax cross-entropy: loss += scale*sum_i (lse_i - z_i[y_i]); dlogits bf16 = scale*(softmax - onehot) */
+int avb_xent(const float* logits, int64_t ld, const int32_t* labels, int B, int C, float scale, float* loss,
+             void* dlogits, int64_t ldd, void* stream);
+
+/* K8: AdamW with decoupled weight decay over a flat fp32 buffer; optional bf16 shadow copy;
+ * decay_mask (nullable, uint8 per element) selects which elements get weight decay. */
+int avb_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask, int64_t n, float lr,
+              float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
+              void* stream);
+int avb_cast_bf16(const float* src, void* dst, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

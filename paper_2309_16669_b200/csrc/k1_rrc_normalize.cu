@@ -41,6 +41,7 @@ struct K1Params {
   int rows_cap;   // staged source rows capacity
   int rowb_cap;   // staged bytes per row (multiple of 16)
   int fast;       // interleaved RGB (s_c == 1, s_w == 3)
+  int tt, tph, tpw;  // tubelet (AVB_LAYOUT_TUBELET)
 };
 
 // Exact-integer tap range + fp64 tent weights (torch/PIL antialias rule).
@@ -230,10 +231,21 @@ __global__ void __launch_bounds__(kThreads) k1_rrc_normalize_kernel(const K1Para
       y[e] = fmaf(acc, p.scale[c], p.bias[c]);
     }
     int64_t o;
-    if (p.out_layout == AVB_LAYOUT_CTHW)
+    if (p.out_layout == AVB_LAYOUT_CTHW) {
       o = ((b * 3 + c) * p.T + t) * plane + (int64_t)(i0 + r) * p.Wt + j;
-    else
+    } else if (p.out_layout == AVB_LAYOUT_TCHW) {
       o = ((b * p.T + t) * 3 + c) * plane + (int64_t)(i0 + r) * p.Wt + j;
+    } else {
+      // tubelet rows: patch n' = ((t/tt)*(Ht/ph) + y/ph)*(Wt/pw) + x/pw, feature
+      // f = ((c*tt + t%tt)*ph + y%ph)*pw + x%pw  (Conv3d weight [D,3,tt,ph,pw] flattening)
+      const int y = i0 + r;
+      const int npy = p.Ht / p.tph, npx = p.Wt / p.tpw;
+      const int64_t Np = (int64_t)(p.T / p.tt) * npy * npx;
+      const int F = 3 * p.tt * p.tph * p.tpw;
+      const int64_t n = ((int64_t)(t / p.tt) * npy + y / p.tph) * npx + j / p.tpw;
+      const int f = ((c * p.tt + t % p.tt) * p.tph + y % p.tph) * p.tpw + j % p.tpw;
+      o = (b * Np + n) * F + f;
+    }
     if (p.out_dtype == AVB_DTYPE_BF16) {
       __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.dst) + o;
       if (pair_ok) {
@@ -266,18 +278,20 @@ extern "C" int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev,
   return avb::launch_status("avb_rrc_taps");
 }
 
-extern "C" int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, int W, int64_t s_clip,
-                                 int64_t s_t, int64_t s_h, int64_t s_w, int64_t s_c,
-                                 const int32_t* boxes_dev, const uint8_t* hflip_dev,
-                                 const int32_t* boxes_host, int Ht, int Wt, const float* mean3,
-                                 const float* inv_std3, int out_dtype, int out_layout, void* dst,
-                                 void* stream) {
+static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W, int64_t s_clip, int64_t s_t,
+                              int64_t s_h, int64_t s_w, int64_t s_c, const int32_t* boxes_dev,
+                              const uint8_t* hflip_dev, const int32_t* boxes_host, int Ht, int Wt,
+                              const float* mean3, const float* inv_std3, int out_dtype, int out_layout, int tt,
+                              int tph, int tpw, void* dst, void* stream) {
   AVB_CHECK_ARG(B >= 0 && T >= 1 && H >= 1 && W >= 1, "bad frame dims B=%lld T=%d H=%d W=%d",
                 (long long)B, T, H, W);
   AVB_CHECK_ARG(Ht >= 1 && Wt >= 1, "target size must be >= 1 pixel");
   AVB_CHECK_ARG(out_dtype == AVB_DTYPE_BF16 || out_dtype == AVB_DTYPE_F32, "bad out_dtype %d", out_dtype);
-  AVB_CHECK_ARG(out_layout == AVB_LAYOUT_CTHW || out_layout == AVB_LAYOUT_TCHW, "bad out_layout %d",
-                out_layout);
+  AVB_CHECK_ARG(out_layout == AVB_LAYOUT_CTHW || out_layout == AVB_LAYOUT_TCHW || out_layout == AVB_LAYOUT_TUBELET,
+                "bad out_layout %d", out_layout);
+  if (out_layout == AVB_LAYOUT_TUBELET)
+    AVB_CHECK_ARG(tt >= 1 && tph >= 1 && tpw >= 2 && tpw % 2 == 0 && T % tt == 0 && Ht % tph == 0 && Wt % tpw == 0,
+                  "tubelet %dx%dx%d must tile %dx%dx%d with an even width", tt, tph, tpw, T, Ht, Wt);
   AVB_CHECK_ARG(mean3 && inv_std3, "mean/inv_std must be given");
   if (B == 0) return AVB_OK;
   AVB_CHECK_ARG(src && boxes_dev && dst, "null device pointer");
@@ -310,6 +324,7 @@ extern "C" int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, in
     p.bias[c] = -mean3[c] * inv_std3[c];
   }
   p.dst = dst; p.out_dtype = out_dtype; p.out_layout = out_layout;
+  p.tt = tt; p.tph = tph; p.tpw = tpw;
   p.tx_cap = tx_cap; p.ty_cap = ty_cap;
   p.rowb_cap = ((3 * W + 15) / 16) * 16 + 16;
   p.fast = (s_c == 1 && s_w == 3) ? 1 : 0;
@@ -338,4 +353,24 @@ extern "C" int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, in
   AVB_CHECK_ARG(B <= 65535 && T <= 65535, "B and T must be <= 65535");
   k1_rrc_normalize_kernel<<<grid, kThreads, smem, avb::as_stream(stream)>>>(p);
   return avb::launch_status("avb_rrc_normalize");
+}
+
+extern "C" int avb_rrc_normalize(const uint8_t* src, int64_t B, int T, int H, int W, int64_t s_clip, int64_t s_t,
+                                 int64_t s_h, int64_t s_w, int64_t s_c, const int32_t* boxes_dev,
+                                 const uint8_t* hflip_dev, const int32_t* boxes_host, int Ht, int Wt,
+                                 const float* mean3, const float* inv_std3, int out_dtype, int out_layout, void* dst,
+                                 void* stream) {
+  AVB_CHECK_ARG(out_layout != AVB_LAYOUT_TUBELET, "use avb_rrc_normalize_tubelet for the tubelet layout");
+  return rrc_normalize_impl(src, B, T, H, W, s_clip, s_t, s_h, s_w, s_c, boxes_dev, hflip_dev, boxes_host, Ht, Wt,
+                            mean3, inv_std3, out_dtype, out_layout, 1, 1, 2, dst, stream);
+}
+
+extern "C" int avb_rrc_normalize_tubelet(const uint8_t* src, int64_t B, int T, int H, int W, int64_t s_clip,
+                                         int64_t s_t, int64_t s_h, int64_t s_w, int64_t s_c,
+                                         const int32_t* boxes_dev, const uint8_t* hflip_dev,
+                                         const int32_t* boxes_host, int Ht, int Wt, const float* mean3,
+                                         const float* inv_std3, int out_dtype, int tub_t, int tub_h, int tub_w,
+                                         void* dst, void* stream) {
+  return rrc_normalize_impl(src, B, T, H, W, s_clip, s_t, s_h, s_w, s_c, boxes_dev, hflip_dev, boxes_host, Ht, Wt,
+                            mean3, inv_std3, out_dtype, AVB_LAYOUT_TUBELET, tub_t, tub_h, tub_w, dst, stream);
 }

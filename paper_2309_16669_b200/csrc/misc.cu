@@ -1,0 +1,223 @@
+// Supporting kernels of the training step (all HBM/latency-bound, no reference code):
+//   bias-gradient column sums, token assembly (cls + pos-embed),
+//   softmax cross-entropy head loss (fine-tune), fused AdamW (K8).
+#include "common.cuh"
+
+#include <algorithm>
+
+namespace {
+
+__device__ __forceinline__ void ld8f(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 v = __bfloat1622float2(h[e]);
+    f[2 * e] = v.x;
+    f[2 * e + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void st8f(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 q;
+  q.x = pack_bf16x2(f[0], f[1]);
+  q.y = pack_bf16x2(f[2], f[3]);
+  q.z = pack_bf16x2(f[4], f[5]);
+  q.w = pack_bf16x2(f[6], f[7]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+// out[n] += sum_m X[m, n]; block (64, 4): 64 column-octets x 4 row lanes
+__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t ldx, int M, int N, float* __restrict__ out) {
+  __shared__ float red[4][64 * 8 + 4];
+  const int c8 = blockIdx.x * 64 + threadIdx.x;
+  const int col = c8 * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (col < N) {
+    for (int64_t r = (int64_t)blockIdx.y * 4 + threadIdx.y; r < M; r += (int64_t)gridDim.y * 4) {
+      float f[8];
+      ld8f(X + r * ldx + col, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[threadIdx.y][threadIdx.x * 8 + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.y == 0 && col < N) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      atomicAdd(out + col + e, red[0][threadIdx.x * 8 + e] + red[1][threadIdx.x * 8 + e] + red[2][threadIdx.x * 8 + e] +
+                                   red[3][threadIdx.x * 8 + e]);
+  }
+}
+
+// x[b, 0] = cls + pos[0];  x[b, 1+n] = pe[b*Np + n] + pos[1+n]
+__global__ void tokens_fwd_kernel(const __nv_bfloat16* __restrict__ pe, const float* __restrict__ cls,
+                                  const float* __restrict__ pos, __nv_bfloat16* __restrict__ x, int B, int Np, int D) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per_row = D / 8;
+  const int64_t total = (int64_t)B * (Np + 1) * per_row;
+  if (gid >= total) return;
+  const int c = (gid % per_row) * 8;
+  const int64_t tok = gid / per_row;
+  const int t = tok % (Np + 1);
+  const int b = tok / (Np + 1);
+  float f[8];
+  if (t == 0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = cls[c + e] + pos[c + e];
+  } else {
+    ld8f(pe + ((int64_t)b * Np + t - 1) * D + c, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] += pos[(int64_t)t * D + c + e];
+  }
+  st8f(x + tok * D + c, f);
+}
+
+// dpe = dx[:, 1:];  dpos[t] += sum_b dx[b, t];  dcls += sum_b dx[b, 0]
+__global__ void tokens_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_bfloat16* __restrict__ dpe,
+                                  float* __restrict__ dcls, float* __restrict__ dpos, int B, int Np, int D) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per_row = D / 8;
+  const int64_t total = (int64_t)(Np + 1) * per_row;
+  if (gid >= total) return;
+  const int c = (gid % per_row) * 8;
+  const int t = gid / per_row;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < B; ++b) {
+    float f[8];
+    const int64_t tok = (int64_t)b * (Np + 1) + t;
+    ld8f(dx + tok * D + c, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    if (t > 0 && dpe) st8f(dpe + ((int64_t)b * Np + t - 1) * D + c, f);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (dpos) dpos[(int64_t)t * D + c + e] += acc[e];
+    if (t == 0 && dcls) dcls[c + e] += acc[e];
+  }
+}
+
+// one block per row: loss += scale * (lse - z[y]);  dlogits = scale * (softmax - onehot)
+__global__ void xent_kernel(const float* __restrict__ logits, int64_t ld, const int32_t* __restrict__ labels, int C,
+                            float scale, float* __restrict__ loss, __nv_bfloat16* __restrict__ dlogits, int64_t ldd) {
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  const float* z = logits + (int64_t)row * ld;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) mx = fmaxf(mx, z[j]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, sh[w]);
+  __syncthreads();
+  float s = 0.f;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) s += __expf(z[j] - mx);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+  const float lse = mx + __logf(s);
+  const int y = labels[row];
+  if (threadIdx.x == 0) atomicAdd(loss, scale * (lse - z[y]));
+  if (dlogits) {
+    for (int j = threadIdx.x; j < C; j += blockDim.x) {
+      const float p = __expf(z[j] - lse) - (j == y ? 1.f : 0.f);
+      dlogits[(int64_t)row * ldd + j] = __float2bfloat16_rn(scale * p);
+    }
+  }
+}
+
+// AdamW (decoupled weight decay), bias-corrected; optional bf16 shadow of the updated weights
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, __nv_bfloat16* __restrict__ pb, const uint8_t* __restrict__ mask,
+                             int64_t n, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                             float gscale) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i] * gscale;
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float wdi = (mask == nullptr || mask[i]) ? wd : 0.f;
+    float pi = p[i] * (1.f - lr * wdi);
+    pi -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    p[i] = pi;
+    if (pb) pb[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+}  // namespace
+
+extern "C" int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void* stream) {
+  AVB_CHECK_ARG(M >= 0 && N >= 0 && N % 8 == 0 && ldx % 8 == 0, "colsum needs N and ldx multiples of 8");
+  if (M == 0 || N == 0) return AVB_OK;
+  AVB_CHECK_ARG(X && out, "null pointer");
+  dim3 block(64, 4);
+  const int gx = (N / 8 + 63) / 64;
+  const int gy = std::max(1, std::min((M + 3) / 4, avb::sm_count() * 8 / gx));
+  colsum_kernel<<<dim3(gx, gy), block, 0, avb::as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(X), ldx, M,
+                                                                      N, out);
+  return avb::launch_status("avb_colsum_accum");
+}
+
+extern "C" int avb_tokens_fwd(const void* pe, const float* cls, const float* pos, void* x, int B, int Np, int D,
+                              void* stream) {
+  AVB_CHECK_ARG(B >= 0 && Np >= 0 && D % 8 == 0, "tokens: D must be a multiple of 8");
+  if (B == 0) return AVB_OK;
+  AVB_CHECK_ARG(pe && cls && pos && x, "null pointer");
+  const int64_t total = (int64_t)B * (Np + 1) * (D / 8);
+  tokens_fwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(pe), cls, pos, reinterpret_cast<__nv_bfloat16*>(x), B, Np, D);
+  return avb::launch_status("avb_tokens_fwd");
+}
+
+extern "C" int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos, int B, int Np, int D, void* stream) {
+  AVB_CHECK_ARG(B >= 0 && Np >= 0 && D % 8 == 0, "tokens: D must be a multiple of 8");
+  if (B == 0) return AVB_OK;
+  AVB_CHECK_ARG(dx, "null pointer");
+  const int64_t total = (int64_t)(Np + 1) * (D / 8);
+  tokens_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(dx), reinterpret_cast<__nv_bfloat16*>(dpe), dcls, dpos, B, Np, D);
+  return avb::launch_status("avb_tokens_bwd");
+}
+
+extern "C" int avb_xent(const float* logits, int64_t ld, const int32_t* labels, int B, int C, float scale, float* loss,
+                        void* dlogits, int64_t ldd, void* stream) {
+  AVB_CHECK_ARG(B >= 0 && C >= 1 && ld >= C, "bad xent dims");
+  if (B == 0) return AVB_OK;
+  AVB_CHECK_ARG(logits && labels && loss, "null pointer");
+  xent_kernel<<<B, 256, 0, avb::as_stream(stream)>>>(logits, ld, labels, C, scale, loss,
+                                                     reinterpret_cast<__nv_bfloat16*>(dlogits), ldd);
+  return avb::launch_status("avb_xent");
+}
+
+extern "C" int avb_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask,
+                         int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                         float grad_scale, void* stream) {
+  AVB_CHECK_ARG(n >= 0 && step >= 1, "adamw: n >= 0, step >= 1");
+  if (n == 0) return AVB_OK;
+  AVB_CHECK_ARG(p && g && m && v, "null pointer");
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)avb::sm_count() * 8);
+  adamw_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(p, g, m, v, reinterpret_cast<__nv_bfloat16*>(p_bf16), decay_mask, n, lr,
+                                                           beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
+  return avb::launch_status("avb_adamw");
+}
+
+extern "C" int avb_cast_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  AVB_CHECK_ARG(n >= 0, "n >= 0");
+  if (n == 0) return AVB_OK;
+  AVB_CHECK_ARG(src && dst, "null pointer");
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)avb::sm_count() * 8);
+  cast_bf16_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(src, reinterpret_cast<__nv_bfloat16*>(dst), n);
+  return avb::launch_status("avb_cast_bf16");
+}

@@ -124,3 +124,64 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
                                   _lib.stream_ptr())
     _lib.check(st, "attn_bwd")
     return dq, dk, dv
+
+
+# ----------------------------------------------------------------------------- LayerNorm / misc
+def layernorm_fwd(x, gamma, beta, eps=1e-5, out=None, mean=None, rstd=None):
+    M, D = x.shape
+    out = torch.empty_like(x) if out is None else out
+    mean = torch.empty(M, dtype=torch.float32, device=x.device) if mean is None else mean
+    rstd = torch.empty(M, dtype=torch.float32, device=x.device) if rstd is None else rstd
+    st = _lib.load().avb_layernorm_fwd(x.data_ptr(), _rowmajor(x, "x"), gamma.data_ptr(), beta.data_ptr(),
+                                       out.data_ptr(), _rowmajor(out, "out"), mean.data_ptr(), rstd.data_ptr(), M, D,
+                                       float(eps), _lib.stream_ptr())
+    _lib.check(st, "layernorm_fwd")
+    return out, mean, rstd
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma=None, dbeta=None, accumulate=False):
+    M, D = x.shape
+    st = _lib.load().avb_layernorm_bwd(dy.data_ptr(), _rowmajor(dy, "dy"), x.data_ptr(), _rowmajor(x, "x"),
+                                       gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+                                       _rowmajor(dx, "dx"), _ptr(dgamma), _ptr(dbeta), M, D, int(accumulate),
+                                       _lib.stream_ptr())
+    _lib.check(st, "layernorm_bwd")
+    return dx
+
+
+def colsum_accum(x, out):
+    M, N = x.shape
+    _lib.check(_lib.load().avb_colsum_accum(x.data_ptr(), _rowmajor(x, "x"), M, N, out.data_ptr(), _lib.stream_ptr()),
+               "colsum_accum")
+    return out
+
+
+def tokens_fwd(pe, cls, pos, B, Np, out):
+    D = pe.shape[-1]
+    _lib.check(_lib.load().avb_tokens_fwd(pe.data_ptr(), cls.data_ptr(), pos.data_ptr(), out.data_ptr(), B, Np, D,
+                                          _lib.stream_ptr()), "tokens_fwd")
+    return out
+
+
+def tokens_bwd(dx, dpe, dcls, dpos, B, Np):
+    D = dx.shape[-1]
+    _lib.check(_lib.load().avb_tokens_bwd(dx.data_ptr(), _ptr(dpe), _ptr(dcls), _ptr(dpos), B, Np, D,
+                                          _lib.stream_ptr()), "tokens_bwd")
+
+
+def xent(logits, labels, scale, loss, dlogits=None):
+    B, C = logits.shape
+    ldd = dlogits.stride(0) if dlogits is not None else 0
+    _lib.check(_lib.load().avb_xent(logits.data_ptr(), logits.stride(0), labels.data_ptr(), B, C, float(scale),
+                                    loss.data_ptr(), _ptr(dlogits), ldd, _lib.stream_ptr()), "xent")
+
+
+def adamw(p, g, m, v, p_bf16, lr, beta1, beta2, eps, wd, step, grad_scale=1.0, decay_mask=None):
+    _lib.check(_lib.load().avb_adamw(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(p_bf16),
+                                     _ptr(decay_mask), p.numel(),
+                                     float(lr), float(beta1), float(beta2), float(eps), float(wd), int(step),
+                                     float(grad_scale), _lib.stream_ptr()), "adamw")
+
+
+def cast_bf16(src, dst):
+    _lib.check(_lib.load().avb_cast_bf16(src.data_ptr(), dst.data_ptr(), src.numel(), _lib.stream_ptr()), "cast_bf16")

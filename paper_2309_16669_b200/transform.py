@@ -26,7 +26,7 @@ CLIP_MEAN = (0.48145466, 0.4578275, 0.40821073)
 CLIP_STD = (0.26862954, 0.26130258, 0.27577711)
 
 _DT = {torch.bfloat16: _lib.AVB_DTYPE_BF16, torch.float32: _lib.AVB_DTYPE_F32}
-_LAYOUT = {"cthw": _lib.AVB_LAYOUT_CTHW, "tchw": _lib.AVB_LAYOUT_TCHW}
+_LAYOUT = {"cthw": _lib.AVB_LAYOUT_CTHW, "tchw": _lib.AVB_LAYOUT_TCHW, "tubelet": _lib.AVB_LAYOUT_TUBELET}
 
 
 def _boxes_to_host(crops) -> np.ndarray:
@@ -37,15 +37,19 @@ def _boxes_to_host(crops) -> np.ndarray:
     return np.asarray(crops, dtype=np.int32).reshape(-1, 4)
 
 
-def output_shape(B: int, T: int, target: tuple[int, int], layout: str) -> tuple[int, ...]:
+def output_shape(B: int, T: int, target: tuple[int, int], layout: str, tubelet=(2, 16, 16)) -> tuple[int, ...]:
     Ht, Wt = target
+    if layout == "tubelet":
+        tt, ph, pw = tubelet
+        return (B * (T // tt) * (Ht // ph) * (Wt // pw), 3 * tt * ph * pw)
     return (B, 3, T, Ht, Wt) if layout == "cthw" else (B, T, 3, Ht, Wt)
 
 
 def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] = (224, 224),
               mean: Sequence[float] = CLIP_MEAN, std: Sequence[float] = CLIP_STD, *,
               out: torch.Tensor | None = None, out_dtype: torch.dtype = torch.bfloat16,
-              layout: str = "cthw", channels_last: bool = True, validate: bool = True) -> torch.Tensor:
+              layout: str = "cthw", channels_last: bool = True, validate: bool = True,
+              tubelet: tuple[int, int, int] = (2, 16, 16)) -> torch.Tensor:
     """Crop -> hflip -> antialiased bilinear -> normalize -> cast, on the GPU.
 
     frames:  uint8 CUDA tensor, [B,T,H,W,3] (channels_last, decoded RGB24) or
@@ -58,7 +62,8 @@ def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] =
     validate: check every box on the host first (needs a host copy of the boxes;
              pass False inside CUDA-graph capture with device boxes -- the kernel
              still skips out-of-frame boxes).
-    Returns `out` (layout "cthw" = [B,3,T,Ht,Wt] encoder input; "tchw" = [B,T,3,Ht,Wt]).
+    Returns `out` (layout "cthw" = [B,3,T,Ht,Wt]; "tchw" = [B,T,3,Ht,Wt]; "tubelet" = the
+    patch-embed GEMM operand [B*Np, 3*tt*ph*pw] for `tubelet=(tt, ph, pw)`).
     """
     if not isinstance(frames, torch.Tensor) or frames.dtype != torch.uint8:
         raise InputError("frames must be a uint8 torch tensor")
@@ -104,7 +109,7 @@ def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] =
     if flips_dev is not None and flips_dev.numel() != B:
         raise InputError(f"need one flip per clip: {flips_dev.numel()} for {B} clips")
 
-    shape = output_shape(B, T, (Ht, Wt), layout)
+    shape = output_shape(B, T, (Ht, Wt), layout, tubelet)
     if out is None:
         out = torch.empty(shape, dtype=out_dtype, device=dev)
     elif tuple(out.shape) != shape or out.dtype != out_dtype or not out.is_contiguous() or out.device != dev:
@@ -114,12 +119,19 @@ def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] =
     bh = np.ascontiguousarray(boxes_host, dtype=np.int32) if boxes_host is not None else None
     inv_std = [1.0 / float(s) for s in std]
     lib = _lib.load()
+    fl = flips_dev.data_ptr() if flips_dev is not None else None
+    bhp = bh.ctypes.data if bh is not None else None
     with torch.cuda.device(dev):
-        st = lib.avb_rrc_normalize(
-            frames.data_ptr(), B, T, H, W, s_clip, s_t, s_h, s_w, s_c,
-            boxes_dev.data_ptr(), flips_dev.data_ptr() if flips_dev is not None else None,
-            bh.ctypes.data if bh is not None else None, Ht, Wt, _lib.f32x3(mean), _lib.f32x3(inv_std),
-            _DT[out_dtype], _LAYOUT[layout], out.data_ptr(), _lib.stream_ptr())
+        if layout == "tubelet":
+            st = lib.avb_rrc_normalize_tubelet(
+                frames.data_ptr(), B, T, H, W, s_clip, s_t, s_h, s_w, s_c, boxes_dev.data_ptr(), fl, bhp, Ht, Wt,
+                _lib.f32x3(mean), _lib.f32x3(inv_std), _DT[out_dtype], int(tubelet[0]), int(tubelet[1]),
+                int(tubelet[2]), out.data_ptr(), _lib.stream_ptr())
+        else:
+            st = lib.avb_rrc_normalize(
+                frames.data_ptr(), B, T, H, W, s_clip, s_t, s_h, s_w, s_c, boxes_dev.data_ptr(), fl, bhp, Ht, Wt,
+                _lib.f32x3(mean), _lib.f32x3(inv_std), _DT[out_dtype], _LAYOUT[layout], out.data_ptr(),
+                _lib.stream_ptr())
     _lib.check(st, "transform")
     return out
 

@@ -26,7 +26,13 @@ def mk(*shape, seed=0):
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 208, 136), (1024, 768, 768), (264, 3072, 768),
                                    (1569, 2304, 768), (128, 128, 1536)])
 def test_gemm_layouts(a_mn, b_mn, M, N, K):
+    from paper_2309_16669_b200.errors import InputError
     A = mk(K, M, seed=1) if a_mn else mk(M, K, seed=1)
+    if (a_mn and M % 8) or (b_mn and N % 8):
+        B = mk(K, N, seed=2) if b_mn else mk(N, K, seed=2)
+        with pytest.raises(InputError):   # leading dims must be 16-byte multiples (TMA)
+            ops.gemm(A, B, a_mn=a_mn, b_mn=b_mn)
+        return
     B = mk(K, N, seed=2) if b_mn else mk(N, K, seed=2)
     Af = A.float().t() if a_mn else A.float()
     Bf = B.float() if b_mn else B.float().t()

@@ -1,0 +1,115 @@
+"""Encoder + head + loss + gradients on the GPU kernels vs the fp32 torch oracle (oracle/vit_oracle.py).
+
+Same inputs (patch rows), same fp32 master weights.  Tolerance (north_star): loss,
+outputs and every parameter gradient within 2e-2 norm-relative of fp32.
+"""
+
+import pytest
+import torch
+
+from oracle import vit_oracle as VO
+from paper_2309_16669_b200 import ops
+from paper_2309_16669_b200.vit import CONFIG1_TINY, FineTuneModel, VitConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return ((a.float().cpu() - b.float().cpu()).norm() / b.float().cpu().norm().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("cfg,B,C", [(VitConfig(frames=4, height=64, width=64, cube_t=2, depth=2, dim=128, heads=2), 3, 10),
+                                     (CONFIG1_TINY, 4, 400)])
+def test_finetune_step_matches_oracle(cfg, B, C):
+    torch.manual_seed(0)
+    model = FineTuneModel(cfg, num_classes=C, seed=1)
+    # make every parameter non-trivial (biases / LN / cls start at constants)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    model.store.data.add_(torch.randn(model.store.n, generator=g, device="cuda") * 0.02)
+    ops.cast_bf16(model.store.data, model.store.shadow)
+    patches = torch.randn(B * cfg.patches, cfg.patch_dim, generator=g, device="cuda").to(torch.bfloat16)
+    labels = torch.randint(0, C, (B,), generator=g, device="cuda", dtype=torch.int32)
+    loss = torch.zeros(1, device="cuda")
+    model.zero_grad()
+    model.forward_backward(patches, labels, B, loss)
+    torch.cuda.synchronize()
+
+    names = [s[0] for s in model.store.specs]
+    P = {n: model.store.p(n).detach().cpu().clone().requires_grad_(True) for n in names}
+    x = VO.encoder_forward(P, patches.float().cpu(), cfg, B)
+    ref_loss, _ = VO.head_loss(P, x, B, cfg.tokens, labels.cpu(), C)
+    ref_loss.backward()
+    assert abs(loss.item() - ref_loss.item()) / abs(ref_loss.item()) < 2e-2
+    bad = []
+    for n in names:
+        ref = P[n].grad
+        if ref is None or ref.norm() < 1e-12:
+            continue
+        got = model.store.g(n)
+        if n == "head.w" or n == "head.b":
+            got, ref = got[:C], ref[:C]
+        r = rel(got, ref)
+        if r > 2e-2:
+            bad.append((n, r))
+    assert not bad, bad
+
+
+def test_adamw_kernel_matches_torch():
+    n = 10_000
+    g0 = torch.Generator(device="cuda").manual_seed(3)
+    p = torch.randn(n, device="cuda", generator=g0)
+    grads = [torch.randn(n, device="cuda", generator=g0) for _ in range(3)]
+    m, v = torch.zeros_like(p), torch.zeros_like(p)
+    sh = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    mask = (torch.arange(n, device="cuda") % 3 != 0).to(torch.uint8)
+    tp_d = p.clone().requires_grad_(True)
+    tp_n = p.clone().requires_grad_(True)
+    opt = torch.optim.AdamW([{"params": [tp_d], "weight_decay": 0.01}, {"params": [tp_n], "weight_decay": 0.0}],
+                            lr=1e-3, betas=(0.9, 0.999), eps=1e-8)
+    for i, gr in enumerate(grads):
+        ops.adamw(p, gr, m, v, sh, 1e-3, 0.9, 0.999, 1e-8, 0.01, i + 1, decay_mask=mask)
+        tp_d.grad, tp_n.grad = gr.clone(), gr.clone()
+        opt.step()
+    ref = torch.where(mask.bool(), tp_d.detach(), tp_n.detach())
+    assert (p - ref).abs().max().item() < 1e-6
+    assert torch.equal(sh, p.to(torch.bfloat16))
+
+
+def test_layernorm_and_colsum():
+    M, D = 1000, 768
+    g0 = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(M, D, device="cuda", generator=g0).to(torch.bfloat16)
+    gam = torch.randn(D, device="cuda", generator=g0)
+    bet = torch.randn(D, device="cuda", generator=g0)
+    y, mu, rs = ops.layernorm_fwd(x, gam, bet)
+    xf = x.float().requires_grad_(True)
+    gf, bf = gam.clone().requires_grad_(True), bet.clone().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xf, (D,), gf, bf, 1e-5)
+    assert rel(y, ref) < 1e-2
+    dy = torch.randn(M, D, device="cuda", generator=g0).to(torch.bfloat16)
+    ref.backward(dy.float())
+    dx = torch.randn(M, D, device="cuda", generator=g0).to(torch.bfloat16)
+    dx0 = dx.float().clone()
+    dg = torch.zeros(D, device="cuda")
+    db = torch.zeros(D, device="cuda")
+    ops.layernorm_bwd(dy, x, gam, mu, rs, dx, dg, db, accumulate=True)
+    assert rel(dx.float() - dx0, xf.grad) < 2e-2
+    assert rel(dg, gf.grad) < 1e-3 and rel(db, bf.grad) < 1e-3
+    cs = torch.zeros(D, device="cuda")
+    ops.colsum_accum(dy, cs)
+    assert rel(cs, dy.float().sum(0)) < 1e-4
+
+
+def test_tubelet_layout_matches_patchify():
+    import numpy as np
+    from oracle import transform_oracle as TO
+    from paper_2309_16669_b200 import transform as TR
+    cfg = VitConfig(frames=4, height=64, width=96, cube_t=2, cube_h=16, cube_w=16, depth=1, dim=64, heads=1)
+    B = 2
+    g0 = torch.Generator().manual_seed(5)
+    fr = torch.randint(0, 256, (B, 4, 120, 160, 3), generator=g0, dtype=torch.uint8)
+    boxes = np.asarray([[3, 4, 150, 101], [10, 0, 140, 120]], dtype=np.int32)
+    flips = np.asarray([1, 0], dtype=np.uint8)
+    cthw = TR.transform(fr.cuda(), boxes, flips, (64, 96), out_dtype=torch.float32)
+    tub = TR.transform(fr.cuda(), boxes, flips, (64, 96), out_dtype=torch.float32, layout="tubelet", tubelet=(2, 16, 16))
+    assert torch.equal(tub, VO.patchify(cthw, cfg))
