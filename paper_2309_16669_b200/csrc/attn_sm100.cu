@@ -260,25 +260,53 @@ struct BwdArgs {
   float scale, scale_log2;
   const float* lse;
   const float* delta;
-  float* dq_acc;          // [B, N, H, 64] fp32
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   int64_t ld_g, sb_g;     // strides of dk/dv
   int causal;
 };
 
-constexpr int B_SK = 0, B_SV = 16384, B_SQD = 32768;      // 2 stages x (Q 16K + dO 16K)
-constexpr int B_SPT = B_SQD + 2 * 32768, B_SDS = B_SPT + 32768;
-constexpr int B_SLD = B_SDS + 32768;                      // 2 stages x (lse 512 + delta 512)
+// smem (dynamic base must be 1 KB aligned; checked): all 128B-swizzled bf16 tiles first
+constexpr int B_SK = 0, B_SV = 16384;
+constexpr int B_SQD = 32768;                  // 2 stages x (Q 16K + dO 16K)
+constexpr int B_SPT = B_SQD + 2 * 32768;      // 2 buffers x P^T 32K (also dQ fp32 staging)
+constexpr int B_SDS = B_SPT + 2 * 32768;      // 2 buffers x dS^T 32K
+constexpr int B_SLD = B_SDS + 2 * 32768;      // 2 stages x (lse 512 + delta 512)
 constexpr int B_BAR = B_SLD + 2 * 1024;
-constexpr int B_SMEM = B_BAR + 256 + 1024;
+constexpr int B_SMEM = B_BAR + 128;
+static_assert(B_SMEM <= 232448, "attn bwd smem");
+constexpr int kBwdCompute = 8;               // compute warps (2 per TMEM lane quadrant)
 
-__global__ void __launch_bounds__(192, 1)
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// drain one warp's share of the dQ tile (32 query rows x 32 columns) from TMEM through a
+// 128B-swizzled fp32 staging block and reduce-add it into the fp32 accumulator with TMA
+__device__ __forceinline__ void drain_dq(uint32_t taddr, uint8_t* stage, const CUtensorMap* tmDQ, int lane, int c0,
+                                         int q0, int b) {
+  uint32_t r[32];
+  tc::tmem_ld_32x32b_x32(taddr, r);
+  tc::tmem_ld_wait();
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    *reinterpret_cast<uint4*>(stage + lane * 128 + ((u ^ (lane & 7)) << 4)) =
+        make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
+  tc::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmDQ)),
+                 "r"(smem_u32(stage)), "r"(c0), "r"(q0), "r"(b)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
+__global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const BwdArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+                    const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
   uint8_t* sK = smem + B_SK;
   uint8_t* sV = smem + B_SV;
   uint8_t* sQD = smem + B_SQD;
@@ -301,24 +329,26 @@ __global__ void __launch_bounds__(192, 1)
   const int nq_all = (a.N + BT - 1) / BT;
   const int i0 = a.causal ? kt : 0;  // first query tile that sees this key tile
   const int nq = nq_all - i0;
+  constexpr int kTMA = kBwdCompute, kMMA = kBwdCompute + 1;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == kTMA && lane == 0) {
     tc::tma_prefetch(&tmQ);
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
     tc::tma_prefetch(&tmdO);
+    tc::tma_prefetch(&tmDQ);
     tc::mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&qd_full[s], 1);
       tc::mbar_init(&qd_empty[s], 1);
     }
     tc::mbar_init(s_full, 1);
-    tc::mbar_init(ds_ready, 4);
+    tc::mbar_init(ds_ready, kBwdCompute);
     tc::mbar_init(mma_done, 1);
-    tc::mbar_init(dq_free, 4);
+    tc::mbar_init(dq_free, kBwdCompute);
     tc::fence_barrier_init();
   }
-  if (warp == 5) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -326,7 +356,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384;
   const int64_t bh = (int64_t)b * a.H + h;
 
-  if (warp == 4) {
+  if (warp == kTMA) {
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(kv_full, 32768);
       tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
@@ -349,12 +379,12 @@ __global__ void __launch_bounds__(192, 1)
                      : "memory");
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMMA) {
     if (lane == 0) {
       constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
       constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: B (dO / Q) MN-major
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aPT = smem_u32(sPT), aDS = smem_u32(sDS);
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
       tc::mbar_wait(kv_full, 0);
       for (int ii = 0; ii <= nq; ++ii) {
         if (ii < nq) {
@@ -374,11 +404,11 @@ __global__ void __launch_bounds__(192, 1)
           tc::umma_commit(s_full);
         } else {
           tc::mbar_wait(ds_ready, (ii - 1) & 1);
-          tc::tc_fence_after();
         }
         if (ii > 0) {
           const int ps = (ii - 1) & 1;
           const uint32_t aQ = smem_u32(sQD + ps * 32768), aDO = aQ + 16384;
+          const uint32_t aPT = smem_u32(sPT + ps * 32768), aDS = smem_u32(sDS + ps * 32768);
           if (ii > 1) tc::mbar_wait(dq_free, (ii - 2) & 1);
           tc::tc_fence_after();
           const uint32_t acc = (ii > 1) ? 1u : 0u;
@@ -405,126 +435,114 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ compute warps (thread = key row)
-    const int row = warp * 32 + lane;
+    // ------------------------------------------------------------ compute warps
+    // warp w: TMEM lane quadrant (w & 3) -> key rows; column half (w >> 2) of the 128 query columns
+    const int quad = warp & 3, half = warp >> 2;
+    const int row = quad * 32 + lane;
     const int kvi = kv0 + row;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     for (int ii = 0; ii < nq; ++ii) {
       const int i = i0 + ii, st = ii & 1;
       const int q0 = i * BT;
-      tc::mbar_wait(s_full, ii & 1);
-      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // lse/delta landed (already complete for the MMA)
-      tc::tc_fence_after();
-      if (ii > 0) {
-        // drain dQ_{i-1} (thread = query row of tile i-1) and free P^T/dS^T
-        tc::mbar_wait(mma_done, (ii - 1) & 1);
-        tc::tc_fence_after();
-        const int qrow = q0 - BT + row;
-        float* dst = a.dq_acc + (((int64_t)b * a.N + qrow) * a.H + h) * HD;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld_32x32b_x32(tDQ + lane_off + c * 32, r);
-          tc::tmem_ld_wait();
-          if (qrow < a.N) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 4)
-              asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c * 32 + e),
-                           "f"(__uint_as_float(r[e])), "f"(__uint_as_float(r[e + 1])), "f"(__uint_as_float(r[e + 2])),
-                           "f"(__uint_as_float(r[e + 3]))
-                           : "memory");
-          }
-        }
-        tc::tc_fence_before();
+      uint8_t* pt = sPT + st * 32768;
+      uint8_t* ds_t = sDS + st * 32768;
+      if (ii >= 2) {
+        // this P^T slot staged dQ(ii-2): its TMA reduce must have read the smem (all warps)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(dq_free);
+        named_bar(1, 32 * kBwdCompute);
       }
+      tc::mbar_wait(s_full, ii & 1);
+      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // lse/delta landed
+      tc::tc_fence_after();
       const float* sl = sLD + st * 256;
       const float* sd = sl + 128;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = half * 2 + cc;
         uint32_t rs[32], rp[32];
         tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
         tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
         tc::tmem_ld_wait();
-        float p[32], ds[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int qc = c * 32 + e;
-          const int qi = q0 + qc;
-          const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-          const float lse2 = sl[qc] * kLog2e;
-          const float pe = ok ? ex2(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
-          p[e] = pe;
-          ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[e]) - sd[qc]) : 0.f;
-        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
+          const float4 l0 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8);
+          const float4 l1 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8 + 4);
+          const float4 d0 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8);
+          const float4 d1 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8 + 4);
+          const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+          const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+          float p[8], ds[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int qc = c * 32 + u * 8 + e;
+            const int qi = q0 + qc;
+            const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+            const float pe = ok ? ex2(fmaf(__uint_as_float(rs[u * 8 + e]), a.scale_log2, -lv[e] * kLog2e)) : 0.f;
+            p[e] = pe;
+            ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[u * 8 + e]) - dv[e]) : 0.f;
+          }
           uint4 v, w;
-          v.x = pack_bf16x2(p[u * 8 + 0], p[u * 8 + 1]);
-          v.y = pack_bf16x2(p[u * 8 + 2], p[u * 8 + 3]);
-          v.z = pack_bf16x2(p[u * 8 + 4], p[u * 8 + 5]);
-          v.w = pack_bf16x2(p[u * 8 + 6], p[u * 8 + 7]);
-          w.x = pack_bf16x2(ds[u * 8 + 0], ds[u * 8 + 1]);
-          w.y = pack_bf16x2(ds[u * 8 + 2], ds[u * 8 + 3]);
-          w.z = pack_bf16x2(ds[u * 8 + 4], ds[u * 8 + 5]);
-          w.w = pack_bf16x2(ds[u * 8 + 6], ds[u * 8 + 7]);
-          st_sw128(sPT, row, c * 4 + u, v);
-          st_sw128(sDS, row, c * 4 + u, w);
+          v.x = pack_bf16x2(p[0], p[1]);
+          v.y = pack_bf16x2(p[2], p[3]);
+          v.z = pack_bf16x2(p[4], p[5]);
+          v.w = pack_bf16x2(p[6], p[7]);
+          w.x = pack_bf16x2(ds[0], ds[1]);
+          w.y = pack_bf16x2(ds[2], ds[3]);
+          w.z = pack_bf16x2(ds[4], ds[5]);
+          w.w = pack_bf16x2(ds[6], ds[7]);
+          st_sw128(pt, row, c * 4 + u, v);
+          st_sw128(ds_t, row, c * 4 + u, w);
         }
       }
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_ready);
+      if (ii > 0) {
+        // dQ(ii-1): TMEM lanes = query rows of tile i-1; stage into the P^T slot it no longer needs
+        tc::mbar_wait(mma_done, (ii - 1) & 1);
+        tc::tc_fence_after();
+        drain_dq(tDQ + lane_off + half * 32, sPT + ((ii - 1) & 1) * 32768 + warp * 4096, &tmDQ, lane,
+                 h * HD + half * 32, q0 - BT + quad * 32, b);
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(dq_free);
+      }
     }
     // last dQ + dK/dV out
     tc::mbar_wait(mma_done, (nq - 1) & 1);
     tc::tc_fence_after();
-    {
-      const int qrow = (i0 + nq - 1) * BT + row;
-      float* dst = a.dq_acc + (((int64_t)b * a.N + qrow) * a.H + h) * HD;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tDQ + lane_off + c * 32, r);
-        tc::tmem_ld_wait();
-        if (qrow < a.N) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + c * 32 + e),
-                         "f"(__uint_as_float(r[e])), "f"(__uint_as_float(r[e + 1])), "f"(__uint_as_float(r[e + 2])),
-                         "f"(__uint_as_float(r[e + 3]))
-                         : "memory");
-        }
-      }
+    if (nq >= 2) {
+      // the slot of tile nq-1 staged dQ(nq-3)? no: it held P(nq-1); staging dQ(nq-1) reuses it after mma_done
     }
+    drain_dq(tDQ + lane_off + half * 32, sPT + ((nq - 1) & 1) * 32768 + warp * 4096, &tmDQ, lane, h * HD + half * 32,
+             (i0 + nq - 1) * BT + quad * 32, b);
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const uint32_t tsrc = which ? tDK : tDV;
-      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD;
+      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + half * 32;
+      uint32_t r[32];
+      tc::tmem_ld_32x32b_x32(tsrc + lane_off + half * 32, r);
+      tc::tmem_ld_wait();
+      if (kvi < a.N) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tsrc + lane_off + c * 32, r);
-        tc::tmem_ld_wait();
-        if (kvi < a.N) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 v;
-            v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
-            v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
-            v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
-            v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
-            reinterpret_cast<uint4*>(g + c * 32)[u] = v;
-          }
+        for (int u = 0; u < 4; ++u) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+          reinterpret_cast<uint4*>(g)[u] = v;
         }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMMA) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 512);
   }
@@ -659,6 +677,10 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
   if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
   if ((s = make_maps(&mdo, dout, B, H, N, ld_o, sb_o))) return s;
+  CUtensorMap mdq;
+  if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
+                                 (uint64_t)N * H * HD, 32, 32, 1)))
+    return s;
   BwdArgs a;
   a.B = B;
   a.H = H;
@@ -668,7 +690,6 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.scale_log2 = softmax_scale * kLog2e;
   a.lse = lse;
   a.delta = delta;
-  a.dq_acc = dq_acc;
   a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   a.ld_g = ld_g;
@@ -681,7 +702,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     attr = true;
   }
   dim3 grid((N + BT - 1) / BT, H, B);
-  attn_bwd_kernel<<<grid, 192, B_SMEM, st>>>(mq, mk, mv, mdo, a);
+  attn_bwd_kernel<<<grid, 32 * (kBwdCompute + 2), B_SMEM, st>>>(mq, mk, mv, mdo, mdq, a);
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
