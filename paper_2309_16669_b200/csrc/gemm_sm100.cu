@@ -19,6 +19,9 @@
 // restated from PAPER.md:258-260,727).
 #include "tc_common.cuh"
 
+#include <stdlib.h>
+#include <string.h>
+
 namespace {
 
 constexpr int BM = 128;
@@ -36,6 +39,7 @@ struct GemmArgs {
   void* aux_out;         // bf16 [M, ldaux]: pre-activation out (EPI_BIAS_GELU)
   int num_m, num_n, splits, kb_per_split, num_kb;
   int vec_ok;            // 16B-aligned rows for vector epilogue stores
+  int tma_out;           // bf16 C (and aux_out) written by TMA stores from swizzled smem
   float alpha;
 };
 
@@ -46,7 +50,8 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = 4 * 2 * 2048;            // 4 epilogue warps x 2 x [32 rows x 32 bf16]
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
 };
 
@@ -131,13 +136,41 @@ __device__ __forceinline__ void store_aux_chunk(const GemmArgs& a, int row, int 
   }
 }
 
+// Stage 32 rows x 32 bf16 (thread = row) into a 64B-swizzled 2 KB block and TMA-store it.
+__device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap* map, int lane, const float (&v)[32],
+                                                int col, int row0) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this buffer's last store read
+  __syncwarp();
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint4 q;
+    q.x = pack_bf16x2(v[u * 8 + 0], v[u * 8 + 1]);
+    q.y = pack_bf16x2(v[u * 8 + 2], v[u * 8 + 3]);
+    q.z = pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]);
+    q.w = pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]);
+    *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ sw) << 4)) = q;
+  }
+  tc::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(stg)), "r"(col), "r"(row0)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs a) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const GemmArgs a) {
   using C = Cfg<BN, A_MN, B_MN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -149,6 +182,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
+    if (a.tma_out) {
+      tc::tma_prefetch(&tmC);
+      if (a.epi == AVB_EPI_BIAS_GELU) tc::tma_prefetch(&tmX);
+    }
     for (int s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -239,6 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
     const int ew = warp & 3;
+    uint8_t* stg = smem_epi + ew * 4096;
+    int sbuf = 0;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int mn = t % (a.num_m * a.num_n);
@@ -270,7 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) v[j] += rr[j];
           }
         } else if (a.epi == AVB_EPI_BIAS_GELU) {
-          store_aux_chunk(a, row, col, v);
+          if (a.tma_out) {
+            tma_store_chunk(stg + sbuf * 2048, &tmX, lane, v, col, m0 + ew * 32);
+            sbuf ^= 1;
+          } else {
+            store_aux_chunk(a, row, col, v);
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = tc::quick_gelu(v[j]);
         } else if (a.epi == AVB_EPI_DGELU) {
@@ -279,7 +323,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= tc::quick_gelu_grad(h[j]);
         }
-        store_row_chunk(a, row, col, v);
+        if (a.tma_out) {
+          tma_store_chunk(stg + sbuf * 2048, &tmC, lane, v, col, m0 + ew * 32);
+          sbuf ^= 1;
+        } else {
+          store_row_chunk(a, row, col, v);
+        }
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -287,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (warp >= 4 && a.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
@@ -295,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int BN, bool A_MN, bool B_MN>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t st) {
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, const CUtensorMap& tx,
+           const GemmArgs& a, cudaStream_t st) {
   using C = Cfg<BN, A_MN, B_MN>;
   static bool attr = false;
   if (!attr) {
@@ -305,7 +356,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cuda
   }
   const int total = a.num_m * a.num_n * a.splits;
   const int grid = total < avb::sm_count() ? total : avb::sm_count();
-  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::SMEM, st>>>(ta, tb, a);
+  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::SMEM, st>>>(ta, tb, tcm, tx, a);
   return avb::launch_status("avb_gemm");
 }
 
@@ -364,6 +415,28 @@ int make_tmap_3d_bf16(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d
   }
   return AVB_OK;
 }
+int make_tmap_2d_bf16_sw(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                         uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+  int s = get_encode();
+  if (s) return s;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(2d bf16 sw%d) failed (%d)", swizzle_bytes, (int)r);
+    return AVB_E_ARG;
+  }
+  return AVB_OK;
+}
+
 int make_tmap_3d_f32(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_elems,
                      uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2) {
   int s = get_encode();
@@ -440,16 +513,27 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   g.vec_ok = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc * esz) % 16 == 0) &&
              (!aux || (((reinterpret_cast<uintptr_t>(aux) & 15) == 0) && (ldaux * 2) % 16 == 0)) &&
              (!aux_out || (((reinterpret_cast<uintptr_t>(aux_out) & 15) == 0) && (ldaux * 2) % 16 == 0));
+  // bf16 outputs go out through TMA stores (64B-swizzled 32x32 boxes; TMA clips M/N tails)
+  CUtensorMap tcm, tx;
+  memset(&tcm, 0, sizeof(tcm));
+  memset(&tx, 0, sizeof(tx));
+  g.tma_out = 0;
+  if (g.vec_ok && (epilogue == AVB_EPI_BF16 || epilogue == AVB_EPI_BIAS_GELU || epilogue == AVB_EPI_DGELU) &&
+      !getenv("AVB_GEMM_NO_TMA_STORE")) {
+    int s1 = avb::make_tmap_2d_bf16_sw(&tcm, C, N, M, ldc, 32, 32, 64);
+    int s2 = (epilogue == AVB_EPI_BIAS_GELU) ? avb::make_tmap_2d_bf16_sw(&tx, aux_out, N, M, ldaux, 32, 32, 64) : 0;
+    if (s1 == AVB_OK && s2 == AVB_OK) g.tma_out = 1;
+  }
   cudaStream_t st = avb::as_stream(stream);
   const int key = (BN == 256 ? 4 : 0) | (a_major << 1) | b_major;
   switch (key) {
-    case 0: return launch<128, false, false>(ta, tb, g, st);
-    case 1: return launch<128, false, true>(ta, tb, g, st);
-    case 2: return launch<128, true, false>(ta, tb, g, st);
-    case 3: return launch<128, true, true>(ta, tb, g, st);
-    case 4: return launch<256, false, false>(ta, tb, g, st);
-    case 5: return launch<256, false, true>(ta, tb, g, st);
-    case 6: return launch<256, true, false>(ta, tb, g, st);
-    default: return launch<256, true, true>(ta, tb, g, st);
+    case 0: return launch<128, false, false>(ta, tb, tcm, tx, g, st);
+    case 1: return launch<128, false, true>(ta, tb, tcm, tx, g, st);
+    case 2: return launch<128, true, false>(ta, tb, tcm, tx, g, st);
+    case 3: return launch<128, true, true>(ta, tb, tcm, tx, g, st);
+    case 4: return launch<256, false, false>(ta, tb, tcm, tx, g, st);
+    case 5: return launch<256, false, true>(ta, tb, tcm, tx, g, st);
+    case 6: return launch<256, true, false>(ta, tb, tcm, tx, g, st);
+    default: return launch<256, true, true>(ta, tb, tcm, tx, g, st);
   }
 }
