@@ -29,7 +29,7 @@ class LaunchTimer:
         self.ev = {}
         self.active = False
 
-    def wrap(self, name, fn):
+    def wrap(self, name, fn, keyfn=None):
         def inner(*a, **k):
             if not self.active:
                 return fn(*a, **k)
@@ -40,6 +40,8 @@ class LaunchTimer:
             r = fn(*a, **k)
             e1.record(s)
             self.ev.setdefault(name, []).append((e0, e1))
+            if keyfn is not None:
+                self.ev.setdefault(name + ":" + keyfn(*a, **k), []).append((e0, e1))
             return r
         return inner
 
@@ -82,6 +84,11 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
                                          "colsum_accum", "tokens_fwd", "tokens_bwd", "xent", "adamw")}
     per_launch = {"attn_bwd": 3}
 
+    def gemm_key(a, b, a_mn=False, b_mn=False, epilogue=0, split_k=1, **k):
+        M, K = (a.shape[1], a.shape[0]) if a_mn else (a.shape[0], a.shape[1])
+        N = b.shape[1] if b_mn else b.shape[0]
+        return f"{M}x{N}x{K}/{'T' if a_mn else 'N'}{'T' if b_mn else 'N'}/epi{epilogue}/s{split_k}"
+
     def counted(name, fn):
         def inner(*a, **k):
             counts["n"] += per_launch.get(name, 1)
@@ -90,8 +97,10 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
 
     for n, fn in orig.items():
         f = counted(n, fn)
-        if n in ("attn_fwd", "attn_bwd", "gemm"):
+        if n in ("attn_fwd", "attn_bwd"):
             f = timer.wrap(n, f)
+        elif n == "gemm":
+            f = timer.wrap(n, f, keyfn=gemm_key)
         setattr(ops, n, f)
 
     store = model.store
@@ -159,6 +168,14 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     step_ms_events = ms
     for k in kern:
         kern[k]["share_of_step"] = kern[k]["total_ms"] / args.steps / step_ms_events
+    shapes = {}
+    for k, v in fam.items():
+        if k.startswith("gemm:"):
+            dims = k.split(":")[1].split("/")[0].split("x")
+            fl = 2.0 * int(dims[0]) * int(dims[1]) * int(dims[2])
+            shapes[k[5:]] = {"ms_per_step": v["total_ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                             "tflops": fl / (v["avg_ms"] / 1e3) / 1e12}
+    shapes = dict(sorted(shapes.items(), key=lambda kv: -kv[1]["ms_per_step"])[:16])
     dom = max(kern, key=lambda k: kern[k]["total_ms"]) if kern else None
     roof = None
     if dom:
@@ -202,6 +219,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
                    "l2": "per-step working set (activations ~30 GB) >> 126 MB L2; no flush needed"},
         "attn_tflops": attn_tflops,
         "kernels": kern,
+        "gemm_shapes": shapes,
         "roofline": roof,
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "clips/s", "h2d_bytes_per_step": int(host.numel()),
                 "d2h_bytes_per_step": 4},
