@@ -40,6 +40,7 @@ struct GemmArgs {
   int num_m, num_n, splits, kb_per_split, num_kb;
   int vec_ok;            // 16B-aligned rows for vector epilogue stores
   int tma_out;           // bf16 C (and aux_out) written by TMA stores from swizzled smem
+  int tma_aux;           // aux (residual / pre-activation) tiles TMA-prefetched into a smem ring
   float alpha;
 };
 
@@ -50,8 +51,9 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int EPI_BYTES = 4 * 2 * 2048;            // 4 epilogue warps x 2 x [32 rows x 32 bf16]
+  static constexpr int EPI_BYTES = 2 * 4 * 2 * 2048;        // (store staging + aux ring) x 4 warps x 2 x 2 KB
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  static_assert(SMEM <= 232448, "gemm smem");
   static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
 };
 
@@ -174,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* aux_bar = tempty + 2;  // [4 warps][2 slots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.num_m * a.num_n * a.splits;
@@ -182,10 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    if (a.tma_out) {
-      tc::tma_prefetch(&tmC);
-      if (a.epi == AVB_EPI_BIAS_GELU) tc::tma_prefetch(&tmX);
-    }
+    if (a.tma_out) tc::tma_prefetch(&tmC);
+    if (a.tma_out || a.tma_aux) tc::tma_prefetch(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], 4);
     }
+    for (int s = 0; s < 8; ++s) tc::mbar_init(&aux_bar[s], 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -276,41 +278,91 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
     const int ew = warp & 3;
-    uint8_t* stg = smem_epi + ew * 4096;
+    uint8_t* stg = smem_epi + ew * 4096;               // 2 x 2 KB TMA-store staging
+    uint8_t* axs = smem_epi + 4 * 4096 + ew * 4096;    // 2 x 2 KB TMA-loaded aux ring
+    uint64_t* axb = aux_bar + ew * 2;
     int sbuf = 0;
+    uint32_t auxc = 0;                                 // aux chunks consumed (ring position)
+    constexpr int NCH = BN / 32;
+    const bool tma_aux = a.tma_aux != 0;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int mn = t % (a.num_m * a.num_n);
       const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int row0 = m0 + ew * 32;
+      if (tma_aux && lane == 0) {
+        // prefetch this tile's first two aux chunks (the ring slots were freed by the last tile)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int slot = (auxc + c) & 1;
+          tc::mbar_arrive_expect_tx(&axb[slot], 2048);
+          tc::tma_load_2d(axs + slot * 2048, &tmX, &axb[slot], n0 + c * 32, row0);
+        }
+      }
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
-      const int row = m0 + ew * 32 + lane;
+      const int row = row0 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         const int col = n0 + c * 32;
         uint32_t r[32];
         tc::tmem_ld_32x32b_x32(tmem + acc * BN + ((uint32_t)(ew * 32) << 16) + c * 32, r);
+        float xa[32];
+        if (tma_aux) {
+          const int slot = auxc & 1;
+          tc::mbar_wait(&axb[slot], (auxc >> 1) & 1);
+          const uint8_t* src = axs + slot * 2048 + lane * 64;
+          const int sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 q = *reinterpret_cast<const uint4*>(src + ((u ^ sw) << 4));
+            const __nv_bfloat162* hq = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(hq[e]);
+              xa[u * 8 + 2 * e] = f.x;
+              xa[u * 8 + 2 * e + 1] = f.y;
+            }
+          }
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && c + 2 < NCH) {
+            tc::mbar_arrive_expect_tx(&axb[slot], 2048);
+            tc::tma_load_2d(axs + slot * 2048, &tmX, &axb[slot], col + 64, row0);
+          }
+          ++auxc;
+        }
         tc::tmem_ld_wait();
         if (col >= a.N) continue;
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * a.alpha;
         if (a.bias) {
+          if (col + 32 <= a.N && a.vec_ok) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += (col + j < a.N) ? __ldg(a.bias + col + j) : 0.f;
+            for (int j = 0; j < 32; j += 4) {
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + col + j));
+              v[j] += bb.x;
+              v[j + 1] += bb.y;
+              v[j + 2] += bb.z;
+              v[j + 3] += bb.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (col + j < a.N) ? __ldg(a.bias + col + j) : 0.f;
+          }
         }
         if (a.epi == AVB_EPI_BF16) {
           if (a.aux) {
-            float rr[32];
-            load_aux_chunk(a, a.aux, row, col, rr);
+            if (!tma_aux) load_aux_chunk(a, a.aux, row, col, xa);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += rr[j];
+            for (int j = 0; j < 32; ++j) v[j] += xa[j];
           }
         } else if (a.epi == AVB_EPI_BIAS_GELU) {
           if (a.tma_out) {
-            tma_store_chunk(stg + sbuf * 2048, &tmX, lane, v, col, m0 + ew * 32);
+            tma_store_chunk(stg + sbuf * 2048, &tmX, lane, v, col, row0);
             sbuf ^= 1;
           } else {
             store_aux_chunk(a, row, col, v);
@@ -318,13 +370,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = tc::quick_gelu(v[j]);
         } else if (a.epi == AVB_EPI_DGELU) {
-          float h[32];
-          load_aux_chunk(a, a.aux, row, col, h);
+          if (!tma_aux) load_aux_chunk(a, a.aux, row, col, xa);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= tc::quick_gelu_grad(h[j]);
+          for (int j = 0; j < 32; ++j) v[j] *= tc::quick_gelu_grad(xa[j]);
         }
         if (a.tma_out) {
-          tma_store_chunk(stg + sbuf * 2048, &tmC, lane, v, col, m0 + ew * 32);
+          tma_store_chunk(stg + sbuf * 2048, &tmC, lane, v, col, row0);
           sbuf ^= 1;
         } else {
           store_row_chunk(a, row, col, v);
@@ -523,6 +574,10 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
     int s1 = avb::make_tmap_2d_bf16_sw(&tcm, C, N, M, ldc, 32, 32, 64);
     int s2 = (epilogue == AVB_EPI_BIAS_GELU) ? avb::make_tmap_2d_bf16_sw(&tx, aux_out, N, M, ldaux, 32, 32, 64) : 0;
     if (s1 == AVB_OK && s2 == AVB_OK) g.tma_out = 1;
+  }
+  g.tma_aux = 0;
+  if (g.vec_ok && aux && (epilogue == AVB_EPI_BF16 || epilogue == AVB_EPI_DGELU) && !getenv("AVB_GEMM_NO_TMA_AUX")) {
+    if (avb::make_tmap_2d_bf16_sw(&tx, aux, N, M, ldaux, 32, 32, 64) == AVB_OK) g.tma_aux = 1;
   }
   cudaStream_t st = avb::as_stream(stream);
   const int key = (BN == 256 ? 4 : 0) | (a_major << 1) | b_major;

@@ -172,10 +172,19 @@ __device__ __forceinline__ uint32_t elect_one() {
   return pred;
 }
 
-__device__ __forceinline__ float quick_gelu(float x) { return x / (1.0f + __expf(-1.702f * x)); }
+// QuickGELU x*sigmoid(1.702x) with sigmoid(z) = 0.5 + 0.5*tanh(z/2): one MUFU op per element
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float quick_gelu(float x) {
+  const float s = fmaf(0.5f, tanh_approx(0.851f * x), 0.5f);
+  return x * s;
+}
 __device__ __forceinline__ float quick_gelu_grad(float x) {
-  const float s = 1.0f / (1.0f + __expf(-1.702f * x));
-  return s + 1.702f * x * s * (1.0f - s);
+  const float s = fmaf(0.5f, tanh_approx(0.851f * x), 0.5f);
+  return fmaf(1.702f * x * s, 1.0f - s, s);
 }
 
 }  // namespace tc
