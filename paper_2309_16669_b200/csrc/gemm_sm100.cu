@@ -44,14 +44,17 @@ struct GemmArgs {
   float alpha;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int EK>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;               // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;               // 32 KB (BN=256)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int STAGES = (BN == 256) ? (EK ? 3 : 4) : 6;
+  // EK 0: plain; 1: bf16 aux read (residual / GELU pre-activation); 2: second bf16 output (BIAS_GELU)
+  static constexpr int SSLOTS = EK == 0 ? 2 : (EK == 1 ? 4 : 10);  // TMA-store staging slots per epilogue warp
+  static constexpr int XSLOTS = EK == 0 ? 2 : (EK == 1 ? 6 : 1);   // TMA-load aux ring slots per epilogue warp
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int EPI_BYTES = 2 * 4 * 2 * 2048;        // (store staging + aux ring) x 4 warps x 2 x 2 KB
+  static constexpr int EPI_BYTES = (SSLOTS + XSLOTS) * 4 * 2048;  // per epilogue warp: store + aux slots of 2 KB
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static_assert(SMEM <= 232448, "gemm smem");
   static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
@@ -139,9 +142,11 @@ __device__ __forceinline__ void store_aux_chunk(const GemmArgs& a, int row, int 
 }
 
 // Stage 32 rows x 32 bf16 (thread = row) into a 64B-swizzled 2 KB block and TMA-store it.
+template <int PENDING>
 __device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap* map, int lane, const float (&v)[32],
                                                 int col, int row0) {
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this buffer's last store read
+  // the slot we overwrite was used PENDING+1 stores ago: allow PENDING groups in flight
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(PENDING) : "memory");
   __syncwarp();
   const int sw = (lane >> 1) & 3;
 #pragma unroll
@@ -164,11 +169,11 @@ __device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap*
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int EK>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const GemmArgs a) {
-  using C = Cfg<BN, A_MN, B_MN>;
+  using C = Cfg<BN, A_MN, B_MN, EK>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* aux_bar = tempty + 2;  // [4 warps][2 slots]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 8);
+  uint64_t* aux_bar = tempty + 2;  // [4 warps][XSLOTS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4 * C::XSLOTS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.num_m * a.num_n * a.splits;
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], 4);
     }
-    for (int s = 0; s < 8; ++s) tc::mbar_init(&aux_bar[s], 1);
+    for (int s = 0; s < 4 * C::XSLOTS; ++s) tc::mbar_init(&aux_bar[s], 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -278,9 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
     const int ew = warp & 3;
-    uint8_t* stg = smem_epi + ew * 4096;               // 2 x 2 KB TMA-store staging
-    uint8_t* axs = smem_epi + 4 * 4096 + ew * 4096;    // 2 x 2 KB TMA-loaded aux ring
-    uint64_t* axb = aux_bar + ew * 2;
+    constexpr int SS = C::SSLOTS, XS = C::XSLOTS;
+    uint8_t* stg = smem_epi + ew * SS * 2048;                    // TMA-store staging slots
+    uint8_t* axs = smem_epi + 4 * SS * 2048 + ew * XS * 2048;    // TMA-loaded aux ring
+    uint64_t* axb = aux_bar + ew * XS;
     int sbuf = 0;
     uint32_t auxc = 0;                                 // aux chunks consumed (ring position)
     constexpr int NCH = BN / 32;
@@ -293,10 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row0 = m0 + ew * 32;
       if (tma_aux && lane == 0) {
-        // prefetch this tile's first two aux chunks (the ring slots were freed by the last tile)
+        // prefetch this tile's first XS aux chunks (the ring slots were freed by the last tile)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int slot = (auxc + c) & 1;
+        for (int c = 0; c < XS && c < NCH; ++c) {
+          const int slot = (auxc + c) % XS;
           tc::mbar_arrive_expect_tx(&axb[slot], 2048);
           tc::tma_load_2d(axs + slot * 2048, &tmX, &axb[slot], n0 + c * 32, row0);
         }
@@ -311,8 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tmem_ld_32x32b_x32(tmem + acc * BN + ((uint32_t)(ew * 32) << 16) + c * 32, r);
         float xa[32];
         if (tma_aux) {
-          const int slot = auxc & 1;
-          tc::mbar_wait(&axb[slot], (auxc >> 1) & 1);
+          const int slot = auxc % XS;
+          tc::mbar_wait(&axb[slot], (auxc / XS) & 1);
           const uint8_t* src = axs + slot * 2048 + lane * 64;
           const int sw = (lane >> 1) & 3;
 #pragma unroll
@@ -328,9 +334,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc::fence_proxy_async();
           __syncwarp();
-          if (lane == 0 && c + 2 < NCH) {
+          if (lane == 0 && c + XS < NCH) {
             tc::mbar_arrive_expect_tx(&axb[slot], 2048);
-            tc::tma_load_2d(axs + slot * 2048, &tmX, &axb[slot], col + 64, row0);
+            tc::tma_load_2d(axs + slot * 2048, &tmX, &axb[slot], col + XS * 32, row0);
           }
           ++auxc;
         }
@@ -362,8 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else if (a.epi == AVB_EPI_BIAS_GELU) {
           if (a.tma_out) {
-            tma_store_chunk(stg + sbuf * 2048, &tmX, lane, v, col, row0);
-            sbuf ^= 1;
+            tma_store_chunk<SS - 1>(stg + sbuf * 2048, &tmX, lane, v, col, row0);
+            sbuf = (sbuf + 1) % SS;
           } else {
             store_aux_chunk(a, row, col, v);
           }
@@ -375,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) v[j] *= tc::quick_gelu_grad(xa[j]);
         }
         if (a.tma_out) {
-          tma_store_chunk(stg + sbuf * 2048, &tmC, lane, v, col, row0);
-          sbuf ^= 1;
+          tma_store_chunk<SS - 1>(stg + sbuf * 2048, &tmC, lane, v, col, row0);
+          sbuf = (sbuf + 1) % SS;
         } else {
           store_row_chunk(a, row, col, v);
         }
@@ -395,19 +401,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int EK>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, const CUtensorMap& tx,
            const GemmArgs& a, cudaStream_t st) {
-  using C = Cfg<BN, A_MN, B_MN>;
+  using C = Cfg<BN, A_MN, B_MN, EK>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return avb::cuda_status(e, "gemm: set smem attribute");
     attr = true;
   }
   const int total = a.num_m * a.num_n * a.splits;
   const int grid = total < avb::sm_count() ? total : avb::sm_count();
-  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::SMEM, st>>>(ta, tb, tcm, tx, a);
+  gemm_kernel<BN, A_MN, B_MN, EK><<<grid, kThreads, C::SMEM, st>>>(ta, tb, tcm, tx, a);
   return avb::launch_status("avb_gemm");
 }
 
@@ -581,14 +588,26 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   }
   cudaStream_t st = avb::as_stream(stream);
   const int key = (BN == 256 ? 4 : 0) | (a_major << 1) | b_major;
+  // heavy epilogues (bf16 aux read or a second bf16 output) get 3 mainloop stages and 6-deep
+  // aux / store rings so TMA latency is covered while the epilogue streams 32-column chunks
+  const bool heavy = BN == 256 && a_major == 0 && (g.tma_aux || (g.tma_out && epilogue == AVB_EPI_BIAS_GELU)) &&
+                     !getenv("AVB_GEMM_NO_HEAVY");
+  if (heavy) {
+    if (g.tma_aux) {
+      if (b_major == 0) return launch<256, false, false, 1>(ta, tb, tcm, tx, g, st);
+      return launch<256, false, true, 1>(ta, tb, tcm, tx, g, st);
+    }
+    if (b_major == 0) return launch<256, false, false, 2>(ta, tb, tcm, tx, g, st);
+    return launch<256, false, true, 2>(ta, tb, tcm, tx, g, st);
+  }
   switch (key) {
-    case 0: return launch<128, false, false>(ta, tb, tcm, tx, g, st);
-    case 1: return launch<128, false, true>(ta, tb, tcm, tx, g, st);
-    case 2: return launch<128, true, false>(ta, tb, tcm, tx, g, st);
-    case 3: return launch<128, true, true>(ta, tb, tcm, tx, g, st);
-    case 4: return launch<256, false, false>(ta, tb, tcm, tx, g, st);
-    case 5: return launch<256, false, true>(ta, tb, tcm, tx, g, st);
-    case 6: return launch<256, true, false>(ta, tb, tcm, tx, g, st);
-    default: return launch<256, true, true>(ta, tb, tcm, tx, g, st);
+    case 0: return launch<128, false, false, 0>(ta, tb, tcm, tx, g, st);
+    case 1: return launch<128, false, true, 0>(ta, tb, tcm, tx, g, st);
+    case 2: return launch<128, true, false, 0>(ta, tb, tcm, tx, g, st);
+    case 3: return launch<128, true, true, 0>(ta, tb, tcm, tx, g, st);
+    case 4: return launch<256, false, false, 0>(ta, tb, tcm, tx, g, st);
+    case 5: return launch<256, false, true, 0>(ta, tb, tcm, tx, g, st);
+    case 6: return launch<256, true, false, 0>(ta, tb, tcm, tx, g, st);
+    default: return launch<256, true, true, 0>(ta, tb, tcm, tx, g, st);
   }
 }
