@@ -51,7 +51,7 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? (EK ? 3 : 4) : 6;
   // EK 0: plain; 1: bf16 aux read (residual / GELU pre-activation); 2: second bf16 output (BIAS_GELU)
-  static constexpr int SSLOTS = EK == 0 ? 2 : (EK == 1 ? 4 : 10);  // TMA-store staging slots per epilogue warp
+  static constexpr int SSLOTS = EK == 0 ? 2 : (EK == 1 ? 4 : 8);   // TMA-store staging slots per epilogue warp
   static constexpr int XSLOTS = EK == 0 ? 2 : (EK == 1 ? 6 : 1);   // TMA-load aux ring slots per epilogue warp
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_BYTES = (SSLOTS + XSLOTS) * 4 * 2048;  // per epilogue warp: store + aux slots of 2 KB
