@@ -26,7 +26,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;   // warps 0-3 producer/MMA/alloc/spare, warps 4-11 epilogue
+constexpr int kEpiWarps = 8;
 
 struct GemmArgs {
   void* C;
@@ -51,10 +52,10 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? (EK ? 3 : 4) : 6;
   // EK 0: plain; 1: bf16 aux read (residual / GELU pre-activation); 2: second bf16 output (BIAS_GELU)
-  static constexpr int SSLOTS = EK == 0 ? 2 : (EK == 1 ? 4 : 8);   // TMA-store staging slots per epilogue warp
-  static constexpr int XSLOTS = EK == 0 ? 2 : (EK == 1 ? 6 : 1);   // TMA-load aux ring slots per epilogue warp
+  static constexpr int SSLOTS = EK == 0 ? 2 : (EK == 1 ? 2 : 4);  // TMA-store staging slots per epilogue warp
+  static constexpr int XSLOTS = EK == 1 ? 3 : 1;                   // TMA-load aux ring slots per epilogue warp
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int EPI_BYTES = (SSLOTS + XSLOTS) * 4 * 2048;  // per epilogue warp: store + aux slots of 2 KB
+  static constexpr int EPI_BYTES = (SSLOTS + (EK == 1 ? XSLOTS : 0)) * kEpiWarps * 2048;  // 2 KB slots per epilogue warp
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static_assert(SMEM <= 232448, "gemm smem");
   static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
@@ -181,8 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* aux_bar = tempty + 2;  // [4 warps][XSLOTS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4 * C::XSLOTS);
+  uint64_t* aux_bar = tempty + 2;  // [kEpiWarps][XSLOTS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps * C::XSLOTS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.num_m * a.num_n * a.splits;
@@ -198,9 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 4);
+      tc::mbar_init(&tempty[s], kEpiWarps);
     }
-    for (int s = 0; s < 4 * C::XSLOTS; ++s) tc::mbar_init(&aux_bar[s], 1);
+    for (int s = 0; s < kEpiWarps * C::XSLOTS; ++s) tc::mbar_init(&aux_bar[s], 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -282,19 +283,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue
-    const int ew = warp & 3;
+    // warp w: TMEM lane quadrant (w & 3) = rows 32q..32q+31, column half (w-4)/4 of the tile
+    const int ew = warp & 3, eh = (warp - 4) >> 2, ei = warp - 4;
     constexpr int SS = C::SSLOTS, XS = C::XSLOTS;
-    uint8_t* stg = smem_epi + ew * SS * 2048;                    // TMA-store staging slots
-    uint8_t* axs = smem_epi + 4 * SS * 2048 + ew * XS * 2048;    // TMA-loaded aux ring
-    uint64_t* axb = aux_bar + ew * XS;
+    constexpr int NCH = BN / 64;                       // 32-column chunks per warp
+    uint8_t* stg = smem_epi + ei * SS * 2048;                            // TMA-store staging slots
+    uint8_t* axs = smem_epi + kEpiWarps * SS * 2048 + ei * XS * 2048;    // TMA-loaded aux ring
+    uint64_t* axb = aux_bar + ei * XS;
     int sbuf = 0;
     uint32_t auxc = 0;                                 // aux chunks consumed (ring position)
-    constexpr int NCH = BN / 32;
-    const bool tma_aux = a.tma_aux != 0;
+    const bool tma_aux = (EK == 1) && a.tma_aux != 0;
+    const uint32_t tlane = (uint32_t)(ew * 32) << 16;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int mn = t % (a.num_m * a.num_n);
-      const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN;
+      const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN + eh * (BN / 2);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int row0 = m0 + ew * 32;
@@ -310,11 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int row = row0 + lane;
-#pragma unroll 1
+      const uint32_t tbase = tmem + acc * BN + tlane + eh * (BN / 2);
+      uint32_t rbuf[2][32];
+      tc::tmem_ld_32x32b_x32(tbase, rbuf[0]);
+#pragma unroll
       for (int c = 0; c < NCH; ++c) {
         const int col = n0 + c * 32;
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tmem + acc * BN + ((uint32_t)(ew * 32) << 16) + c * 32, r);
+        uint32_t (&r)[32] = rbuf[c & 1];
+        tc::tmem_ld_wait();
+        if (c + 1 < NCH) tc::tmem_ld_32x32b_x32(tbase + (c + 1) * 32, rbuf[(c + 1) & 1]);  // overlap next load
         float xa[32];
         if (tma_aux) {
           const int slot = auxc % XS;
@@ -340,7 +347,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ++auxc;
         }
-        tc::tmem_ld_wait();
         if (col >= a.N) continue;
         float v[32];
 #pragma unroll
@@ -394,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   if (warp >= 4 && a.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
   __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
@@ -583,7 +590,8 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
     if (s1 == AVB_OK && s2 == AVB_OK) g.tma_out = 1;
   }
   g.tma_aux = 0;
-  if (g.vec_ok && aux && (epilogue == AVB_EPI_BF16 || epilogue == AVB_EPI_DGELU) && !getenv("AVB_GEMM_NO_TMA_AUX")) {
+  if (g.vec_ok && aux && (epilogue == AVB_EPI_BF16 || epilogue == AVB_EPI_DGELU) && a_major == 0 && N > 128 &&
+      !getenv("AVB_GEMM_NO_TMA_AUX")) {
     if (avb::make_tmap_2d_bf16_sw(&tx, aux, N, M, ldaux, 32, 32, 64) == AVB_OK) g.tma_aux = 1;
   }
   cudaStream_t st = avb::as_stream(stream);
