@@ -74,7 +74,9 @@ __device__ __forceinline__ void store_row_chunk(const GemmArgs& a, int row, int 
                      "f"(v[j + 2]), "f"(v[j + 3])
                      : "memory");
     } else {
-      for (int j = 0; j < 32 && col + j < a.N; ++j) atomicAdd(c + j, v[j]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < a.N) atomicAdd(c + j, v[j]);
     }
     return;
   }
@@ -84,7 +86,9 @@ __device__ __forceinline__ void store_row_chunk(const GemmArgs& a, int row, int 
 #pragma unroll
       for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     } else {
-      for (int j = 0; j < 32 && col + j < a.N; ++j) c[j] = v[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < a.N) c[j] = v[j];
     }
     return;
   }
@@ -100,7 +104,9 @@ __device__ __forceinline__ void store_row_chunk(const GemmArgs& a, int row, int 
       *reinterpret_cast<uint4*>(c + j) = q;
     }
   } else {
-    for (int j = 0; j < 32 && col + j < a.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col + j < a.N) c[j] = __float2bfloat16_rn(v[j]);
   }
 }
 
@@ -138,7 +144,9 @@ __device__ __forceinline__ void store_aux_chunk(const GemmArgs& a, int row, int 
       *reinterpret_cast<uint4*>(c + j) = q;
     }
   } else {
-    for (int j = 0; j < 32 && col + j < a.N; ++j) c[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col + j < a.N) c[j] = __float2bfloat16_rn(v[j]);
   }
 }
 

@@ -1,0 +1,17 @@
+"""Single launches of the fc1 bias+GELU GEMM and the plain QKV GEMM (for ncu)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2309_16669_b200 import ops
+M, D = 64 * 1569, 768
+x = torch.randn(M, D, device="cuda").to(torch.bfloat16)
+w1 = torch.randn(4 * D, D, device="cuda").to(torch.bfloat16)
+wq = torch.randn(3 * D, D, device="cuda").to(torch.bfloat16)
+b1 = torch.randn(4 * D, device="cuda")
+pre = torch.empty(M, 4 * D, device="cuda", dtype=torch.bfloat16)
+act = torch.empty(M, 4 * D, device="cuda", dtype=torch.bfloat16)
+q = torch.empty(M, 3 * D, device="cuda", dtype=torch.bfloat16)
+for _ in range(3):
+    ops.gemm(x, w1, bias=b1, epilogue=ops.EPI_BIAS_GELU, aux_out=pre, out=act)
+    ops.gemm(x, wq, out=q)
+torch.cuda.synchronize()
