@@ -164,6 +164,17 @@ int avb_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, const 
               void* stream);
 int avb_cast_bf16(const float* src, void* dst, int64_t n, void* stream);
 
+/*
+ * K7: CLIP InfoNCE over a global batch. v, t: fp32 [Bg, E] raw (un-normalised)
+ * embeddings; S = s * v^ t^T.  fwd: norms [Bg], row/col LSE [Bg]; loss += L; dscale += dL/ds.
+ * bwd: dv, dt [n, E] (=) grad_scale * dL/d(raw) for global rows / columns [r0, r0+n).
+ */
+int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, float logit_scale, float* norms_v,
+                    float* norms_t, float* lse_r, float* lse_c, float* loss, float* dscale, void* stream);
+int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, float logit_scale,
+                    const float* norms_v, const float* norms_t, const float* lse_r, const float* lse_c,
+                    int r0, int n, float grad_scale, float* dv, float* dt, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -185,3 +185,35 @@ def adamw(p, g, m, v, p_bf16, lr, beta1, beta2, eps, wd, step, grad_scale=1.0, d
 
 def cast_bf16(src, dst):
     _lib.check(_lib.load().avb_cast_bf16(src.data_ptr(), dst.data_ptr(), src.numel(), _lib.stream_ptr()), "cast_bf16")
+
+
+# ----------------------------------------------------------------------------- InfoNCE
+def infonce(v: torch.Tensor, t: torch.Tensor, logit_scale: float, r0: int = 0, n: int | None = None,
+            grad_scale: float = 1.0):
+    """CLIP loss over the global batch v, t [Bg, E] fp32 (raw embeddings).
+
+    Returns (loss [1], dscale [1], dv [n, E], dt [n, E]) with dv/dt the gradients of the
+    rows/columns [r0, r0+n) scaled by grad_scale.
+    """
+    if v.dtype != torch.float32 or t.dtype != torch.float32 or v.shape != t.shape or not v.is_contiguous() \
+            or not t.is_contiguous():
+        raise InputError("v, t must be contiguous fp32 [Bg, E] of equal shape")
+    Bg, E = v.shape
+    n = Bg - r0 if n is None else n
+    dev = v.device
+    nv = torch.empty(Bg, device=dev)
+    nt = torch.empty(Bg, device=dev)
+    lr = torch.empty(Bg, device=dev)
+    lc = torch.empty(Bg, device=dev)
+    loss = torch.zeros(1, device=dev)
+    ds = torch.zeros(1, device=dev)
+    dv = torch.empty(n, E, device=dev)
+    dt = torch.empty(n, E, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.avb_infonce_fwd(v.data_ptr(), t.data_ptr(), Bg, E, float(logit_scale), nv.data_ptr(),
+                                   nt.data_ptr(), lr.data_ptr(), lc.data_ptr(), loss.data_ptr(), ds.data_ptr(),
+                                   _lib.stream_ptr()), "infonce_fwd")
+    _lib.check(lib.avb_infonce_bwd(v.data_ptr(), t.data_ptr(), Bg, E, float(logit_scale), nv.data_ptr(),
+                                   nt.data_ptr(), lr.data_ptr(), lc.data_ptr(), int(r0), int(n), float(grad_scale),
+                                   dv.data_ptr(), dt.data_ptr(), _lib.stream_ptr()), "infonce_bwd")
+    return loss, ds, dv, dt
