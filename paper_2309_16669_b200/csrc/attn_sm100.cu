@@ -51,11 +51,16 @@ struct FwdArgs {
   int causal;
 };
 
-constexpr int F_SQ = 0, F_SKV = 16384, F_SP = F_SKV + 2 * 32768, F_TILES = F_SP + 32768;
+constexpr int F_STAGES = 3;
+constexpr int F_SQ = 0, F_SKV = 16384, F_TILES = F_SKV + F_STAGES * 32768;
 // barriers live in the first 128 B of the dynamic window, tiles start at the next 1 KB boundary;
 // 115712 B = (228 KB - 2 x 1 KB reserved) / 2 keeps two CTAs per SM.
 constexpr int F_SMEM = F_TILES + 1024;
 static_assert(F_SMEM <= 115712, "attn fwd must fit two CTAs per SM");
+
+// TMEM columns per CTA (2 CTAs/SM -> 256 each): S fp32 [0,128), P bf16x2 [128,192), O fp32 [192,256)
+constexpr uint32_t T_S = 0, T_P = 128, T_O = 192;
+constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only when the running max grows by > 2^8
 
 __global__ void __launch_bounds__(192, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -65,15 +70,15 @@ __global__ void __launch_bounds__(192, 2)
   if (smem + F_TILES > smem_raw + F_SMEM) __trap();  // dynamic smem base not 1 KB aligned
   uint8_t* sQ = smem + F_SQ;
   uint8_t* sKV = smem + F_SKV;
-  uint8_t* sP = smem + F_SP;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* o_full = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* kv_full = bars + 1;              // [F_STAGES]
+  uint64_t* kv_empty = bars + 1 + F_STAGES;  // [F_STAGES]
+  uint64_t* s_full = bars + 1 + 2 * F_STAGES;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = s_full + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -86,11 +91,12 @@ __global__ void __launch_bounds__(192, 2)
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < F_STAGES; ++s) {
       tc::mbar_init(&kv_full[s], 1);
       tc::mbar_init(&kv_empty[s], 1);
     }
     tc::mbar_init(s_full, 1);
+    tc::mbar_init(s_free, 4);
     tc::mbar_init(p_full, 4);
     tc::mbar_init(o_full, 1);
     tc::fence_barrier_init();
@@ -100,15 +106,14 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + 128;
 
   if (warp == 4) {
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(q_full, 16384);
       tc::tma_load_3d(sQ, &tmQ, q_full, h * HD, q0, b);
       for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        tc::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % F_STAGES;
+        tc::mbar_wait(&kv_empty[st], ((j / F_STAGES) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&kv_full[st], 32768);
         tc::tma_load_3d(sKV + st * 32768, &tmK, &kv_full[st], h * HD, j * BT, b);
         tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
@@ -117,134 +122,131 @@ __global__ void __launch_bounds__(192, 2)
   } else if (warp == 5) {
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16_f32(128, 128, 0, 0);
-      constexpr uint32_t idO = tc::idesc_bf16_f32(128, 64, 0, 1);
-      const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
+      constexpr uint32_t idO = tc::idesc_bf16_f32(128, 64, 0, 1);   // A = P from TMEM, B = V MN-major
+      const uint32_t aQ = smem_u32(sQ);
+      auto issue_s = [&](int j) {
+        const int st = j % F_STAGES;
+        tc::mbar_wait(&kv_full[st], (j / F_STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t aK = smem_u32(sKV + st * 32768);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tmem + T_S, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024),
+                          idS, kk > 0);
+        tc::umma_commit(s_full);
+      };
       tc::mbar_wait(q_full, 0);
-      for (int j = 0; j <= nkv; ++j) {
-        if (j < nkv) {
-          const int st = j & 1;
-          tc::mbar_wait(&kv_full[st], (j >> 1) & 1);
-          if (j > 0) tc::mbar_wait(p_full, (j - 1) & 1);
-          tc::tc_fence_after();
-          const uint32_t aK = smem_u32(sKV + st * 32768);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::umma_f16_ss(tS, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024), idS,
-                            kk > 0);
-          tc::umma_commit(s_full);
-        } else {
-          tc::mbar_wait(p_full, (j - 1) & 1);
-          tc::tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) {
+          tc::mbar_wait(s_free, j & 1);  // softmax has S(j) in registers
+          issue_s(j + 1);
         }
-        if (j > 0) {
-          const int ps = (j - 1) & 1;
-          const uint32_t aV = smem_u32(sKV + ps * 32768 + 16384);
+        tc::mbar_wait(p_full, j & 1);
+        tc::tc_fence_after();
+        const int st = j % F_STAGES;
+        const uint32_t aV = smem_u32(sKV + st * 32768 + 16384);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            tc::umma_f16_ss(tO, tc::sdesc_sw128(aP + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                            tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO, kk > 0);
-          tc::umma_commit(o_full);
-          tc::umma_commit(&kv_empty[ps]);
-        }
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ts(tmem + T_O, tmem + T_P + kk * 8, tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO,
+                          (j > 0 || kk > 0) ? 1u : 0u);
+        tc::umma_commit(o_full);
+        tc::umma_commit(&kv_empty[st]);
       }
     }
   } else {
-    // ---------------------------------------------------------------- softmax warps
+    // ---------------------------------------------------------------- softmax warps (thread = query row)
     const int row = warp * 32 + lane;
     const int qi = q0 + row;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    float o[HD];
-#pragma unroll
-    for (int e = 0; e < HD; ++e) o[e] = 0.f;
-
+    float m_run = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       tc::mbar_wait(s_full, j & 1);
       tc::tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tc::tmem_ld_32x32b_x32(tmem + T_S + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(s_free);
       const int kv0 = j * BT;
-      int lim = a.N - kv0;                       // valid key columns in this tile
+      int lim = a.N - kv0;
       if (a.causal) lim = min(lim, qi - kv0 + 1);
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tS + lane_off + c * 32, r);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (c * 32 + e < lim) mx = fmaxf(mx, __uint_as_float(r[e]));
-      }
-      const float m_new = fmaxf(m, mx * a.scale_log2);
-      const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-      const float alpha = (m == -INFINITY) ? 0.f : ex2(m - m_use);
-      if (j > 0) {
+      for (int e = 0; e < 128; ++e)
+        if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
+      const float m_new = fmaxf(m_run, mx * a.scale_log2);
+      // warp-uniform lazy rescale of the TMEM accumulator (tcgen05.ld/st are warp-collective)
+      const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + kRescaleThresh);
+      if (j > 0 && __any_sync(0xffffffff, need)) {
+        const float alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
         tc::mbar_wait(o_full, (j - 1) & 1);
         tc::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
-          tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+          tc::tmem_ld_32x32b_x32(tmem + T_O + lane_off + c * 32, r);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[c * 32 + e] = fmaf(o[c * 32 + e], alpha_prev, __uint_as_float(r[e]));
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          tc::tmem_st_32x32b_x32(tmem + T_O + lane_off + c * 32, r);
         }
+        tc::tmem_st_wait();
+        l *= alpha;
+        m_run = m_new;
+      } else if (j == 0) {
+        m_run = m_new;
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      if (j > 0) {
+        tc::mbar_wait(o_full, (j - 1) & 1);  // PV(j-1) has finished reading P
+        tc::tc_fence_after();
       }
       float sum = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tS + lane_off + c * 32, r);
-        tc::tmem_ld_wait();
+        uint32_t pk[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float p[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int col = c * 32 + u * 8 + e;
-            const float pe = (col < lim) ? ex2(fmaf(__uint_as_float(r[u * 8 + e]), a.scale_log2, -m_use)) : 0.f;
-            p[e] = pe;
-            sum += pe;
-          }
-          uint4 v;
-          v.x = pack_bf16x2(p[0], p[1]);
-          v.y = pack_bf16x2(p[2], p[3]);
-          v.z = pack_bf16x2(p[4], p[5]);
-          v.w = pack_bf16x2(p[6], p[7]);
-          st_sw128(sP, row, c * 4 + u, v);
+        for (int e = 0; e < 32; e += 2) {
+          const int col = c * 32 + e;
+          const float p0 = (col < lim) ? ex2(fmaf(__uint_as_float(sr[col]), a.scale_log2, -m_use)) : 0.f;
+          const float p1 = (col + 1 < lim) ? ex2(fmaf(__uint_as_float(sr[col + 1]), a.scale_log2, -m_use)) : 0.f;
+          sum += p0 + p1;
+          pk[e >> 1] = pack_bf16x2(p0, p1);
         }
+        tc::tmem_st_32x32b_x16(tmem + T_P + lane_off + c * 16, pk);
       }
-      l = fmaf(l, alpha, sum);
-      tc::fence_proxy_async();
+      l += sum;
+      tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full);
-      alpha_prev = alpha;
-      m = m_new;
     }
     tc::mbar_wait(o_full, (nkv - 1) & 1);
     tc::tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = a.o + (int64_t)b * a.sb_o + (int64_t)qi * a.ld_o + h * HD;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       uint32_t r[32];
-      tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+      tc::tmem_ld_32x32b_x32(tmem + T_O + lane_off + c * 32, r);
       tc::tmem_ld_wait();
+      if (qi < a.N) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) o[c * 32 + e] = fmaf(o[c * 32 + e], alpha_prev, __uint_as_float(r[e]));
-    }
-    if (qi < a.N) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* dst = a.o + (int64_t)b * a.sb_o + (int64_t)qi * a.ld_o + h * HD;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        uint4 v;
-        v.x = pack_bf16x2(o[u * 8 + 0] * inv, o[u * 8 + 1] * inv);
-        v.y = pack_bf16x2(o[u * 8 + 2] * inv, o[u * 8 + 3] * inv);
-        v.z = pack_bf16x2(o[u * 8 + 4] * inv, o[u * 8 + 5] * inv);
-        v.w = pack_bf16x2(o[u * 8 + 6] * inv, o[u * 8 + 7] * inv);
-        reinterpret_cast<uint4*>(dst)[u] = v;
+        for (int u = 0; u < 4; ++u) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * inv, __uint_as_float(r[u * 8 + 1]) * inv);
+          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * inv, __uint_as_float(r[u * 8 + 3]) * inv);
+          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * inv, __uint_as_float(r[u * 8 + 5]) * inv);
+          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * inv, __uint_as_float(r[u * 8 + 7]) * inv);
+          reinterpret_cast<uint4*>(dst + c * 32)[u] = v;
+        }
       }
-      a.lse[(int64_t)(b * a.H + h) * a.Npad + qi] = (l > 0.f) ? (m + __log2f(l)) * kLn2 : -INFINITY;
     }
+    if (qi < a.N) a.lse[(int64_t)(b * a.H + h) * a.Npad + qi] = (l > 0.f) ? (m_run + __log2f(l)) * kLn2 : -INFINITY;
   }
   tc::tc_fence_before();
   __syncthreads();

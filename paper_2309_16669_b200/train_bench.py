@@ -62,8 +62,6 @@ def golden_boxes(n: int, offset: int = 0):
 
 
 def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
-    import torch.distributed as dist
-
     cfg = CONFIG4_VIT_B_16F
     B = CLIPS_PER_GPU
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -103,17 +101,11 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
             f = timer.wrap(n, f, keyfn=gemm_key)
         setattr(ops, n, f)
 
-    store = model.store
-    group_order = list(store.groups)
-    handles = []
+    from .dp import GradBucketReducer
 
-    def on_layer_done(group):
-        if world == 1:
-            return
-        names = [group] if group in store.groups else []
-        for gname in names:
-            a, b = store.group_slice(gname)
-            handles.append(dist.all_reduce(store.grad[a:b], async_op=True))
+    store = model.store
+    reducer = GradBucketReducer(store.grad, {g: store.group_slice(g) for g in store.groups})
+    on_layer_done = reducer.on_layer_done
 
     from . import transform as TR
 
@@ -124,9 +116,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
         TR.transform(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet",
                      tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
         model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
-        for h in handles:
-            h.wait()
-        handles.clear()
+        reducer.finish()
         model.optimizer_step(grad_scale=1.0 / world)
 
     for _ in range(args.warmup):
