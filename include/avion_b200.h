@@ -166,14 +166,25 @@ int avb_cast_bf16(const float* src, void* dst, int64_t n, void* stream);
 
 /*
  * K7: CLIP InfoNCE over a global batch. v, t: fp32 [Bg, E] raw (un-normalised)
- * embeddings; S = s * v^ t^T.  fwd: norms [Bg], row/col LSE [Bg]; loss += L; dscale += dL/ds.
+ * embeddings; S = s * v^ t^T with s = exp(min(*log_scale, ln 100)) read on the device (no host sync).
+ * fwd: norms [Bg], row/col LSE [Bg]; loss += L; dlog_scale (nullable) += dL/dlog_scale.
  * bwd: dv, dt [n, E] (=) grad_scale * dL/d(raw) for global rows / columns [r0, r0+n).
  */
-int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, float logit_scale, float* norms_v,
-                    float* norms_t, float* lse_r, float* lse_c, float* loss, float* dscale, void* stream);
-int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, float logit_scale,
+int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, const float* log_scale, float* norms_v,
+                    float* norms_t, float* lse_r, float* lse_c, float* loss, float* dlog_scale, void* stream);
+int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, const float* log_scale,
                     const float* norms_v, const float* norms_t, const float* lse_r, const float* lse_c,
                     int r0, int n, float grad_scale, float* dv, float* dt, void* stream);
+
+/* text-side token embedding: x[b*L+l] = table[tok] + pos[l] (bf16 out); bwd: dtable[tok] += dx (atomic),
+ * dpos[l] += sum_b dx.  Out-of-range ids are clamped to [0, V). */
+int avb_embed_fwd(const int32_t* tokens, const float* table, const float* pos, void* x, int B, int L, int D,
+                  int V, void* stream);
+int avb_embed_bwd(const int32_t* tokens, const void* dx, float* dtable, float* dpos, int B, int L, int D,
+                  int V, void* stream);
+/* bf16 row gather/scatter: dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i], i < n */
+int avb_rows_copy(const void* src, int64_t lds, const int32_t* src_idx, void* dst, int64_t ldd,
+                  const int32_t* dst_idx, int n, int D, void* stream);
 
 #ifdef __cplusplus
 }

@@ -42,9 +42,12 @@ EXPORTS: dict[str, tuple] = {
     "avb_adamw": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, _i32,
                          C.c_float, _vp]),
     "avb_cast_bf16": (_i32, [_vp, _vp, _i64, _vp]),
-    "avb_infonce_fwd": (_i32, [_vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "avb_infonce_bwd": (_i32, [_vp, _vp, _i32, _i32, C.c_float, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp,
+    "avb_infonce_fwd": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "avb_infonce_bwd": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp,
                                _vp]),
+    "avb_embed_fwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "avb_embed_bwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "avb_rows_copy": (_i32, [_vp, _i64, _vp, _vp, _i64, _vp, _i32, _i32, _vp]),
     "avb_gemm": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp,
                         C.c_float, _i32, _vp]),
     "avb_attn_fwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _i32, C.c_float,

@@ -52,41 +52,39 @@ struct FwdArgs {
 };
 
 constexpr int F_STAGES = 3;
-constexpr int F_SQ = 0, F_SKV = 16384, F_TILES = F_SKV + F_STAGES * 32768;
-// barriers live in the first 128 B of the dynamic window, tiles start at the next 1 KB boundary;
-// 115712 B = (228 KB - 2 x 1 KB reserved) / 2 keeps two CTAs per SM.
-constexpr int F_SMEM = F_TILES + 1024;
-static_assert(F_SMEM <= 115712, "attn fwd must fit two CTAs per SM");
+constexpr int F_SQ = 0;                               // 2 Q tiles (A, B) x 16 KB
+constexpr int F_SKV = 32768;                          // F_STAGES x (K 16 KB + V 16 KB)
+constexpr int F_BAR = F_SKV + F_STAGES * 32768;
+constexpr int F_SMEM = F_BAR + 256;
+static_assert(F_SMEM <= 232448, "attn fwd smem");
 
-// TMEM columns per CTA (2 CTAs/SM -> 256 each): S fp32 [0,128), P bf16x2 [128,192), O fp32 [192,256)
-constexpr uint32_t T_S = 0, T_P = 128, T_O = 192;
+// TMEM (512 columns, 1 CTA/SM), per query tile g in {0,1}:
+//   S_g fp32 [128g*... ] at 128*g, P_g bf16x2 at 256 + 64*g, O_g fp32 at 384 + 64*g
 constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only when the running max grows by > 2^8
 
-__global__ void __launch_bounds__(192, 2)
+__global__ void __launch_bounds__(320, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 128 + 1023) & ~uintptr_t(1023));
-  if (smem + F_TILES > smem_raw + F_SMEM) __trap();  // dynamic smem base not 1 KB aligned
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
   uint8_t* sQ = smem + F_SQ;
   uint8_t* sKV = smem + F_SKV;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + F_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;              // [F_STAGES]
   uint64_t* kv_empty = bars + 1 + F_STAGES;  // [F_STAGES]
-  uint64_t* s_full = bars + 1 + 2 * F_STAGES;
-  uint64_t* s_free = s_full + 1;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_full = s_full + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
+  uint64_t* gb = bars + 1 + 2 * F_STAGES;    // per group g: s_full, s_free, p_full, o_full at gb + 4g
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gb + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qt * BT;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * 2 * BT;
+  const bool hasB = q0 + BT < a.N;
+  const int ng = hasB ? 2 : 1;
   const int nkv_all = (a.N + BT - 1) / BT;
-  const int nkv = a.causal ? min(nkv_all, qt + 1) : nkv_all;
+  const int nkv = a.causal ? min(nkv_all, (q0 + ng * BT - 1) / BT + 1) : nkv_all;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tc::tma_prefetch(&tmQ);
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
@@ -95,22 +93,25 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_init(&kv_full[s], 1);
       tc::mbar_init(&kv_empty[s], 1);
     }
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(s_free, 4);
-    tc::mbar_init(p_full, 4);
-    tc::mbar_init(o_full, 1);
+    for (int g = 0; g < 2; ++g) {
+      tc::mbar_init(gb + 4 * g + 0, 1);  // s_full
+      tc::mbar_init(gb + 4 * g + 1, 4);  // s_free
+      tc::mbar_init(gb + 4 * g + 2, 4);  // p_full
+      tc::mbar_init(gb + 4 * g + 3, 1);  // o_full
+    }
     tc::fence_barrier_init();
   }
-  if (warp == 5) tc::tmem_alloc(tmem_slot, 256);
+  if (warp == 9) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
-      tc::mbar_arrive_expect_tx(q_full, 16384);
+      tc::mbar_arrive_expect_tx(q_full, 16384 * ng);
       tc::tma_load_3d(sQ, &tmQ, q_full, h * HD, q0, b);
+      if (hasB) tc::tma_load_3d(sQ + 16384, &tmQ, q_full, h * HD, q0 + BT, b);
       for (int j = 0; j < nkv; ++j) {
         const int st = j % F_STAGES;
         tc::mbar_wait(&kv_empty[st], ((j / F_STAGES) & 1) ^ 1);
@@ -119,140 +120,155 @@ __global__ void __launch_bounds__(192, 2)
         tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16_f32(128, 64, 0, 1);   // A = P from TMEM, B = V MN-major
       const uint32_t aQ = smem_u32(sQ);
-      auto issue_s = [&](int j) {
-        const int st = j % F_STAGES;
-        tc::mbar_wait(&kv_full[st], (j / F_STAGES) & 1);
-        tc::tc_fence_after();
-        const uint32_t aK = smem_u32(sKV + st * 32768);
+      auto issue_s = [&](int g, int j) {
+        const uint32_t aK = smem_u32(sKV + (j % F_STAGES) * 32768);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + T_S, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024),
-                          idS, kk > 0);
-        tc::umma_commit(s_full);
+          tc::umma_f16_ss(tmem + 128 * g, tc::sdesc_sw128(aQ + g * 16384 + kk * 32, 16, 1024),
+                          tc::sdesc_sw128(aK + kk * 32, 16, 1024), idS, kk > 0);
+        tc::umma_commit(gb + 4 * g + 0);
       };
-      tc::mbar_wait(q_full, 0);
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) {
-          tc::mbar_wait(s_free, j & 1);  // softmax has S(j) in registers
-          issue_s(j + 1);
-        }
-        tc::mbar_wait(p_full, j & 1);
-        tc::tc_fence_after();
-        const int st = j % F_STAGES;
-        const uint32_t aV = smem_u32(sKV + st * 32768 + 16384);
+      auto issue_pv = [&](int g, int j) {
+        const uint32_t aV = smem_u32(sKV + (j % F_STAGES) * 32768 + 16384);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts(tmem + T_O, tmem + T_P + kk * 8, tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO,
-                          (j > 0 || kk > 0) ? 1u : 0u);
-        tc::umma_commit(o_full);
-        tc::umma_commit(&kv_empty[st]);
+          tc::umma_f16_ts(tmem + 384 + 64 * g, tmem + 256 + 64 * g + kk * 8,
+                          tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+        tc::umma_commit(gb + 4 * g + 3);
+      };
+      tc::mbar_wait(q_full, 0);
+      tc::mbar_wait(&kv_full[0], 0);
+      tc::tc_fence_after();
+      for (int g = 0; g < ng; ++g) issue_s(g, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool more = j + 1 < nkv;
+        if (more) tc::mbar_wait(&kv_full[(j + 1) % F_STAGES], ((j + 1) / F_STAGES) & 1);
+        for (int g = 0; g < ng; ++g) {
+          tc::mbar_wait(gb + 4 * g + 2, j & 1);    // P_g(j) in TMEM, S_g(j) consumed
+          tc::tc_fence_after();
+          issue_pv(g, j);
+          if (more) issue_s(g, j + 1);
+        }
+        tc::umma_commit(&kv_empty[j % F_STAGES]);
       }
     }
   } else {
-    // ---------------------------------------------------------------- softmax warps (thread = query row)
-    const int row = warp * 32 + lane;
-    const int qi = q0 + row;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    float m_run = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      tc::mbar_wait(s_full, j & 1);
-      tc::tc_fence_after();
-      uint32_t sr[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tc::tmem_ld_32x32b_x32(tmem + T_S + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-      tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(s_free);
-      const int kv0 = j * BT;
-      int lim = a.N - kv0;
-      if (a.causal) lim = min(lim, qi - kv0 + 1);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < 128; ++e)
-        if (e < lim) mx = fmaxf(mx, __uint_as_float(sr[e]));
-      const float m_new = fmaxf(m_run, mx * a.scale_log2);
-      // warp-uniform lazy rescale of the TMEM accumulator (tcgen05.ld/st are warp-collective)
-      const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + kRescaleThresh);
-      if (j > 0 && __any_sync(0xffffffff, need)) {
-        const float alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
-        tc::mbar_wait(o_full, (j - 1) & 1);
+    // ---------------------------------------------------------------- softmax groups (thread = query row)
+    const int g = warp >> 2, quad = warp & 3;
+    if (g < ng) {
+      uint64_t* s_full = gb + 4 * g;
+      uint64_t* p_full = s_full + 2;
+      uint64_t* o_full = s_full + 3;
+      const uint32_t tS = tmem + 128 * g, tP = tmem + 256 + 64 * g, tO = tmem + 384 + 64 * g;
+      const int row = quad * 32 + lane;
+      const int qi = q0 + g * BT + row;
+      const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      float m_run = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        tc::mbar_wait(s_full, j & 1);
         tc::tc_fence_after();
+        const int kv0 = j * BT;
+        int lim = a.N - kv0;
+        if (a.causal) lim = min(lim, qi - kv0 + 1);
+        // pass 1: row max (two TMEM round trips of 64 columns)
+        float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld_32x32b_x32(tmem + T_O + lane_off + c * 32, r);
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t r0[32], r1[32];
+          tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64, r0);
+          tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64 + 32, r1);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tc::tmem_st_32x32b_x32(tmem + T_O + lane_off + c * 32, r);
+          for (int e = 0; e < 32; ++e) {
+            if (hh * 64 + e < lim) mx = fmaxf(mx, __uint_as_float(r0[e]));
+            if (hh * 64 + 32 + e < lim) mx = fmaxf(mx, __uint_as_float(r1[e]));
+          }
         }
+        const float m_new = fmaxf(m_run, mx * a.scale_log2);
+        if (j > 0) {
+          tc::mbar_wait(o_full, (j - 1) & 1);  // PV(j-1) done: O stable, P buffer free
+          tc::tc_fence_after();
+        }
+        // warp-uniform lazy rescale of the TMEM accumulator (tcgen05.ld/st are warp-collective)
+        const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + kRescaleThresh);
+        if (j > 0 && __any_sync(0xffffffff, need)) {
+          const float alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            tc::tmem_st_32x32b_x32(tO + lane_off + c * 32, r);
+          }
+          l *= alpha;
+          m_run = m_new;
+        } else if (j == 0) {
+          m_run = m_new;
+        }
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        // pass 2: p = exp2(s*scale - m), row sum, bf16 pack straight into the TMEM P tile
+        float sum = 0.f;
+        uint32_t rb[2][32];
+        tc::tmem_ld_32x32b_x32(tS + lane_off, rb[0]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          tc::tmem_ld_wait();
+          if (c + 1 < 4) tc::tmem_ld_32x32b_x32(tS + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int col = c * 32 + e;
+            const float p0 = (col < lim) ? ex2(fmaf(__uint_as_float(rb[c & 1][e]), a.scale_log2, -m_use)) : 0.f;
+            const float p1 =
+                (col + 1 < lim) ? ex2(fmaf(__uint_as_float(rb[c & 1][e + 1]), a.scale_log2, -m_use)) : 0.f;
+            sum += p0 + p1;
+            pk[e >> 1] = pack_bf16x2(p0, p1);
+          }
+          tc::tmem_st_32x32b_x16(tP + lane_off + c * 16, pk);
+        }
+        l += sum;
         tc::tmem_st_wait();
-        l *= alpha;
-        m_run = m_new;
-      } else if (j == 0) {
-        m_run = m_new;
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_full);   // also frees S_g for S_g(j+1)
       }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      if (j > 0) {
-        tc::mbar_wait(o_full, (j - 1) & 1);  // PV(j-1) has finished reading P
-        tc::tc_fence_after();
-      }
-      float sum = 0.f;
+      tc::mbar_wait(o_full, (nkv - 1) & 1);
+      tc::tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* dst = a.o + (int64_t)b * a.sb_o + (int64_t)qi * a.ld_o + h * HD;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+        tc::tmem_ld_wait();
+        if (qi < a.N) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = c * 32 + e;
-          const float p0 = (col < lim) ? ex2(fmaf(__uint_as_float(sr[col]), a.scale_log2, -m_use)) : 0.f;
-          const float p1 = (col + 1 < lim) ? ex2(fmaf(__uint_as_float(sr[col + 1]), a.scale_log2, -m_use)) : 0.f;
-          sum += p0 + p1;
-          pk[e >> 1] = pack_bf16x2(p0, p1);
-        }
-        tc::tmem_st_32x32b_x16(tmem + T_P + lane_off + c * 16, pk);
-      }
-      l += sum;
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
-    }
-    tc::mbar_wait(o_full, (nkv - 1) & 1);
-    tc::tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* dst = a.o + (int64_t)b * a.sb_o + (int64_t)qi * a.ld_o + h * HD;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t r[32];
-      tc::tmem_ld_32x32b_x32(tmem + T_O + lane_off + c * 32, r);
-      tc::tmem_ld_wait();
-      if (qi < a.N) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * inv, __uint_as_float(r[u * 8 + 1]) * inv);
-          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * inv, __uint_as_float(r[u * 8 + 3]) * inv);
-          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * inv, __uint_as_float(r[u * 8 + 5]) * inv);
-          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * inv, __uint_as_float(r[u * 8 + 7]) * inv);
-          reinterpret_cast<uint4*>(dst + c * 32)[u] = v;
+          for (int u = 0; u < 4; ++u) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * inv, __uint_as_float(r[u * 8 + 1]) * inv);
+            v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * inv, __uint_as_float(r[u * 8 + 3]) * inv);
+            v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * inv, __uint_as_float(r[u * 8 + 5]) * inv);
+            v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * inv, __uint_as_float(r[u * 8 + 7]) * inv);
+            reinterpret_cast<uint4*>(dst + c * 32)[u] = v;
+          }
         }
       }
+      if (qi < a.N)
+        a.lse[(int64_t)(b * a.H + h) * a.Npad + qi] = (l > 0.f) ? (m_run + __log2f(l)) * kLn2 : -INFINITY;
     }
-    if (qi < a.N) a.lse[(int64_t)(b * a.H + h) * a.Npad + qi] = (l > 0.f) ? (m_run + __log2f(l)) * kLn2 : -INFINITY;
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 256);
+    tc::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -645,8 +661,8 @@ extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t
     if (e != cudaSuccess) return avb::cuda_status(e, "attn_fwd smem attr");
     attr = true;
   }
-  dim3 grid((N + BT - 1) / BT, H, B);
-  attn_fwd_kernel<<<grid, 192, F_SMEM, avb::as_stream(stream)>>>(mq, mk, mv, a);
+  dim3 grid((N + 2 * BT - 1) / (2 * BT), H, B);
+  attn_fwd_kernel<<<grid, 320, F_SMEM, avb::as_stream(stream)>>>(mq, mk, mv, a);
   return avb::launch_status("avb_attn_fwd");
 }
 

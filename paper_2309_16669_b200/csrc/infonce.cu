@@ -67,12 +67,17 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// CLIP parameterisation: s = exp(min(log_scale, ln 100)); the clamp blocks the gradient
+__device__ __forceinline__ float clip_scale(const float* log_scale) { return __expf(fminf(*log_scale, 4.6051702f)); }
+
 __global__ void __launch_bounds__(kThr) infonce_stats_kernel(const float* __restrict__ v, const float* __restrict__ t,
                                                              const float* __restrict__ nv, const float* __restrict__ nt,
-                                                             int Bg, int E, float scale, float* __restrict__ lse_r,
-                                                             float* __restrict__ lse_c, float* __restrict__ loss,
-                                                             float* __restrict__ dscale) {
+                                                             int Bg, int E, const float* __restrict__ log_scale,
+                                                             float* __restrict__ lse_r, float* __restrict__ lse_c,
+                                                             float* __restrict__ loss, float* __restrict__ dlog_scale) {
   extern __shared__ float sm[];
+  const float scale = clip_scale(log_scale);
+  const float dpar = (*log_scale < 4.6051702f) ? scale : 0.f;   // ds / d log_scale
   float* vrow = sm;                 // [RB][E]  normalised v rows i0..
   float* tcol = vrow + RB * E;      // [RB][E]  normalised t rows j0..
   float* Sr = tcol + RB * E;        // [RB][Bg] S[i0+r][j]
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(kThr) infonce_stats_kernel(const float* __rest
         const float diag = S[i0 + r];
         (pass == 0 ? lse_r : lse_c)[i0 + r] = lse;
         atomicAdd(loss, inv2b * (lse - diag));
-        atomicAdd(dscale, inv2b / scale * (sx / se - diag));
+        if (dlog_scale) atomicAdd(dlog_scale, dpar * inv2b / scale * (sx / se - diag));
       }
     }
   }
@@ -119,7 +124,8 @@ __global__ void __launch_bounds__(kThr) infonce_stats_kernel(const float* __rest
 // which = 0: d v for rows [r0, r0+n); which = 1: d t for columns [r0, r0+n)
 __global__ void __launch_bounds__(kThr) infonce_grad_kernel(const float* __restrict__ v, const float* __restrict__ t,
                                                             const float* __restrict__ nv, const float* __restrict__ nt,
-                                                            int Bg, int E, float scale, const float* __restrict__ lse_r,
+                                                            int Bg, int E, const float* __restrict__ log_scale,
+                                                            const float* __restrict__ lse_r,
                                                             const float* __restrict__ lse_c, int r0, int n,
                                                             float grad_scale, float* __restrict__ dv,
                                                             float* __restrict__ dt) {
@@ -132,6 +138,7 @@ __global__ void __launch_bounds__(kThr) infonce_grad_kernel(const float* __restr
   const float* lse_fix = which ? lse_c : lse_r;   // softmax along the fixed index's own direction
   const float* lse_oth = which ? lse_r : lse_c;
   float* out = which ? dt : dv;
+  const float scale = clip_scale(log_scale);
   float* fix = sm;                 // [RB][E] normalised
   float* S = fix + RB * E;         // [RB][Bg]
   float* red = S + RB * Bg;        // [RB]
@@ -186,11 +193,11 @@ __global__ void __launch_bounds__(kThr) infonce_grad_kernel(const float* __restr
 
 }  // namespace
 
-extern "C" int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, float logit_scale, float* norms_v,
-                               float* norms_t, float* lse_r, float* lse_c, float* loss, float* dscale, void* stream) {
+extern "C" int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, const float* log_scale, float* norms_v,
+                               float* norms_t, float* lse_r, float* lse_c, float* loss, float* dlog_scale,
+                               void* stream) {
   AVB_CHECK_ARG(Bg >= 1 && E >= 4 && E % 4 == 0 && E <= 1024, "InfoNCE needs E % 4 == 0, E <= 1024");
-  AVB_CHECK_ARG(v && t && norms_v && norms_t && lse_r && lse_c && loss && dscale, "null pointer");
-  AVB_CHECK_ARG(logit_scale > 0.f, "logit scale must be > 0");
+  AVB_CHECK_ARG(v && t && norms_v && norms_t && lse_r && lse_c && loss && log_scale, "null pointer");
   cudaStream_t st = avb::as_stream(stream);
   rownorm_kernel<<<(Bg + 7) / 8, 256, 0, st>>>(v, Bg, E, norms_v);
   rownorm_kernel<<<(Bg + 7) / 8, 256, 0, st>>>(t, Bg, E, norms_t);
@@ -202,18 +209,18 @@ extern "C" int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, fl
     cudaFuncSetAttribute(infonce_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  infonce_stats_kernel<<<(Bg + RB - 1) / RB, kThr, smem, st>>>(v, t, norms_v, norms_t, Bg, E, logit_scale, lse_r,
-                                                               lse_c, loss, dscale);
+  infonce_stats_kernel<<<(Bg + RB - 1) / RB, kThr, smem, st>>>(v, t, norms_v, norms_t, Bg, E, log_scale, lse_r,
+                                                               lse_c, loss, dlog_scale);
   return avb::launch_status("avb_infonce_fwd");
 }
 
-extern "C" int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, float logit_scale, const float* norms_v,
+extern "C" int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, const float* log_scale, const float* norms_v,
                                const float* norms_t, const float* lse_r, const float* lse_c, int r0, int n,
                                float grad_scale, float* dv, float* dt, void* stream) {
   AVB_CHECK_ARG(Bg >= 1 && E >= 4 && E % 4 == 0 && E <= 1024, "InfoNCE needs E % 4 == 0, E <= 1024");
   AVB_CHECK_ARG(r0 >= 0 && n >= 0 && r0 + n <= Bg, "local rows out of range");
   if (n == 0) return AVB_OK;
-  AVB_CHECK_ARG(v && t && norms_v && norms_t && lse_r && lse_c && dv && dt, "null pointer");
+  AVB_CHECK_ARG(v && t && log_scale && norms_v && norms_t && lse_r && lse_c && dv && dt, "null pointer");
   const size_t smem = sizeof(float) * (2 * RB * E + (size_t)RB * Bg + RB);
   AVB_CHECK_ARG(smem <= 200 * 1024, "global batch too large for one InfoNCE pass (Bg=%d)", Bg);
   static bool attr = false;
@@ -222,7 +229,7 @@ extern "C" int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, fl
     attr = true;
   }
   dim3 grid((n + RB - 1) / RB, 2);
-  infonce_grad_kernel<<<grid, kThr, smem, avb::as_stream(stream)>>>(v, t, norms_v, norms_t, Bg, E, logit_scale, lse_r,
+  infonce_grad_kernel<<<grid, kThr, smem, avb::as_stream(stream)>>>(v, t, norms_v, norms_t, Bg, E, log_scale, lse_r,
                                                                     lse_c, r0, n, grad_scale, dv, dt);
   return avb::launch_status("avb_infonce_bwd");
 }

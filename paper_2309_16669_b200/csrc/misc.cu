@@ -155,7 +155,99 @@ __global__ void cast_bf16_kernel(const float* __restrict__ s, __nv_bfloat16* __r
     d[i] = __float2bfloat16_rn(s[i]);
 }
 
+// x[b*L + l] = table[tok[b*L + l]] + pos[l]  (fp32 table -> bf16 rows)
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ table,
+                                 const float* __restrict__ pos, __nv_bfloat16* __restrict__ x, int B, int L, int D,
+                                 int V) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = D / 8;
+  if (gid >= (int64_t)B * L * per) return;
+  const int c = (gid % per) * 8;
+  const int64_t r = gid / per;
+  const int l = r % L;
+  int id = tok[r];
+  id = id < 0 ? 0 : (id >= V ? V - 1 : id);
+  float f[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = table[(int64_t)id * D + c + e] + pos[(int64_t)l * D + c + e];
+  st8f(x + r * D + c, f);
+}
+
+// dtable[tok] += dx (atomics; repeated ids accumulate); dpos[l] += sum_b dx[b, l]
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
+                                 float* __restrict__ dtable, float* __restrict__ dpos, int B, int L, int D, int V) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = D / 8;
+  if (gid >= (int64_t)L * per) return;
+  const int c = (gid % per) * 8;
+  const int l = gid / per;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < B; ++b) {
+    const int64_t r = (int64_t)b * L + l;
+    float f[8];
+    ld8f(dx + r * D + c, f);
+    int id = tok[r];
+    id = id < 0 ? 0 : (id >= V ? V - 1 : id);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      acc[e] += f[e];
+      if (dtable) atomicAdd(dtable + (int64_t)id * D + c + e, f[e]);
+    }
+  }
+  if (dpos) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dpos[(int64_t)l * D + c + e] += acc[e];
+  }
+}
+
+// dst[dst_idx ? dst_idx[i] : i] = src[src_idx ? src_idx[i] : i]  (bf16 rows of D)
+__global__ void rows_copy_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds, const int32_t* __restrict__ sidx,
+                                 __nv_bfloat16* __restrict__ dst, int64_t ldd, const int32_t* __restrict__ didx, int n,
+                                 int D) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = D / 8;
+  if (gid >= (int64_t)n * per) return;
+  const int c = (gid % per) * 8;
+  const int i = gid / per;
+  const int64_t rs = sidx ? sidx[i] : i, rd = didx ? didx[i] : i;
+  *reinterpret_cast<uint4*>(dst + rd * ldd + c) = *reinterpret_cast<const uint4*>(src + rs * lds + c);
+}
+
 }  // namespace
+
+extern "C" int avb_embed_fwd(const int32_t* tokens, const float* table, const float* pos, void* x, int B, int L, int D,
+                             int V, void* stream) {
+  AVB_CHECK_ARG(B >= 0 && L >= 1 && D % 8 == 0 && V >= 1, "embed: D % 8 == 0");
+  if (B == 0) return AVB_OK;
+  AVB_CHECK_ARG(tokens && table && pos && x, "null pointer");
+  const int64_t total = (int64_t)B * L * (D / 8);
+  embed_fwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
+      tokens, table, pos, reinterpret_cast<__nv_bfloat16*>(x), B, L, D, V);
+  return avb::launch_status("avb_embed_fwd");
+}
+
+extern "C" int avb_embed_bwd(const int32_t* tokens, const void* dx, float* dtable, float* dpos, int B, int L, int D,
+                             int V, void* stream) {
+  AVB_CHECK_ARG(B >= 0 && L >= 1 && D % 8 == 0 && V >= 1, "embed: D % 8 == 0");
+  if (B == 0) return AVB_OK;
+  AVB_CHECK_ARG(tokens && dx, "null pointer");
+  const int64_t total = (int64_t)L * (D / 8);
+  embed_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
+      tokens, reinterpret_cast<const __nv_bfloat16*>(dx), dtable, dpos, B, L, D, V);
+  return avb::launch_status("avb_embed_bwd");
+}
+
+extern "C" int avb_rows_copy(const void* src, int64_t lds, const int32_t* src_idx, void* dst, int64_t ldd,
+                             const int32_t* dst_idx, int n, int D, void* stream) {
+  AVB_CHECK_ARG(n >= 0 && D % 8 == 0 && lds % 8 == 0 && ldd % 8 == 0, "rows_copy: D, lds, ldd multiples of 8");
+  if (n == 0) return AVB_OK;
+  AVB_CHECK_ARG(src && dst, "null pointer");
+  const int64_t total = (int64_t)n * (D / 8);
+  rows_copy_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(src), lds, src_idx, reinterpret_cast<__nv_bfloat16*>(dst), ldd, dst_idx,
+      n, D);
+  return avb::launch_status("avb_rows_copy");
+}
 
 extern "C" int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void* stream) {
   AVB_CHECK_ARG(M >= 0 && N >= 0 && N % 8 == 0 && ldx % 8 == 0, "colsum needs N and ldx multiples of 8");

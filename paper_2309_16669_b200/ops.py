@@ -187,33 +187,65 @@ def cast_bf16(src, dst):
     _lib.check(_lib.load().avb_cast_bf16(src.data_ptr(), dst.data_ptr(), src.numel(), _lib.stream_ptr()), "cast_bf16")
 
 
-# ----------------------------------------------------------------------------- InfoNCE
-def infonce(v: torch.Tensor, t: torch.Tensor, logit_scale: float, r0: int = 0, n: int | None = None,
-            grad_scale: float = 1.0):
-    """CLIP loss over the global batch v, t [Bg, E] fp32 (raw embeddings).
-
-    Returns (loss [1], dscale [1], dv [n, E], dt [n, E]) with dv/dt the gradients of the
-    rows/columns [r0, r0+n) scaled by grad_scale.
-    """
+# ----------------------------------------------------------------------------- InfoNCE / embeddings
+def infonce_fwd(v, t, log_scale, loss, dlog_scale=None):
+    """Global-batch CLIP loss: loss += L, dlog_scale += dL/dlog_scale; returns the stats for bwd."""
     if v.dtype != torch.float32 or t.dtype != torch.float32 or v.shape != t.shape or not v.is_contiguous() \
             or not t.is_contiguous():
         raise InputError("v, t must be contiguous fp32 [Bg, E] of equal shape")
     Bg, E = v.shape
-    n = Bg - r0 if n is None else n
     dev = v.device
-    nv = torch.empty(Bg, device=dev)
-    nt = torch.empty(Bg, device=dev)
-    lr = torch.empty(Bg, device=dev)
-    lc = torch.empty(Bg, device=dev)
-    loss = torch.zeros(1, device=dev)
-    ds = torch.zeros(1, device=dev)
-    dv = torch.empty(n, E, device=dev)
-    dt = torch.empty(n, E, device=dev)
-    lib = _lib.load()
-    _lib.check(lib.avb_infonce_fwd(v.data_ptr(), t.data_ptr(), Bg, E, float(logit_scale), nv.data_ptr(),
-                                   nt.data_ptr(), lr.data_ptr(), lc.data_ptr(), loss.data_ptr(), ds.data_ptr(),
-                                   _lib.stream_ptr()), "infonce_fwd")
-    _lib.check(lib.avb_infonce_bwd(v.data_ptr(), t.data_ptr(), Bg, E, float(logit_scale), nv.data_ptr(),
-                                   nt.data_ptr(), lr.data_ptr(), lc.data_ptr(), int(r0), int(n), float(grad_scale),
-                                   dv.data_ptr(), dt.data_ptr(), _lib.stream_ptr()), "infonce_bwd")
-    return loss, ds, dv, dt
+    st = {"nv": torch.empty(Bg, device=dev), "nt": torch.empty(Bg, device=dev),
+          "lr": torch.empty(Bg, device=dev), "lc": torch.empty(Bg, device=dev)}
+    _lib.check(_lib.load().avb_infonce_fwd(v.data_ptr(), t.data_ptr(), Bg, E, log_scale.data_ptr(),
+                                           st["nv"].data_ptr(), st["nt"].data_ptr(), st["lr"].data_ptr(),
+                                           st["lc"].data_ptr(), loss.data_ptr(), _ptr(dlog_scale), _lib.stream_ptr()),
+               "infonce_fwd")
+    return st
+
+
+def infonce_bwd(v, t, log_scale, stats, r0, n, grad_scale=1.0, dv=None, dt=None):
+    Bg, E = v.shape
+    dv = torch.empty(n, E, device=v.device) if dv is None else dv
+    dt = torch.empty(n, E, device=v.device) if dt is None else dt
+    _lib.check(_lib.load().avb_infonce_bwd(v.data_ptr(), t.data_ptr(), Bg, E, log_scale.data_ptr(),
+                                           stats["nv"].data_ptr(), stats["nt"].data_ptr(), stats["lr"].data_ptr(),
+                                           stats["lc"].data_ptr(), int(r0), int(n), float(grad_scale), dv.data_ptr(),
+                                           dt.data_ptr(), _lib.stream_ptr()), "infonce_bwd")
+    return dv, dt
+
+
+def infonce(v: torch.Tensor, t: torch.Tensor, log_scale: torch.Tensor, r0: int = 0, n: int | None = None,
+            grad_scale: float = 1.0):
+    """(loss [1], dlog_scale [1], dv [n,E], dt [n,E]) for the CLIP loss over the global batch v, t."""
+    Bg = v.shape[0]
+    n = Bg - r0 if n is None else n
+    loss = torch.zeros(1, device=v.device)
+    dls = torch.zeros(1, device=v.device)
+    st = infonce_fwd(v, t, log_scale, loss, dls)
+    dv, dt = infonce_bwd(v, t, log_scale, st, r0, n, grad_scale)
+    return loss, dls, dv, dt
+
+
+def embed_fwd(tokens, table, pos, out):
+    B, L = tokens.shape
+    V, D = table.shape
+    _lib.check(_lib.load().avb_embed_fwd(tokens.data_ptr(), table.data_ptr(), pos.data_ptr(), out.data_ptr(), B, L, D,
+                                         V, _lib.stream_ptr()), "embed_fwd")
+    return out
+
+
+def embed_bwd(tokens, dx, dtable, dpos):
+    B, L = tokens.shape
+    V, D = dtable.shape
+    _lib.check(_lib.load().avb_embed_bwd(tokens.data_ptr(), dx.data_ptr(), dtable.data_ptr(), _ptr(dpos), B, L, D, V,
+                                         _lib.stream_ptr()), "embed_bwd")
+
+
+def rows_copy(src, dst, src_idx=None, dst_idx=None, n=None):
+    n = (src_idx.numel() if src_idx is not None else src.shape[0]) if n is None else n
+    D = src.shape[-1]
+    _lib.check(_lib.load().avb_rows_copy(src.data_ptr(), _rowmajor(src, "src"), _ptr(src_idx), dst.data_ptr(),
+                                         _rowmajor(dst, "dst"), _ptr(dst_idx), int(n), D, _lib.stream_ptr()),
+               "rows_copy")
+    return dst

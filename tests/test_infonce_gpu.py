@@ -23,8 +23,11 @@ def test_infonce_matches_oracle(Bg, E, r0, n):
     sr = torch.tensor(s, requires_grad=True)
     ref = VO.clip_loss(vr, tr, sr)
     ref.backward()
-    loss, ds, dv, dt = ops.infonce(v.cuda(), t.cuda(), s, r0, n, grad_scale=2.0)
+    import math
+    ls = torch.tensor([math.log(s)], device="cuda")
+    loss, dls, dv, dt = ops.infonce(v.cuda(), t.cuda(), ls, r0, n, grad_scale=2.0)
     assert abs(loss.item() - ref.item()) / ref.item() < 1e-4
-    assert abs(ds.item() - sr.grad.item()) < 1e-4 * max(1.0, abs(sr.grad.item()))
+    # d/dlog_scale = s * d/ds
+    assert abs(dls.item() - s * sr.grad.item()) < 1e-4 * max(1.0, abs(s * sr.grad.item()))
     assert rel(dv, 2.0 * vr.grad[r0:r0 + n]) < 1e-4
     assert rel(dt, 2.0 * tr.grad[r0:r0 + n]) < 1e-4
