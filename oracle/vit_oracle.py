@@ -37,12 +37,26 @@ def patchify(clips, cfg):
     return x.reshape(B * (T // t) * (H // h) * (W // w), C * t * h * w)
 
 
-def attention(qkv, B, N, H):
+def attention(qkv, B, N, H, causal=False):
     D = H * 64
     q, k, v = qkv.view(B, N, 3, H, 64).permute(2, 0, 3, 1, 4)
     s = q @ k.transpose(-1, -2) / math.sqrt(64)
+    if causal:
+        s = s.masked_fill(torch.ones(N, N, dtype=torch.bool).triu(1), float("-inf"))
     o = torch.softmax(s, -1) @ v
     return o.permute(0, 2, 1, 3).reshape(B * N, D)
+
+
+def blocks(P: dict, x, B, N, D, heads, depth, prefix, causal=False):
+    for l in range(depth):
+        g = f"{prefix}.blk{l}"
+        h = F.layer_norm(x, (D,), P[f"{g}.ln1.g"], P[f"{g}.ln1.b"], 1e-5)
+        qkv = h @ P[f"{g}.qkv.w"].t() + P[f"{g}.qkv.b"]
+        x = x + attention(qkv, B, N, heads, causal) @ P[f"{g}.proj.w"].t() + P[f"{g}.proj.b"]
+        h = F.layer_norm(x, (D,), P[f"{g}.ln2.g"], P[f"{g}.ln2.b"], 1e-5)
+        a = quick_gelu(h @ P[f"{g}.fc1.w"].t() + P[f"{g}.fc1.b"])
+        x = x + a @ P[f"{g}.fc2.w"].t() + P[f"{g}.fc2.b"]
+    return x
 
 
 def encoder_forward(P: dict, patches, cfg, B, prefix="enc"):
@@ -51,15 +65,26 @@ def encoder_forward(P: dict, patches, cfg, B, prefix="enc"):
     pe = pe.view(B, N - 1, D)
     cls = P[f"{prefix}.cls"].view(1, 1, D).expand(B, 1, D)
     x = (torch.cat([cls, pe], 1) + P[f"{prefix}.pos"].view(1, N, D)).reshape(B * N, D)
-    for l in range(cfg.depth):
-        g = f"{prefix}.blk{l}"
-        h = F.layer_norm(x, (D,), P[f"{g}.ln1.g"], P[f"{g}.ln1.b"], 1e-5)
-        qkv = h @ P[f"{g}.qkv.w"].t() + P[f"{g}.qkv.b"]
-        x = x + attention(qkv, B, N, cfg.heads) @ P[f"{g}.proj.w"].t() + P[f"{g}.proj.b"]
-        h = F.layer_norm(x, (D,), P[f"{g}.ln2.g"], P[f"{g}.ln2.b"], 1e-5)
-        a = quick_gelu(h @ P[f"{g}.fc1.w"].t() + P[f"{g}.fc1.b"])
-        x = x + a @ P[f"{g}.fc2.w"].t() + P[f"{g}.fc2.b"]
-    return x
+    return blocks(P, x, B, N, D, cfg.heads, cfg.depth, prefix)
+
+
+def text_forward(P: dict, tokens, tcfg, prefix="txt"):
+    """Causal GPT-like text tower: token + position embedding -> blocks."""
+    B, L = tokens.shape
+    x = (P[f"{prefix}.tok"][tokens.long()] + P[f"{prefix}.pos"][:L]).reshape(B * L, tcfg.dim)
+    return blocks(P, x, B, L, tcfg.dim, tcfg.heads, tcfg.depth, prefix, causal=True)
+
+
+def clip_forward_loss(P: dict, patches, tokens, eot, vcfg, tcfg):
+    """Dual-encoder CLIP loss: cls / EOT pooling -> LN -> projection -> InfoNCE (logit scale = exp(param))."""
+    B, L = tokens.shape
+    xv = encoder_forward(P, patches, vcfg, B)
+    v = F.layer_norm(xv.view(B, vcfg.tokens, vcfg.dim)[:, 0], (vcfg.dim,), P["clip.vln.g"], P["clip.vln.b"], 1e-5)
+    v = v @ P["clip.vproj"].t()
+    xt = text_forward(P, tokens, tcfg)
+    t = F.layer_norm(xt[eot.long()], (tcfg.dim,), P["clip.tln.g"], P["clip.tln.b"], 1e-5)
+    t = t @ P["clip.tproj"].t()
+    return clip_loss(v, t, P["clip.logit_scale"].exp().squeeze())
 
 
 def head_loss(P: dict, x, B, N, labels, num_classes, prefix="head"):

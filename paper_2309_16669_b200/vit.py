@@ -175,79 +175,65 @@ def wgrad_split(m_out: int, n_out: int, sms: int = 148) -> int:
     return max(1, sms // tiles)
 
 
-# ----------------------------------------------------------------------------- encoder
-class VideoEncoder:
-    """ViT video encoder over tubelet-patch rows (the K1 "tubelet" layout).
+# ----------------------------------------------------------------------------- blocks
+class TransformerStack:
+    """L pre-LN blocks over a residual stream [B*N, D] bf16.
 
-    forward(patches [B*Np, 3*t*h*w] bf16) -> final residual stream [B*N, D] bf16
-    backward(dx) accumulates every parameter gradient into `store.grad`.
+    Shared by the video encoder (bidirectional) and the text encoder (causal).
     """
 
-    def __init__(self, cfg: VitConfig, store: ParamStore, prefix: str = "enc"):
-        cfg.validate()
-        self.cfg = cfg
-        self.s = store
-        self.pre = prefix
-        D, F, Hd = cfg.dim, cfg.patch_dim, cfg.hidden
-        s, P = store, prefix
-        s.add(f"{P}.pe.w", (D, F), True, "normal", f"{P}.embed")
-        s.add(f"{P}.pe.b", (D,), False, "zeros", f"{P}.embed")
-        s.add(f"{P}.cls", (D,), False, "normal", f"{P}.embed")
-        s.add(f"{P}.pos", (cfg.tokens, D), False, "normal", f"{P}.embed")
-        for l in range(cfg.depth):
-            g = f"{P}.blk{l}"
-            s.add(f"{g}.ln1.g", (D,), False, "ones", g)
-            s.add(f"{g}.ln1.b", (D,), False, "zeros", g)
-            s.add(f"{g}.qkv.w", (3 * D, D), True, "normal", g)
-            s.add(f"{g}.qkv.b", (3 * D,), False, "zeros", g)
-            s.add(f"{g}.proj.w", (D, D), True, "normal", g)
-            s.add(f"{g}.proj.b", (D,), False, "zeros", g)
-            s.add(f"{g}.ln2.g", (D,), False, "ones", g)
-            s.add(f"{g}.ln2.b", (D,), False, "zeros", g)
-            s.add(f"{g}.fc1.w", (Hd, D), True, "normal", g)
-            s.add(f"{g}.fc1.b", (Hd,), False, "zeros", g)
-            s.add(f"{g}.fc2.w", (D, Hd), True, "normal", g)
-            s.add(f"{g}.fc2.b", (D,), False, "zeros", g)
+    def __init__(self, dim: int, heads: int, depth: int, hidden: int, store: ParamStore, prefix: str,
+                 causal: bool = False):
+        if dim != 64 * heads:
+            raise ConfigurationError("head_dim must be 64")
+        self.D, self.H, self.L, self.Hd = dim, heads, depth, hidden
+        self.s, self.pre, self.causal = store, prefix, causal
+        D, Hd = dim, hidden
+        for l in range(depth):
+            g = f"{prefix}.blk{l}"
+            store.add(f"{g}.ln1.g", (D,), False, "ones", g)
+            store.add(f"{g}.ln1.b", (D,), False, "zeros", g)
+            store.add(f"{g}.qkv.w", (3 * D, D), True, "normal", g)
+            store.add(f"{g}.qkv.b", (3 * D,), False, "zeros", g)
+            store.add(f"{g}.proj.w", (D, D), True, "normal", g)
+            store.add(f"{g}.proj.b", (D,), False, "zeros", g)
+            store.add(f"{g}.ln2.g", (D,), False, "ones", g)
+            store.add(f"{g}.ln2.b", (D,), False, "zeros", g)
+            store.add(f"{g}.fc1.w", (Hd, D), True, "normal", g)
+            store.add(f"{g}.fc1.b", (Hd,), False, "zeros", g)
+            store.add(f"{g}.fc2.w", (D, Hd), True, "normal", g)
+            store.add(f"{g}.fc2.b", (D,), False, "zeros", g)
 
-    # -- forward -----------------------------------------------------------------
-    def forward(self, patches: torch.Tensor, B: int, save: bool = True):
-        cfg, s, P = self.cfg, self.s, self.pre
-        N, Np, D, H = cfg.tokens, cfg.patches, cfg.dim, cfg.heads
+    def forward(self, x: torch.Tensor, B: int, N: int, save: bool = True):
+        s, P, D, H = self.s, self.pre, self.D, self.H
         M = B * N
-        dev = patches.device
-        pe = ops.gemm(patches, s.w(f"{P}.pe.w"), bias=s.p(f"{P}.pe.b"))
-        x = torch.empty((M, D), dtype=torch.bfloat16, device=dev)
-        ops.tokens_fwd(pe, s.p(f"{P}.cls"), s.p(f"{P}.pos"), B, Np, x)
-        del pe
+        dev = x.device
         saved = []
-        for l in range(cfg.depth):
+        for l in range(self.L):
             g = f"{P}.blk{l}"
             h1, mu1, rs1 = ops.layernorm_fwd(x, s.p(f"{g}.ln1.g"), s.p(f"{g}.ln1.b"))
             qkv = ops.gemm(h1, s.w(f"{g}.qkv.w"), bias=s.p(f"{g}.qkv.b"))
             q3 = qkv.view(B, N, 3 * D)
-            o, lse = ops.attn_fwd(q3[:, :, :D], q3[:, :, D:2 * D], q3[:, :, 2 * D:], H)
+            o, lse = ops.attn_fwd(q3[:, :, :D], q3[:, :, D:2 * D], q3[:, :, 2 * D:], H, causal=self.causal)
             o2 = o.view(M, D)
             x2 = ops.gemm(o2, s.w(f"{g}.proj.w"), bias=s.p(f"{g}.proj.b"), aux=x)
             h2, mu2, rs2 = ops.layernorm_fwd(x2, s.p(f"{g}.ln2.g"), s.p(f"{g}.ln2.b"))
-            pre = torch.empty((M, cfg.hidden), dtype=torch.bfloat16, device=dev)
+            pre = torch.empty((M, self.Hd), dtype=torch.bfloat16, device=dev)
             a = ops.gemm(h2, s.w(f"{g}.fc1.w"), bias=s.p(f"{g}.fc1.b"), epilogue=ops.EPI_BIAS_GELU, aux_out=pre)
             x3 = ops.gemm(a, s.w(f"{g}.fc2.w"), bias=s.p(f"{g}.fc2.b"), aux=x2)
             if save:
                 saved.append((x, h1, mu1, rs1, qkv, o2, lse, x2, h2, mu2, rs2, pre, a))
             x = x3
-        return x, {"patches": patches, "B": B, "saved": saved}
+        return x, saved
 
-    # -- backward ----------------------------------------------------------------
-    def backward(self, dx: torch.Tensor, ctx: dict, on_layer_done=None):
-        """dx: grad of the final residual stream [B*N, D] bf16 (consumed in place)."""
-        cfg, s, P = self.cfg, self.s, self.pre
-        B = ctx["B"]
-        N, Np, D, H, Hd = cfg.tokens, cfg.patches, cfg.dim, cfg.heads, cfg.hidden
+    def backward(self, dx: torch.Tensor, saved: list, B: int, N: int, on_layer_done=None):
+        """dx: grad of the stack output [B*N, D] bf16; consumed in place, returns grad of the input."""
+        s, P, D, H, Hd = self.s, self.pre, self.D, self.H, self.Hd
         M = B * N
         dev = dx.device
-        for l in reversed(range(cfg.depth)):
+        for l in reversed(range(self.L)):
             g = f"{P}.blk{l}"
-            x, h1, mu1, rs1, qkv, o2, lse, x2, h2, mu2, rs2, pre, a = ctx["saved"][l]
+            x, h1, mu1, rs1, qkv, o2, lse, x2, h2, mu2, rs2, pre, a = saved[l]
             # fc2: x3 = x2 + a W2^T + b2
             ops.gemm(dx, a, a_mn=True, b_mn=True, out=s.g(f"{g}.fc2.w"), epilogue=ops.EPI_F32_ACCUM,
                      split_k=wgrad_split(D, Hd))
@@ -271,7 +257,7 @@ class VideoEncoder:
             dqkv = torch.empty((M, 3 * D), dtype=torch.bfloat16, device=dev)
             d3 = dqkv.view(B, N, 3 * D)
             ops.attn_bwd(q3[:, :, :D], q3[:, :, D:2 * D], q3[:, :, 2 * D:], o2.view(B, N, D), do.view(B, N, D), lse,
-                         H, dq=d3[:, :, :D], dk=d3[:, :, D:2 * D], dv=d3[:, :, 2 * D:])
+                         H, causal=self.causal, dq=d3[:, :, :D], dk=d3[:, :, D:2 * D], dv=d3[:, :, 2 * D:])
             del do
             ops.gemm(dqkv, h1, a_mn=True, b_mn=True, out=s.g(f"{g}.qkv.w"), epilogue=ops.EPI_F32_ACCUM,
                      split_k=wgrad_split(3 * D, D))
@@ -281,14 +267,96 @@ class VideoEncoder:
             ops.layernorm_bwd(dh1, x, s.p(f"{g}.ln1.g"), mu1, rs1, dx, s.g(f"{g}.ln1.g"), s.g(f"{g}.ln1.b"),
                               accumulate=True)
             del dh1
-            ctx["saved"][l] = None
+            saved[l] = None
             if on_layer_done is not None:
                 on_layer_done(g)
-        dpe = torch.empty((B * Np, D), dtype=torch.bfloat16, device=dev)
+        return dx
+
+
+# ----------------------------------------------------------------------------- encoders
+class VideoEncoder:
+    """ViT video encoder over tubelet-patch rows (the K1 "tubelet" layout).
+
+    forward(patches [B*Np, 3*t*h*w] bf16) -> final residual stream [B*N, D] bf16
+    backward(dx) accumulates every parameter gradient into `store.grad`.
+    """
+
+    def __init__(self, cfg: VitConfig, store: ParamStore, prefix: str = "enc"):
+        cfg.validate()
+        self.cfg = cfg
+        self.s = store
+        self.pre = prefix
+        D, F = cfg.dim, cfg.patch_dim
+        s, P = store, prefix
+        s.add(f"{P}.pe.w", (D, F), True, "normal", f"{P}.embed")
+        s.add(f"{P}.pe.b", (D,), False, "zeros", f"{P}.embed")
+        s.add(f"{P}.cls", (D,), False, "normal", f"{P}.embed")
+        s.add(f"{P}.pos", (cfg.tokens, D), False, "normal", f"{P}.embed")
+        self.stack = TransformerStack(D, cfg.heads, cfg.depth, cfg.hidden, store, P)
+
+    def forward(self, patches: torch.Tensor, B: int, save: bool = True):
+        cfg, s, P = self.cfg, self.s, self.pre
+        N, Np, D = cfg.tokens, cfg.patches, cfg.dim
+        pe = ops.gemm(patches, s.w(f"{P}.pe.w"), bias=s.p(f"{P}.pe.b"))
+        x = torch.empty((B * N, D), dtype=torch.bfloat16, device=patches.device)
+        ops.tokens_fwd(pe, s.p(f"{P}.cls"), s.p(f"{P}.pos"), B, Np, x)
+        del pe
+        x, saved = self.stack.forward(x, B, N, save)
+        return x, {"patches": patches, "B": B, "saved": saved}
+
+    def backward(self, dx: torch.Tensor, ctx: dict, on_layer_done=None):
+        """dx: grad of the final residual stream [B*N, D] bf16 (consumed in place)."""
+        cfg, s, P = self.cfg, self.s, self.pre
+        B = ctx["B"]
+        N, Np, D = cfg.tokens, cfg.patches, cfg.dim
+        dx = self.stack.backward(dx, ctx["saved"], B, N, on_layer_done)
+        dpe = torch.empty((B * Np, D), dtype=torch.bfloat16, device=dx.device)
         ops.tokens_bwd(dx, dpe, s.g(f"{P}.cls"), s.g(f"{P}.pos"), B, Np)
         ops.gemm(dpe, ctx["patches"], a_mn=True, b_mn=True, out=s.g(f"{P}.pe.w"), epilogue=ops.EPI_F32_ACCUM,
                  split_k=wgrad_split(D, cfg.patch_dim))
         ops.colsum_accum(dpe, s.g(f"{P}.pe.b"))
+        if on_layer_done is not None:
+            on_layer_done(f"{P}.embed")
+
+
+@dataclass(frozen=True)
+class TextConfig:
+    """CLIP text tower (12-layer GPT-like, <= 77 BPE tokens; width 512 assumed)."""
+
+    vocab: int = 49408
+    context: int = 77
+    dim: int = 512
+    heads: int = 8
+    depth: int = 12
+    mlp_ratio: float = 4.0
+
+    @property
+    def hidden(self) -> int:
+        return int(self.dim * self.mlp_ratio)
+
+
+class TextEncoder:
+    """Token embedding + causal transformer stack; pooled at the EOT position per caption."""
+
+    def __init__(self, cfg: TextConfig, store: ParamStore, prefix: str = "txt"):
+        self.cfg, self.s, self.pre = cfg, store, prefix
+        store.add(f"{prefix}.tok", (cfg.vocab, cfg.dim), False, "normal", f"{prefix}.embed")
+        store.add(f"{prefix}.pos", (cfg.context, cfg.dim), False, "normal", f"{prefix}.embed")
+        self.stack = TransformerStack(cfg.dim, cfg.heads, cfg.depth, cfg.hidden, store, prefix, causal=True)
+
+    def forward(self, tokens: torch.Tensor, save: bool = True):
+        B, L = tokens.shape
+        s, P = self.s, self.pre
+        x = torch.empty((B * L, self.cfg.dim), dtype=torch.bfloat16, device=tokens.device)
+        ops.embed_fwd(tokens, s.p(f"{P}.tok"), s.p(f"{P}.pos"), x)
+        x, saved = self.stack.forward(x, B, L, save)
+        return x, {"tokens": tokens, "B": B, "saved": saved}
+
+    def backward(self, dx: torch.Tensor, ctx: dict, on_layer_done=None):
+        s, P = self.s, self.pre
+        B, L = ctx["tokens"].shape
+        dx = self.stack.backward(dx, ctx["saved"], B, L, on_layer_done)
+        ops.embed_bwd(ctx["tokens"], dx, s.g(f"{P}.tok"), s.g(f"{P}.pos"))
         if on_layer_done is not None:
             on_layer_done(f"{P}.embed")
 

@@ -1,0 +1,51 @@
+"""CLIP dual encoder (config 3 structure, tiny shapes) on the GPU kernels vs the fp32 oracle.
+
+Video ViT + causal text tower + cls/EOT pooling + projections + fused InfoNCE: loss and every
+parameter gradient within 2e-2 norm-relative (north_star tolerance).  Single process
+(world = 1); the DP gradient rule is covered by tests/test_dp_gloo.py.
+"""
+
+import pytest
+import torch
+
+from oracle import vit_oracle as VO
+from paper_2309_16669_b200 import ops
+from paper_2309_16669_b200.clip import CLIPModel
+from paper_2309_16669_b200.vit import TextConfig, VitConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return ((a.float().cpu() - b.float().cpu()).norm() / b.float().cpu().norm().clamp_min(1e-30)).item()
+
+
+def test_clip_step_matches_oracle():
+    vcfg = VitConfig(frames=2, height=32, width=48, cube_t=1, depth=2, dim=128, heads=2)
+    tcfg = TextConfig(vocab=300, context=13, dim=128, heads=2, depth=2)
+    B = 6
+    m = CLIPModel(vcfg, tcfg, embed_dim=64, seed=3)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    m.store.data.add_(torch.randn(m.store.n, generator=g, device="cuda") * 0.02)
+    ops.cast_bf16(m.store.data, m.store.shadow)
+    patches = torch.randn(B * vcfg.patches, vcfg.patch_dim, generator=g, device="cuda").to(torch.bfloat16)
+    tokens = torch.randint(0, tcfg.vocab, (B, tcfg.context), generator=g, device="cuda", dtype=torch.int32)
+    eot = (torch.arange(B, device="cuda", dtype=torch.int32) * tcfg.context + tokens.argmax(1).to(torch.int32))
+    loss = torch.zeros(1, device="cuda")
+    m.zero_grad()
+    m.forward_backward(patches, tokens, eot, loss)
+    torch.cuda.synchronize()
+    names = [s[0] for s in m.store.specs]
+    P = {n: m.store.p(n).detach().cpu().clone().requires_grad_(True) for n in names}
+    ref = VO.clip_forward_loss(P, patches.float().cpu(), tokens.cpu(), eot.cpu(), vcfg, tcfg)
+    ref.backward()
+    assert abs(loss.item() - ref.item()) / abs(ref.item()) < 2e-2
+    bad = []
+    for n in names:
+        r = P[n].grad
+        if r is None or r.norm() < 1e-10:
+            continue
+        e = rel(m.store.g(n), r)
+        if e > 2e-2:
+            bad.append((n, e))
+    assert not bad, bad
