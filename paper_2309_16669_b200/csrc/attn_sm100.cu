@@ -175,20 +175,33 @@ __global__ void __launch_bounds__(320, 1)
         const int kv0 = j * BT;
         int lim = a.N - kv0;
         if (a.causal) lim = min(lim, qi - kv0 + 1);
-        // pass 1: row max (two TMEM round trips of 64 columns)
-        float mx = -INFINITY;
+        // pass 1: row max (two TMEM round trips of 64 columns), 8 independent max chains
+        const bool full = lim >= BT;   // warp-uniform in the non-causal case: no per-element masking
+        float mxa[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mxa[k] = -INFINITY;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t r0[32], r1[32];
           tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64, r0);
           tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64 + 32, r1);
           tc::tmem_ld_wait();
+          if (full) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            if (hh * 64 + e < lim) mx = fmaxf(mx, __uint_as_float(r0[e]));
-            if (hh * 64 + 32 + e < lim) mx = fmaxf(mx, __uint_as_float(r1[e]));
+            for (int e = 0; e < 32; ++e) {
+              mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r0[e]));
+              mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r1[e]));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              if (hh * 64 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r0[e]));
+              if (hh * 64 + 32 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r1[e]));
+            }
           }
         }
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         const float m_new = fmaxf(m_run, mx * a.scale_log2);
         if (j > 0) {
           tc::mbar_wait(o_full, (j - 1) & 1);  // PV(j-1) done: O stable, P buffer free
@@ -213,8 +226,8 @@ __global__ void __launch_bounds__(320, 1)
           m_run = m_new;
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        // pass 2: p = exp2(s*scale - m), row sum, bf16 pack straight into the TMEM P tile
-        float sum = 0.f;
+        // pass 2: p = exp2(s*scale - m), row sum (4 chains), bf16 pack straight into the TMEM P tile
+        float sm4[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t rb[2][32];
         tc::tmem_ld_32x32b_x32(tS + lane_off, rb[0]);
 #pragma unroll
@@ -225,15 +238,18 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const int col = c * 32 + e;
-            const float p0 = (col < lim) ? ex2(fmaf(__uint_as_float(rb[c & 1][e]), a.scale_log2, -m_use)) : 0.f;
-            const float p1 =
-                (col + 1 < lim) ? ex2(fmaf(__uint_as_float(rb[c & 1][e + 1]), a.scale_log2, -m_use)) : 0.f;
-            sum += p0 + p1;
+            float p0 = ex2(fmaf(__uint_as_float(rb[c & 1][e]), a.scale_log2, -m_use));
+            float p1 = ex2(fmaf(__uint_as_float(rb[c & 1][e + 1]), a.scale_log2, -m_use));
+            if (!full) {
+              p0 = (col < lim) ? p0 : 0.f;
+              p1 = (col + 1 < lim) ? p1 : 0.f;
+            }
+            sm4[(e >> 1) & 3] += p0 + p1;
             pk[e >> 1] = pack_bf16x2(p0, p1);
           }
           tc::tmem_st_32x32b_x16(tP + lane_off + c * 16, pk);
         }
-        l += sum;
+        l += (sm4[0] + sm4[1]) + (sm4[2] + sm4[3]);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
