@@ -75,3 +75,23 @@ def test_bwd(B, N, H, causal):
     ro.backward(do.float().view(B, N, H, 64))
     for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
         assert rel(got.reshape(B, N, H, 64), ref) < 2e-2
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_fwd_large_dynamic_range(causal):
+    """Scores growing along the key axis force deferred rescales and the > 2^64 recompute path."""
+    B, N, H = 1, 700, 2
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn(B, N, H, 64, generator=g, device="cuda")
+    k = torch.randn(B, N, H, 64, generator=g, device="cuda")
+    v = torch.randn(B, N, H, 64, generator=g, device="cuda")
+    ramp = torch.linspace(0.0, 30.0, N, device="cuda").view(1, N, 1, 1)
+    q = (q.abs() * 2.0).to(torch.bfloat16)
+    k = (k.abs() * ramp / 8.0).to(torch.bfloat16)
+    v = v.to(torch.bfloat16)
+    o, lse = ops.attn_fwd(q.reshape(B, N, H * 64), k.reshape(B, N, H * 64), v.reshape(B, N, H * 64), H,
+                          causal=causal)
+    ro, rlse = ref_attn(q, k, v, 0.125, causal)
+    assert torch.isfinite(o.float()).all()
+    assert rel(o.view(B, N, H, 64), ro) < 2e-2
+    assert ((lse.view(B, H, -1)[:, :, :N] - rlse).abs() / rlse.abs().clamp_min(1.0)).max().item() < 1e-3
