@@ -168,117 +168,93 @@ __global__ void __launch_bounds__(320, 1)
       const int row = quad * 32 + lane;
       const int qi = q0 + g * BT + row;
       const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-      // Single-pass online softmax against a lagging reference max m_ref (log2 units):
-      //   P(j) = exp2(s*scale - m_ref), the tile max is tracked alongside; when it exceeds m_ref by
-      //   more than kRescaleThresh, O and l are rescaled to the new max at the start of tile j+1
-      //   (after PV(j) has landed in O).  A jump > 64 (fp32 range safety) recomputes the tile.
-      float m_ref = -INFINITY, m_pend = -INFINITY, l = 0.f;
+      float m_run = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         tc::mbar_wait(s_full, j & 1);
         tc::tc_fence_after();
         const int kv0 = j * BT;
         int lim = a.N - kv0;
         if (a.causal) lim = min(lim, qi - kv0 + 1);
-        const bool full = lim >= BT;
+        // pass 1: row max (two TMEM round trips of 64 columns), 8 independent max chains
+        const bool full = lim >= BT;   // warp-uniform in the non-causal case: no per-element masking
+        float mxa[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mxa[k] = -INFINITY;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t r0[32], r1[32];
+          tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64, r0);
+          tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64 + 32, r1);
+          tc::tmem_ld_wait();
+          if (full) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r0[e]));
+              mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r1[e]));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              if (hh * 64 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r0[e]));
+              if (hh * 64 + 32 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r1[e]));
+            }
+          }
+        }
+        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+        const float m_new = fmaxf(m_run, mx * a.scale_log2);
         if (j > 0) {
           tc::mbar_wait(o_full, (j - 1) & 1);  // PV(j-1) done: O stable, P buffer free
           tc::tc_fence_after();
         }
-        // deferred rescale decided at the end of the previous tile (warp-uniform: TMEM ops are collective)
-        if (__any_sync(0xffffffff, m_pend > m_ref)) {
-          const float m_new = fmaxf(m_pend, m_ref);
-          const float alpha = (m_ref == -INFINITY) ? 0.f : ex2(m_ref - m_new);
-          if (j > 0) {
+        // warp-uniform lazy rescale of the TMEM accumulator (tcgen05.ld/st are warp-collective)
+        const bool need = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + kRescaleThresh);
+        if (j > 0 && __any_sync(0xffffffff, need)) {
+          const float alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              uint32_t r[32];
-              tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
-              tc::tmem_ld_wait();
+          for (int c = 0; c < 2; ++c) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
+            tc::tmem_ld_wait();
 #pragma unroll
-              for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-              tc::tmem_st_32x32b_x32(tO + lane_off + c * 32, r);
-            }
+            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            tc::tmem_st_32x32b_x32(tO + lane_off + c * 32, r);
           }
           l *= alpha;
-          m_ref = m_new;
+          m_run = m_new;
+        } else if (j == 0) {
+          m_run = m_new;
         }
-        for (int attempt = 0; attempt < 2; ++attempt) {
-          if (m_ref == -INFINITY && attempt == 0) {
-            // first valid tile of this row: exact max first (one extra TMEM pass)
-            float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        // pass 2: p = exp2(s*scale - m), row sum (4 chains), bf16 pack straight into the TMEM P tile
+        float sm4[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t rb[2][32];
+        tc::tmem_ld_32x32b_x32(tS + lane_off, rb[0]);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t r[32];
-              tc::tmem_ld_32x32b_x32(tS + lane_off + c * 32, r);
-              tc::tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          tc::tmem_ld_wait();
+          if (c + 1 < 4) tc::tmem_ld_32x32b_x32(tS + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
+          uint32_t pk[16];
 #pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (c * 32 + e < lim) mxa[e & 3] = fmaxf(mxa[e & 3], __uint_as_float(r[e]));
+          for (int e = 0; e < 32; e += 2) {
+            const int col = c * 32 + e;
+            float p0 = ex2(fmaf(__uint_as_float(rb[c & 1][e]), a.scale_log2, -m_use));
+            float p1 = ex2(fmaf(__uint_as_float(rb[c & 1][e + 1]), a.scale_log2, -m_use));
+            if (!full) {
+              p0 = (col < lim) ? p0 : 0.f;
+              p1 = (col + 1 < lim) ? p1 : 0.f;
             }
-            const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
-            m_ref = (mx == -INFINITY) ? -INFINITY : mx * a.scale_log2;
+            sm4[(e >> 1) & 3] += p0 + p1;
+            pk[e >> 1] = pack_bf16x2(p0, p1);
           }
-          const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-          float sm4[4] = {0.f, 0.f, 0.f, 0.f};
-          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-          uint32_t rb[2][32];
-          tc::tmem_ld_32x32b_x32(tS + lane_off, rb[0]);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            tc::tmem_ld_wait();
-            if (c + 1 < 4) tc::tmem_ld_32x32b_x32(tS + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
-            uint32_t pk[16];
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const int col = c * 32 + e;
-              const float s0 = __uint_as_float(rb[c & 1][e]), s1 = __uint_as_float(rb[c & 1][e + 1]);
-              float p0 = ex2(fmaf(s0, a.scale_log2, -m_use));
-              float p1 = ex2(fmaf(s1, a.scale_log2, -m_use));
-              if (full) {
-                mx4[(e >> 1) & 3] = fmaxf(mx4[(e >> 1) & 3], fmaxf(s0, s1));
-              } else {
-                p0 = (col < lim) ? p0 : 0.f;
-                p1 = (col + 1 < lim) ? p1 : 0.f;
-                if (col < lim) mx4[(e >> 1) & 3] = fmaxf(mx4[(e >> 1) & 3], s0);
-                if (col + 1 < lim) mx4[(e >> 1) & 3] = fmaxf(mx4[(e >> 1) & 3], s1);
-              }
-              sm4[(e >> 1) & 3] += p0 + p1;
-              pk[e >> 1] = pack_bf16x2(p0, p1);
-            }
-            tc::tmem_st_32x32b_x16(tP + lane_off + c * 16, pk);
-          }
-          const float tmx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-          const float tm = (tmx == -INFINITY) ? -INFINITY : tmx * a.scale_log2;
-          // far above the reference (p could overflow fp32 / lose all other mass): redo with it
-          if (attempt == 0 && __any_sync(0xffffffff, m_ref != -INFINITY && tm > m_ref + 64.f)) {
-            const float m_new = fmaxf(tm, m_ref);
-            const float alpha = (m_ref == -INFINITY) ? 0.f : ex2(m_ref - m_new);
-            if (j > 0) {
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                uint32_t r[32];
-                tc::tmem_ld_32x32b_x32(tO + lane_off + c * 32, r);
-                tc::tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-                tc::tmem_st_32x32b_x32(tO + lane_off + c * 32, r);
-              }
-            }
-            l *= alpha;
-            m_ref = m_new;
-            tc::tmem_st_wait();
-            continue;
-          }
-          l += (sm4[0] + sm4[1]) + (sm4[2] + sm4[3]);
-          m_pend = (tm > m_ref + kRescaleThresh) ? tm : -INFINITY;
-          break;
+          tc::tmem_st_32x32b_x16(tP + lane_off + c * 16, pk);
         }
+        l += (sm4[0] + sm4[1]) + (sm4[2] + sm4[3]);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);   // also frees S_g for S_g(j+1)
       }
-      const float m_run = m_ref;
       tc::mbar_wait(o_full, (nkv - 1) & 1);
       tc::tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
