@@ -95,10 +95,10 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
 
     for n, fn in orig.items():
         f = counted(n, fn)
-        if n in ("attn_fwd", "attn_bwd"):
-            f = timer.wrap(n, f)
-        elif n == "gemm":
+        if n == "gemm":
             f = timer.wrap(n, f, keyfn=gemm_key)
+        else:
+            f = timer.wrap(n, f)
         setattr(ops, n, f)
 
     from .dp import GradBucketReducer
@@ -109,12 +109,15 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
 
     from . import transform as TR
 
+    k1 = timer.wrap("k1_transform", TR.transform)
+    zero = timer.wrap("grad_zero", lambda: store.grad.zero_())
+
     def step():
         counts["n"] += 2  # grad memset + transform
-        store.grad.zero_()
+        zero()
         loss.zero_()
-        TR.transform(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet",
-                     tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
+        k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet",
+           tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
         model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
         reducer.finish()
         model.optimizer_step(grad_scale=1.0 / world)
@@ -155,6 +158,9 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     if "gemm" in fam:
         gms = fam["gemm"]["total_ms"] / args.steps
         kern["gemm_all"] = dict(fam["gemm"], tflops=gemm_flops_step / (gms / 1e3) / 1e12)
+    for k, v in fam.items():
+        if ":" not in k and k not in ("attn_fwd", "attn_bwd", "gemm"):
+            kern[k] = dict(v)
     step_ms_events = ms
     for k in kern:
         kern[k]["share_of_step"] = kern[k]["total_ms"] / args.steps / step_ms_events
@@ -166,7 +172,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
             shapes[k[5:]] = {"ms_per_step": v["total_ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                              "tflops": fl / (v["avg_ms"] / 1e3) / 1e12}
     shapes = dict(sorted(shapes.items(), key=lambda kv: -kv[1]["ms_per_step"])[:16])
-    dom = max(kern, key=lambda k: kern[k]["total_ms"]) if kern else None
+    dom = max((k for k in kern if k in ("attn_fwd", "attn_bwd", "gemm_all")), key=lambda k: kern[k]["total_ms"])
     roof = None
     if dom:
         roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["tflops"], "peak": pk["bf16_tflops_sustained"],
