@@ -19,6 +19,10 @@
 //      coalesced along Wt.
 #include "common.cuh"
 
+#include <algorithm>
+#include <math.h>
+#include <stdlib.h>
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -266,6 +270,194 @@ __global__ void __launch_bounds__(kThreads) k1_rrc_normalize_kernel(const K1Para
   }
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// K1 v2 (fast path: interleaved RGB, 4-byte aligned rows).
+//   grid = (column strips, T, B); a CTA owns one strip of output columns of one frame and walks
+//   down the frame in bands of R output rows.  Per band, the strip's source bytes of the rows the
+//   band touches are copied with 16-byte cp.async (aligned chunks, zero-filled past the row end)
+//   into one of two staging buffers while the previous band is computed (double buffering).
+//   Because every row pitch is a multiple of 4, all staged rows share the same sub-word shift m4,
+//   so the vertical pass reads whole 32-bit words at a per-row word offset; bytes become floats
+//   with one PRMT + one FADD2 (0x4B0000xx - 2^23) and accumulate with packed FFMA2.  The
+//   horizontal pass then reads the fp32 band per (row, output column) for all three channels.
+struct K1v2Params {
+  const uint8_t* src;
+  int64_t s_clip, s_t, s_h;
+  int T, H, W, Ht, Wt;
+  const int32_t* boxes;
+  const uint8_t* flips;
+  float scale[3], bias[3];
+  void* dst;
+  int out_dtype, out_layout, tt, tph, tpw;
+  int R, strips, cps;           // rows per band, column strips, output columns per strip
+  int tx_cap, ty_cap;           // tap-table strides
+  int rows_cap, rowb_cap;       // staging rows per band, staged bytes per row (multiple of 16)
+  int64_t total_bytes;          // bytes of the source tensor (cp.async zero-fill guard)
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return r;
+}
+
+__device__ __forceinline__ int64_t k1_out_index(const K1v2Params& p, int64_t b, int c, int t, int y, int j) {
+  const int64_t plane = (int64_t)p.Ht * p.Wt;
+  if (p.out_layout == AVB_LAYOUT_CTHW) return ((b * 3 + c) * p.T + t) * plane + (int64_t)y * p.Wt + j;
+  if (p.out_layout == AVB_LAYOUT_TCHW) return ((b * p.T + t) * 3 + c) * plane + (int64_t)y * p.Wt + j;
+  const int npy = p.Ht / p.tph, npx = p.Wt / p.tpw;
+  const int64_t Np = (int64_t)(p.T / p.tt) * npy * npx;
+  const int F = 3 * p.tt * p.tph * p.tpw;
+  const int64_t n = ((int64_t)(t / p.tt) * npy + y / p.tph) * npx + j / p.tpw;
+  const int f = ((c * p.tt + t % p.tt) * p.tph + y % p.tph) * p.tpw + j % p.tpw;
+  return (b * Np + n) * F + f;
+}
+
+__global__ void __launch_bounds__(kThreads) k1v2_kernel(const K1v2Params p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int strip = blockIdx.x, t = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int tid = threadIdx.x;
+  const int4 box = *reinterpret_cast<const int4*>(p.boxes + 4 * b);
+  const int x0 = box.x, y0 = box.y, cw = box.z, ch = box.w;
+  if (x0 < 0 || y0 < 0 || cw < 1 || ch < 1 || x0 + cw > p.W || y0 + ch > p.H) return;
+  const bool flip = p.flips ? (p.flips[b] != 0) : false;
+  // this strip, in unflipped column space jj; output column j = flip ? Wt-1-jj : jj
+  const int jj0 = strip * p.cps;
+  const int jj1 = min(p.Wt, jj0 + p.cps);
+  const int nj = jj1 - jj0;
+  if (nj <= 0) return;
+
+  // ---- smem carve-up
+  float* wx = reinterpret_cast<float*>(smem);                 // [cps][tx_cap]
+  int* xlo = reinterpret_cast<int*>(wx + p.cps * p.tx_cap);   // [cps]
+  float* wy = reinterpret_cast<float*>(xlo + p.cps);          // [Ht][ty_cap]
+  int* ylo = reinterpret_cast<int*>(wy + p.Ht * p.ty_cap);    // [Ht]
+  int* yn = ylo + p.Ht;                                       // [Ht]
+  int* rmis = yn + p.Ht;                                      // [2][rows_cap] per staged row: mis - m4
+  size_t off = (reinterpret_cast<uint8_t*>(rmis + 2 * p.rows_cap) - smem + 15) & ~size_t(15);
+  uint8_t* stage = smem + off;                                // [2][rows_cap][rowb_cap]
+  float* vbuf = reinterpret_cast<float*>(stage + 2 * (size_t)p.rows_cap * p.rowb_cap);  // [R][rowb_cap]
+
+  for (int k = tid; k < nj; k += kThreads) {
+    int lo;
+    const int n = k1_taps(cw, p.Wt, jj0 + k, wx + k * p.tx_cap, lo);
+    for (int e = n; e < p.tx_cap; ++e) wx[k * p.tx_cap + e] = 0.f;
+    xlo[k] = lo;
+  }
+  for (int r = tid; r < p.Ht; r += kThreads) {
+    int lo;
+    const int n = k1_taps(ch, p.Ht, r, wy + r * p.ty_cap, lo);
+    ylo[r] = lo;
+    yn[r] = n;
+  }
+  __syncthreads();
+  // strip source columns (crop-local) [sx0, sx1)
+  const int sx0 = xlo[0];
+  const int sx1 = min(cw, xlo[nj - 1] + p.tx_cap);
+  const int nbytes = (sx1 - sx0) * 3;
+  const uint8_t* frame = p.src + b * p.s_clip + (int64_t)t * p.s_t;
+  const uintptr_t first = reinterpret_cast<uintptr_t>(frame + (int64_t)y0 * p.s_h + (int64_t)(x0 + sx0) * 3);
+  const int m4 = (int)(first & 3);
+  const int nwords = (nbytes + m4 + 3) >> 2;
+  const uint8_t* src_end = p.src + p.total_bytes;
+  const int nbands = (p.Ht + p.R - 1) / p.R;
+
+  auto issue_band = [&](int band, int buf) {
+    const int i0 = band * p.R, i1 = min(p.Ht, i0 + p.R);
+    const int r_lo = ylo[i0], r_hi = ylo[i1 - 1] + yn[i1 - 1];
+    const int nrows = r_hi - r_lo;
+    uint8_t* sb = stage + (size_t)buf * p.rows_cap * p.rowb_cap;
+    const int chunks = (nbytes + m4 + 15 + 12) >> 4;   // mis <= 15
+    for (int idx = tid; idx < nrows * chunks; idx += kThreads) {
+      const int rr = idx / chunks, k = idx - rr * chunks;
+      const uint8_t* a = frame + (int64_t)(y0 + r_lo + rr) * p.s_h + (int64_t)(x0 + sx0) * 3;
+      const uintptr_t al = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
+      const uint8_t* g = reinterpret_cast<const uint8_t*>(al) + 16 * k;
+      const int64_t left = src_end - g;
+      const int nb = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
+      if (16 * k < (int)(reinterpret_cast<uintptr_t>(a) - al) + nbytes)
+        cp_async16(sb + (size_t)rr * p.rowb_cap + 16 * k, nb ? g : p.src, nb);
+      if (k == 0) rmis[buf * p.rows_cap + rr] = (int)(reinterpret_cast<uintptr_t>(a) - al) - m4;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  issue_band(0, 0);
+  for (int band = 0; band < nbands; ++band) {
+    const int buf = band & 1;
+    if (band + 1 < nbands) {
+      issue_band(band + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int i0 = band * p.R, nR = min(p.R, p.Ht - i0);
+    const int r_lo = ylo[i0];
+    const uint8_t* sb = stage + (size_t)buf * p.rows_cap * p.rowb_cap;
+    const int* mis = rmis + buf * p.rows_cap;
+    // vertical pass: shifted byte columns u' = 4q..4q+3 of the strip (u' = crop byte - sx0*3 + m4)
+    for (int idx = tid; idx < nR * nwords; idx += kThreads) {
+      const int r = idx / nwords, q = idx - r * nwords;
+      const int base = ylo[i0 + r] - r_lo, n = yn[i0 + r];
+      const float* w = wy + (i0 + r) * p.ty_cap;
+      float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+      for (int k = 0; k < n; ++k) {
+        const int rr = base + k;
+        const uint32_t u = *reinterpret_cast<const uint32_t*>(sb + (size_t)rr * p.rowb_cap + mis[rr] + 4 * q);
+        const float2 magic = make_float2(-8388608.f, -8388608.f);
+        float2 f01 = make_float2(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7440)),
+                                 __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7441)));
+        float2 f23 = make_float2(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7442)),
+                                 __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7443)));
+        f01.x += magic.x; f01.y += magic.y;
+        f23.x += magic.x; f23.y += magic.y;
+        const float2 ww = make_float2(w[k], w[k]);
+        a01 = ffma2(ww, f01, a01);
+        a23 = ffma2(ww, f23, a23);
+      }
+      *reinterpret_cast<float4*>(vbuf + (size_t)r * p.rowb_cap + 4 * q) = make_float4(a01.x, a01.y, a23.x, a23.y);
+    }
+    __syncthreads();
+    // horizontal pass + normalize + store: item = (row, strip column)
+    for (int idx = tid; idx < nR * nj; idx += kThreads) {
+      const int r = idx / nj, k = idx - r * nj;
+      const int jj = jj0 + k;
+      const int j = flip ? (p.Wt - 1 - jj) : jj;
+      const float* w = wx + k * p.tx_cap;
+      const int lim = min(p.tx_cap, cw - xlo[k]);
+      const float* v = vbuf + (size_t)r * p.rowb_cap + (xlo[k] - sx0) * 3 + m4;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+      for (int e = 0; e < lim; ++e) {
+        const float we = w[e];
+        a0 = fmaf(we, v[3 * e], a0);
+        a1 = fmaf(we, v[3 * e + 1], a1);
+        a2 = fmaf(we, v[3 * e + 2], a2);
+      }
+      const float ys[3] = {fmaf(a0, p.scale[0], p.bias[0]), fmaf(a1, p.scale[1], p.bias[1]),
+                           fmaf(a2, p.scale[2], p.bias[2])};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t o = k1_out_index(p, b, c, t, i0 + r, j);
+        if (p.out_dtype == AVB_DTYPE_BF16)
+          reinterpret_cast<__nv_bfloat16*>(p.dst)[o] = __float2bfloat16_rn(ys[c]);
+        else
+          reinterpret_cast<float*>(p.dst)[o] = ys[c];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 extern "C" int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_dev,
@@ -347,7 +539,39 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k1_rrc_normalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k1v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
+  }
+  const bool v2ok = p.fast && (s_h % 4 == 0) && (s_t % 4 == 0) && (s_clip % 4 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(src) & 3) == 0) && !getenv("AVB_K1_V1");
+  if (v2ok) {
+    K1v2Params q;
+    q.src = src; q.s_clip = s_clip; q.s_t = s_t; q.s_h = s_h;
+    q.T = T; q.H = H; q.W = W; q.Ht = Ht; q.Wt = Wt;
+    q.boxes = boxes_dev; q.flips = hflip_dev;
+    for (int c = 0; c < 3; ++c) { q.scale[c] = p.scale[c]; q.bias[c] = p.bias[c]; }
+    q.dst = dst; q.out_dtype = out_dtype; q.out_layout = out_layout; q.tt = tt; q.tph = tph; q.tpw = tpw;
+    q.tx_cap = tx_cap; q.ty_cap = ty_cap;
+    q.total_bytes = (B - 1) * s_clip + (int64_t)(T - 1) * s_t + (int64_t)(H - 1) * s_h + (int64_t)W * 3;
+    q.strips = Wt >= 160 ? 2 : 1;
+    q.cps = (Wt + q.strips - 1) / q.strips;
+    // worst-case strip source width: every column of a full-width crop
+    const int strip_src = (int)std::min<int64_t>(W, (int64_t)((double)W / Wt * q.cps) + tx_cap + 2);
+    q.rowb_cap = ((strip_src * 3 + 15 + 16 + 4) / 16) * 16;
+    size_t smem = 0;
+    for (q.R = 16; q.R >= 1; q.R >>= 1) {
+      q.rows_cap = std::min(H, (int)ceil(sy * (q.R + 1)) + 4);
+      size_t head = sizeof(float) * ((size_t)q.cps * tx_cap + (size_t)Ht * ty_cap) +
+                    sizeof(int) * ((size_t)q.cps + 2 * (size_t)Ht + 2 * (size_t)q.rows_cap);
+      head = (head + 15) & ~size_t(15);
+      smem = head + 2 * (size_t)q.rows_cap * q.rowb_cap + sizeof(float) * (size_t)q.R * q.rowb_cap;
+      if (smem <= 100 * 1024) break;
+    }
+    if (q.R >= 1) {
+      dim3 g2(q.strips, T, (unsigned)B);
+      k1v2_kernel<<<g2, kThreads, smem, avb::as_stream(stream)>>>(q);
+      return avb::launch_status("avb_rrc_normalize");
+    }
   }
   dim3 grid((Ht + R - 1) / R, T, (unsigned)B);
   AVB_CHECK_ARG(B <= 65535 && T <= 65535, "B and T must be <= 65535");
