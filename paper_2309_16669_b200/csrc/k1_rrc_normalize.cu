@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(kThreads) k1v2_kernel(const K1v2Params p) {
   // ---- smem carve-up
   float* wx = reinterpret_cast<float*>(smem);                 // [cps][tx_cap]
   int* xlo = reinterpret_cast<int*>(wx + p.cps * p.tx_cap);   // [cps]
-  float* wy = reinterpret_cast<float*>(xlo + p.cps);          // [Ht][ty_cap]
+  int* xn = xlo + p.cps;                                      // [cps] taps per column
+  float* wy = reinterpret_cast<float*>(xn + p.cps);           // [Ht][ty_cap]
   int* ylo = reinterpret_cast<int*>(wy + p.Ht * p.ty_cap);    // [Ht]
   int* yn = ylo + p.Ht;                                       // [Ht]
   int* rmis = yn + p.Ht;                                      // [2][rows_cap] per staged row: mis - m4
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(kThreads) k1v2_kernel(const K1v2Params p) {
     const int n = k1_taps(cw, p.Wt, jj0 + k, wx + k * p.tx_cap, lo);
     for (int e = n; e < p.tx_cap; ++e) wx[k * p.tx_cap + e] = 0.f;
     xlo[k] = lo;
+    xn[k] = n;
   }
   for (int r = tid; r < p.Ht; r += kThreads) {
     int lo;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(kThreads) k1v2_kernel(const K1v2Params p) {
       const int jj = jj0 + k;
       const int j = flip ? (p.Wt - 1 - jj) : jj;
       const float* w = wx + k * p.tx_cap;
-      const int lim = min(p.tx_cap, cw - xlo[k]);
+      const int lim = xn[k];
       const float* v = vbuf + (size_t)r * p.rowb_cap + (xlo[k] - sx0) * 3 + m4;
       float a0 = 0.f, a1 = 0.f, a2 = 0.f;
       for (int e = 0; e < lim; ++e) {
@@ -562,7 +564,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     for (q.R = 16; q.R >= 1; q.R >>= 1) {
       q.rows_cap = std::min(H, (int)ceil(sy * (q.R + 1)) + 4);
       size_t head = sizeof(float) * ((size_t)q.cps * tx_cap + (size_t)Ht * ty_cap) +
-                    sizeof(int) * ((size_t)q.cps + 2 * (size_t)Ht + 2 * (size_t)q.rows_cap);
+                    sizeof(int) * (2 * (size_t)q.cps + 2 * (size_t)Ht + 2 * (size_t)q.rows_cap);
       head = (head + 15) & ~size_t(15);
       smem = head + 2 * (size_t)q.rows_cap * q.rowb_cap + sizeof(float) * (size_t)q.R * q.rowb_cap;
       if (smem <= 100 * 1024) break;
