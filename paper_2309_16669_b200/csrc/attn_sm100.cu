@@ -289,97 +289,82 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ---------------------------------------------------------------------------------- backward
+// Two atomic-free kernels (no dQ reduce traffic):
+//   dKdV: CTA per (128-key tile, head, clip), loop over query tiles i:
+//     S^T = K Q_i^T, dP^T = V dO_i^T (TMEM) -> P^T = exp2(S^T*scale*log2e - LSE2), dS^T = scale P^T (dP^T - delta)
+//     written as bf16 into TMEM -> dV += P^T dO_i, dK += dS^T Q_i (A-from-TMEM MMAs, dO_i / Q_i MN-major).
+//   dQ:   CTA per (128-query tile, head, clip), loop over key tiles j:
+//     S = Q K_j^T, dP = dO V_j^T -> P, dS (thread = query row: its LSE / delta live in registers)
+//     -> dQ += dS K_j accumulated in TMEM, stored once as bf16.
 struct BwdArgs {
   int B, H, N, Npad;
   float scale, scale_log2;
   const float* lse;
   const float* delta;
+  __nv_bfloat16* dq;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
-  int64_t ld_g, sb_g;     // strides of dk/dv
+  int64_t ld_g, sb_g;     // strides of dq/dk/dv
   int causal;
 };
 
-// smem (dynamic base must be 1 KB aligned; checked): all 128B-swizzled bf16 tiles first
-constexpr int B_SK = 0, B_SV = 16384;
-constexpr int B_SQD = 32768;                  // 2 stages x (Q 16K + dO 16K)
-constexpr int B_SPT = B_SQD + 2 * 32768;      // 2 buffers x P^T 32K (also dQ fp32 staging)
-constexpr int B_SDS = B_SPT + 2 * 32768;      // 2 buffers x dS^T 32K
-constexpr int B_SLD = B_SDS + 2 * 32768;      // 2 stages x (lse 512 + delta 512)
-constexpr int B_BAR = B_SLD + 2 * 1024;
-constexpr int B_SMEM = B_BAR + 128;
-static_assert(B_SMEM <= 232448, "attn bwd smem");
-constexpr int kBwdCompute = 8;               // compute warps (2 per TMEM lane quadrant)
+constexpr int kBwdCompute = 8;   // compute warps (2 per TMEM lane quadrant, split by column half)
+constexpr int KV_STAGES = 3;
+// dKdV smem: K, V (resident), KV_STAGES x (Q 16K + dO 16K), KV_STAGES x (lse 512 + delta 512), barriers
+constexpr int D_SK = 0, D_SV = 16384, D_SQD = 32768;
+constexpr int D_SLD = D_SQD + KV_STAGES * 32768;
+constexpr int D_BAR = D_SLD + KV_STAGES * 1024;
+constexpr int D_SMEM = D_BAR + 256;
+// dQ smem: Q, dO (resident), KV_STAGES x (K 16K + V 16K), barriers
+constexpr int Q_SQ = 0, Q_SDO = 16384, Q_SKV = 32768;
+constexpr int Q_BAR = Q_SKV + KV_STAGES * 32768;
+constexpr int Q_SMEM = Q_BAR + 256;
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ uint32_t pack2(float a, float b) { return pack_bf16x2(a, b); }
 
-// drain one warp's share of the dQ tile (32 query rows x 32 columns) from TMEM through a
-// 128B-swizzled fp32 staging block and reduce-add it into the fp32 accumulator with TMA
-__device__ __forceinline__ void drain_dq(uint32_t taddr, uint8_t* stage, const CUtensorMap* tmDQ, int lane, int c0,
-                                         int q0, int b) {
-  uint32_t r[32];
-  tc::tmem_ld_32x32b_x32(taddr, r);
-  tc::tmem_ld_wait();
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-    *reinterpret_cast<uint4*>(stage + lane * 128 + ((u ^ (lane & 7)) << 4)) =
-        make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
-  tc::fence_proxy_async();
-  __syncwarp();
-  if (lane == 0) {
-    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(tmDQ)),
-                 "r"(smem_u32(stage)), "r"(c0), "r"(q0), "r"(b)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
-}
-
+// --------------------------------------------------------------------------------- dK / dV
 __global__ void __launch_bounds__(320, 1)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                         const BwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
-  uint8_t* sK = smem + B_SK;
-  uint8_t* sV = smem + B_SV;
-  uint8_t* sQD = smem + B_SQD;
-  uint8_t* sPT = smem + B_SPT;
-  uint8_t* sDS = smem + B_SDS;
-  float* sLD = reinterpret_cast<float*>(smem + B_SLD);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
+  uint8_t* sK = smem + D_SK;
+  uint8_t* sV = smem + D_SV;
+  uint8_t* sQD = smem + D_SQD;
+  float* sLD = reinterpret_cast<float*>(smem + D_SLD);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + D_BAR);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_ready = bars + 6;
-  uint64_t* mma_done = bars + 7;
-  uint64_t* dq_free = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* qd_full = bars + 1;                  // [KV_STAGES]
+  uint64_t* qd_empty = bars + 1 + KV_STAGES;     // [KV_STAGES]
+  uint64_t* s_full = bars + 1 + 2 * KV_STAGES;
+  uint64_t* ds_ready = s_full + 1;
+  uint64_t* pd_free = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int kv0 = kt * BT;
   const int nq_all = (a.N + BT - 1) / BT;
-  const int i0 = a.causal ? kt : 0;  // first query tile that sees this key tile
+  const int i0 = a.causal ? kt : 0;
   const int nq = nq_all - i0;
   constexpr int kTMA = kBwdCompute, kMMA = kBwdCompute + 1;
+  // TMEM: S^T [0,128) dP^T [128,256) P^T bf16 [256,320) dS^T bf16 [320,384) dV [384,448) dK [448,512)
+  constexpr uint32_t T_ST = 0, T_DPT = 128, T_PT = 256, T_DST = 320, T_DV = 384, T_DK = 448;
 
   if (warp == kTMA && lane == 0) {
     tc::tma_prefetch(&tmQ);
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
     tc::tma_prefetch(&tmdO);
-    tc::tma_prefetch(&tmDQ);
     tc::mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < KV_STAGES; ++s) {
       tc::mbar_init(&qd_full[s], 1);
       tc::mbar_init(&qd_empty[s], 1);
     }
     tc::mbar_init(s_full, 1);
     tc::mbar_init(ds_ready, kBwdCompute);
-    tc::mbar_init(mma_done, 1);
-    tc::mbar_init(dq_free, kBwdCompute);
+    tc::mbar_init(pd_free, 1);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -387,7 +372,6 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384;
   const int64_t bh = (int64_t)b * a.H + h;
 
   if (warp == kTMA) {
@@ -396,108 +380,84 @@ __global__ void __launch_bounds__(320, 1)
       tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
       tc::tma_load_3d(sV, &tmV, kv_full, h * HD, kv0, b);
       for (int ii = 0; ii < nq; ++ii) {
-        const int i = i0 + ii, st = ii & 1;
-        tc::mbar_wait(&qd_empty[st], ((ii >> 1) & 1) ^ 1);
+        const int i = i0 + ii, st = ii % KV_STAGES;
+        tc::mbar_wait(&qd_empty[st], ((ii / KV_STAGES) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
         tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
         tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
-        const float* gl = a.lse + bh * a.Npad + i * BT;
-        const float* gd = a.delta + bh * a.Npad + i * BT;
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
                          smem_u32(sLD + st * 256)),
-                     "l"(gl), "r"(smem_u32(&qd_full[st]))
+                     "l"(a.lse + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
                      : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
                          smem_u32(sLD + st * 256 + 128)),
-                     "l"(gd), "r"(smem_u32(&qd_full[st]))
+                     "l"(a.delta + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
                      : "memory");
       }
     }
   } else if (warp == kMMA) {
     if (lane == 0) {
       constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
-      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: B (dO / Q) MN-major
-      constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
+      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: A from TMEM, B (dO / Q) MN-major
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+      auto issue_s = [&](int ii) {
+        const int st = ii % KV_STAGES;
+        tc::mbar_wait(&qd_full[st], (ii / KV_STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tmem + T_ST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
+                          idSS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tmem + T_DPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024),
+                          tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_commit(s_full);
+      };
       tc::mbar_wait(kv_full, 0);
-      for (int ii = 0; ii <= nq; ++ii) {
-        if (ii < nq) {
-          const int st = ii & 1;
-          tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);
-          if (ii > 0) tc::mbar_wait(ds_ready, (ii - 1) & 1);
-          tc::tc_fence_after();
-          const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+      issue_s(0);
+      for (int ii = 0; ii < nq; ++ii) {
+        tc::mbar_wait(ds_ready, ii & 1);     // P^T/dS^T(ii) in TMEM, S^T/dP^T consumed
+        tc::tc_fence_after();
+        if (ii + 1 < nq) issue_s(ii + 1);
+        const int st = ii % KV_STAGES;
+        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::umma_f16_ss(tST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
-                            idSS, kk > 0);
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ts(tmem + T_DV, tmem + T_PT + kk * 8, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG,
+                          (ii > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::umma_f16_ss(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
-                            idSS, kk > 0);
-          tc::umma_commit(s_full);
-        } else {
-          tc::mbar_wait(ds_ready, (ii - 1) & 1);
-        }
-        if (ii > 0) {
-          const int ps = (ii - 1) & 1;
-          const uint32_t aQ = smem_u32(sQD + ps * 32768), aDO = aQ + 16384;
-          const uint32_t aPT = smem_u32(sPT + ps * 32768), aDS = smem_u32(sDS + ps * 32768);
-          if (ii > 1) tc::mbar_wait(dq_free, (ii - 2) & 1);
-          tc::tc_fence_after();
-          const uint32_t acc = (ii > 1) ? 1u : 0u;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t dP = tc::sdesc_sw128(aPT + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-            tc::umma_f16_ss(tDV, dP, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t dS = tc::sdesc_sw128(aDS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-            tc::umma_f16_ss(tDK, dS, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
-            // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
-            const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
-            tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
-          }
-          tc::umma_commit(mma_done);
-          tc::umma_commit(&qd_empty[ps]);
-        }
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ts(tmem + T_DK, tmem + T_DST + kk * 8, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG,
+                          (ii > 0 || kk > 0) ? 1u : 0u);
+        tc::umma_commit(pd_free);
+        tc::umma_commit(&qd_empty[st]);
       }
     }
   } else {
-    // ------------------------------------------------------------ compute warps
-    // warp w: TMEM lane quadrant (w & 3) -> key rows; column half (w >> 2) of the 128 query columns
+    // compute warps: thread = key row (quadrant), column half of the 128 query columns
     const int quad = warp & 3, half = warp >> 2;
     const int row = quad * 32 + lane;
     const int kvi = kv0 + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     for (int ii = 0; ii < nq; ++ii) {
-      const int i = i0 + ii, st = ii & 1;
+      const int i = i0 + ii, st = ii % KV_STAGES;
       const int q0 = i * BT;
-      uint8_t* pt = sPT + st * 32768;
-      uint8_t* ds_t = sDS + st * 32768;
-      if (ii >= 2) {
-        // this P^T slot staged dQ(ii-2): its TMA reduce must have read the smem (all warps)
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
-        named_bar(1, 32 * kBwdCompute);
-      }
       tc::mbar_wait(s_full, ii & 1);
-      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // lse/delta landed
+      tc::mbar_wait(&qd_full[st], (ii / KV_STAGES) & 1);  // lse/delta landed
+      if (ii > 0) tc::mbar_wait(pd_free, (ii - 1) & 1);    // dV/dK(ii-1) done reading P^T/dS^T
       tc::tc_fence_after();
       const float* sl = sLD + st * 256;
       const float* sd = sl + 128;
-#pragma unroll 1
+#pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         const int c = half * 2 + cc;
         uint32_t rs[32], rp[32];
-        tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
-        tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+        tc::tmem_ld_32x32b_x32(tmem + T_ST + lane_off + c * 32, rs);
+        tc::tmem_ld_32x32b_x32(tmem + T_DPT + lane_off + c * 32, rp);
         tc::tmem_ld_wait();
+        uint32_t pk[16], dk[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float4 l0 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8);
@@ -509,52 +469,32 @@ __global__ void __launch_bounds__(320, 1)
           float p[8], ds[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int qc = c * 32 + u * 8 + e;
-            const int qi = q0 + qc;
+            const int qi = q0 + c * 32 + u * 8 + e;
             const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
             const float pe = ok ? ex2(fmaf(__uint_as_float(rs[u * 8 + e]), a.scale_log2, -lv[e] * kLog2e)) : 0.f;
             p[e] = pe;
             ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[u * 8 + e]) - dv[e]) : 0.f;
           }
-          uint4 v, w;
-          v.x = pack_bf16x2(p[0], p[1]);
-          v.y = pack_bf16x2(p[2], p[3]);
-          v.z = pack_bf16x2(p[4], p[5]);
-          v.w = pack_bf16x2(p[6], p[7]);
-          w.x = pack_bf16x2(ds[0], ds[1]);
-          w.y = pack_bf16x2(ds[2], ds[3]);
-          w.z = pack_bf16x2(ds[4], ds[5]);
-          w.w = pack_bf16x2(ds[6], ds[7]);
-          st_sw128(pt, row, c * 4 + u, v);
-          st_sw128(ds_t, row, c * 4 + u, w);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            pk[u * 4 + e] = pack2(p[2 * e], p[2 * e + 1]);
+            dk[u * 4 + e] = pack2(ds[2 * e], ds[2 * e + 1]);
+          }
         }
+        tc::tmem_st_32x32b_x16(tmem + T_PT + lane_off + c * 16, pk);
+        tc::tmem_st_32x32b_x16(tmem + T_DST + lane_off + c * 16, dk);
       }
-      tc::fence_proxy_async();
+      tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_ready);
-      if (ii > 0) {
-        // dQ(ii-1): TMEM lanes = query rows of tile i-1; stage into the P^T slot it no longer needs
-        tc::mbar_wait(mma_done, (ii - 1) & 1);
-        tc::tc_fence_after();
-        drain_dq(tDQ + lane_off + half * 32, sPT + ((ii - 1) & 1) * 32768 + warp * 4096, &tmDQ, lane,
-                 h * HD + half * 32, q0 - BT + quad * 32, b);
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(dq_free);
-      }
     }
-    // last dQ + dK/dV out
-    tc::mbar_wait(mma_done, (nq - 1) & 1);
+    // dK / dV out (thread = key row, its column half)
+    tc::mbar_wait(pd_free, (nq - 1) & 1);
     tc::tc_fence_after();
-    if (nq >= 2) {
-      // the slot of tile nq-1 staged dQ(nq-3)? no: it held P(nq-1); staging dQ(nq-1) reuses it after mma_done
-    }
-    drain_dq(tDQ + lane_off + half * 32, sPT + ((nq - 1) & 1) * 32768 + warp * 4096, &tmDQ, lane, h * HD + half * 32,
-             (i0 + nq - 1) * BT + quad * 32, b);
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
-      const uint32_t tsrc = which ? tDK : tDV;
+      const uint32_t tsrc = tmem + (which ? T_DK : T_DV);
       __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + half * 32;
       uint32_t r[32];
       tc::tmem_ld_32x32b_x32(tsrc + lane_off + half * 32, r);
@@ -563,16 +503,184 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
-          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
-          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
-          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+          v.x = pack2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+          v.y = pack2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+          v.z = pack2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+          v.w = pack2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
           reinterpret_cast<uint4*>(g)[u] = v;
         }
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    __syncwarp();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == kMMA) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+// --------------------------------------------------------------------------------- dQ
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                       const BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
+  uint8_t* sQ = smem + Q_SQ;
+  uint8_t* sDO = smem + Q_SDO;
+  uint8_t* sKV = smem + Q_SKV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Q_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;                  // [KV_STAGES]
+  uint64_t* kv_empty = bars + 1 + KV_STAGES;     // [KV_STAGES]
+  uint64_t* s_full = bars + 1 + 2 * KV_STAGES;
+  uint64_t* ds_ready = s_full + 1;
+  uint64_t* ds_free = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qt * BT;
+  const int nkv_all = (a.N + BT - 1) / BT;
+  const int nkv = a.causal ? min(nkv_all, qt + 1) : nkv_all;
+  constexpr int kTMA = kBwdCompute, kMMA = kBwdCompute + 1;
+  // TMEM: S [0,128) dP [128,256) dS bf16 [256,320) dQ [320,384)
+  constexpr uint32_t T_S = 0, T_DP = 128, T_DS = 256, T_DQ = 320;
+
+  if (warp == kTMA && lane == 0) {
+    tc::tma_prefetch(&tmQ);
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmV);
+    tc::tma_prefetch(&tmdO);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < KV_STAGES; ++s) {
+      tc::mbar_init(&kv_full[s], 1);
+      tc::mbar_init(&kv_empty[s], 1);
+    }
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(ds_ready, kBwdCompute);
+    tc::mbar_init(ds_free, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kTMA) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(q_full, 32768);
+      tc::tma_load_3d(sQ, &tmQ, q_full, h * HD, q0, b);
+      tc::tma_load_3d(sDO, &tmdO, q_full, h * HD, q0, b);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % KV_STAGES;
+        tc::mbar_wait(&kv_empty[st], ((j / KV_STAGES) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&kv_full[st], 32768);
+        tc::tma_load_3d(sKV + st * 32768, &tmK, &kv_full[st], h * HD, j * BT, b);
+        tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
+      }
+    }
+  } else if (warp == kMMA) {
+    if (lane == 0) {
+      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
+      constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 0, 1);    // dQ: A = dS from TMEM, B = K MN-major
+      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO);
+      auto issue_s = [&](int j) {
+        const int st = j % KV_STAGES;
+        tc::mbar_wait(&kv_full[st], (j / KV_STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t aK = smem_u32(sKV + st * 32768), aV = aK + 16384;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tmem + T_S, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024),
+                          idSS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tmem + T_DP, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), tc::sdesc_sw128(aV + kk * 32, 16, 1024),
+                          idSS, kk > 0);
+        tc::umma_commit(s_full);
+      };
+      tc::mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        tc::mbar_wait(ds_ready, j & 1);     // dS(j) in TMEM, S/dP(j) consumed
+        tc::tc_fence_after();
+        if (j + 1 < nkv) issue_s(j + 1);
+        const int st = j % KV_STAGES;
+        const uint32_t aK = smem_u32(sKV + st * 32768);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ts(tmem + T_DQ, tmem + T_DS + kk * 8, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ,
+                          (j > 0 || kk > 0) ? 1u : 0u);
+        tc::umma_commit(ds_free);
+        tc::umma_commit(&kv_empty[st]);
+      }
+    }
+  } else {
+    // compute warps: thread = query row (quadrant), column half of the 128 key columns
+    const int quad = warp & 3, half = warp >> 2;
+    const int row = quad * 32 + lane;
+    const int qi = q0 + row;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int64_t bh = (int64_t)b * a.H + h;
+    const float lse2 = (qi < a.N) ? a.lse[bh * a.Npad + qi] * kLog2e : 0.f;
+    const float dlt = (qi < a.N) ? a.delta[bh * a.Npad + qi] : 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int kv0 = j * BT;
+      tc::mbar_wait(s_full, j & 1);
+      if (j > 0) tc::mbar_wait(ds_free, (j - 1) & 1);   // dQ(j-1) MMA done reading dS
+      tc::tc_fence_after();
+      int lim = a.N - kv0;
+      if (a.causal) lim = min(lim, qi - kv0 + 1);
+      if (qi >= a.N) lim = 0;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = half * 2 + cc;
+        uint32_t rs[32], rp[32];
+        tc::tmem_ld_32x32b_x32(tmem + T_S + lane_off + c * 32, rs);
+        tc::tmem_ld_32x32b_x32(tmem + T_DP + lane_off + c * 32, rp);
+        tc::tmem_ld_wait();
+        uint32_t dk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int col = c * 32 + e;
+          float d0 = 0.f, d1 = 0.f;
+          if (col < lim) {
+            const float p0 = ex2(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2));
+            d0 = a.scale * p0 * (__uint_as_float(rp[e]) - dlt);
+          }
+          if (col + 1 < lim) {
+            const float p1 = ex2(fmaf(__uint_as_float(rs[e + 1]), a.scale_log2, -lse2));
+            d1 = a.scale * p1 * (__uint_as_float(rp[e + 1]) - dlt);
+          }
+          dk[e >> 1] = pack2(d0, d1);
+        }
+        tc::tmem_st_32x32b_x16(tmem + T_DS + lane_off + c * 16, dk);
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(ds_ready);
+    }
+    tc::mbar_wait(ds_free, (nkv - 1) & 1);
+    tc::tc_fence_after();
+    uint32_t r[32];
+    tc::tmem_ld_32x32b_x32(tmem + T_DQ + lane_off + half * 32, r);
+    tc::tmem_ld_wait();
+    if (qi < a.N) {
+      __nv_bfloat16* g = a.dq + (int64_t)b * a.sb_g + (int64_t)qi * a.ld_g + h * HD + half * 32;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint4 v;
+        v.x = pack2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+        v.y = pack2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+        v.z = pack2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+        v.w = pack2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+        reinterpret_cast<uint4*>(g)[u] = v;
+      }
+    }
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -610,9 +718,11 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
   s += __shfl_xor_sync(0xffffffff, s, 2);
   s += __shfl_xor_sync(0xffffffff, s, 4);
   if (sub == 0) delta[((int64_t)b * H + h) * Npad + n] = s;
-  float4* z = reinterpret_cast<float4*>(dq_acc + item * HD + sub * 8);
-  z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-  z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (dq_acc) {
+    float4* z = reinterpret_cast<float4*>(dq_acc + item * HD + sub * 8);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int64_t ld,
@@ -689,19 +799,20 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   AVB_CHECK_ARG(head_dim == HD, "head_dim must be 64 (got %d)", head_dim);
   AVB_CHECK_ARG(B >= 0 && H >= 1 && N >= 0, "bad attention dims");
   if (B == 0 || N == 0) return AVB_OK;
-  AVB_CHECK_ARG(q && k && v && o && dout && lse && delta && dq_acc && dq && dk && dv, "null pointer");
+  AVB_CHECK_ARG(q && k && v && o && dout && lse && delta && dq && dk && dv, "null pointer");
   AVB_CHECK_ARG(aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && aligned16(dout) && aligned16(dq) &&
-                    aligned16(dk) && aligned16(dv) && aligned16(lse) && aligned16(delta) && aligned16(dq_acc),
+                    aligned16(dk) && aligned16(dv) && aligned16(lse) && aligned16(delta),
                 "pointers must be 16-byte aligned");
   AVB_CHECK_ARG(ld % 8 == 0 && sb % 8 == 0 && ld_o % 8 == 0 && sb_o % 8 == 0 && ld_g % 8 == 0 && sb_g % 8 == 0,
                 "strides must be multiples of 8 elements");
+  (void)dq_acc;  // the atomic-free backward needs no fp32 dQ accumulator (kept for ABI stability)
   cudaStream_t st = avb::as_stream(stream);
   const int Npad = (N + BT - 1) / BT * BT;
   {
     const int64_t threads = (int64_t)B * N * H * 8;
     attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(o), ld_o, sb_o, reinterpret_cast<const __nv_bfloat16*>(dout), ld_o,
-        sb_o, delta, dq_acc, B, H, N, Npad);
+        sb_o, delta, nullptr, B, H, N, Npad);
     int s = avb::launch_status("attn_bwd_pre");
     if (s) return s;
   }
@@ -711,10 +822,6 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
   if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
   if ((s = make_maps(&mdo, dout, B, H, N, ld_o, sb_o))) return s;
-  CUtensorMap mdq;
-  if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
-                                 (uint64_t)N * H * HD, 32, 32, 1)))
-    return s;
   BwdArgs a;
   a.B = B;
   a.H = H;
@@ -724,6 +831,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.scale_log2 = softmax_scale * kLog2e;
   a.lse = lse;
   a.delta = delta;
+  a.dq = reinterpret_cast<__nv_bfloat16*>(dq);
   a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   a.ld_g = ld_g;
@@ -731,15 +839,15 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.causal = causal;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
     if (e != cudaSuccess) return avb::cuda_status(e, "attn_bwd smem attr");
     attr = true;
   }
   dim3 grid((N + BT - 1) / BT, H, B);
-  attn_bwd_kernel<<<grid, 32 * (kBwdCompute + 2), B_SMEM, st>>>(mq, mk, mv, mdo, mdq, a);
-  if ((s = avb::launch_status("avb_attn_bwd"))) return s;
-  const int64_t threads = (int64_t)B * N * H * 8;
-  attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-      dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N);
-  return avb::launch_status("attn_dq_convert");
+  attn_bwd_dkdv_kernel<<<grid, 32 * (kBwdCompute + 2), D_SMEM, st>>>(mq, mk, mv, mdo, a);
+  if ((s = avb::launch_status("avb_attn_bwd(dkdv)"))) return s;
+  attn_bwd_dq_kernel<<<grid, 32 * (kBwdCompute + 2), Q_SMEM, st>>>(mq, mk, mv, mdo, a);
+  return avb::launch_status("avb_attn_bwd(dq)");
 }
