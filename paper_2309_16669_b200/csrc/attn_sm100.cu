@@ -308,21 +308,32 @@ struct BwdArgs {
   int causal;
 };
 
-constexpr int kBwdCompute = 8;   // compute warps (2 per TMEM lane quadrant, split by column half)
-constexpr int KV_STAGES = 3;
-// dKdV smem: K, V (resident), KV_STAGES x (Q 16K + dO 16K), KV_STAGES x (lse 512 + delta 512), barriers
-constexpr int D_SK = 0, D_SV = 16384, D_SQD = 32768;
-constexpr int D_SLD = D_SQD + KV_STAGES * 32768;
-constexpr int D_BAR = D_SLD + KV_STAGES * 1024;
+constexpr int kBwdCompute = 8;   // compute warps: two groups of 4 (one warp per TMEM lane quadrant)
+constexpr int SB = 64;           // streamed tile (queries in dK/dV, keys in dQ)
+constexpr int BW_STAGES = 4;
+// dKdV smem: K_A, K_B, V_A, V_B (resident 4 x 16 KB), BW_STAGES x (Q 8 KB + dO 8 KB), BW_STAGES x (lse 256 + delta 256)
+constexpr int D_SK = 0, D_SV = 32768, D_SQD = 65536;
+constexpr int D_SLD = D_SQD + BW_STAGES * 16384;
+constexpr int D_BAR = D_SLD + BW_STAGES * 512;
 constexpr int D_SMEM = D_BAR + 256;
-// dQ smem: Q, dO (resident), KV_STAGES x (K 16K + V 16K), barriers
-constexpr int Q_SQ = 0, Q_SDO = 16384, Q_SKV = 32768;
-constexpr int Q_BAR = Q_SKV + KV_STAGES * 32768;
+// dQ smem: Q_A, Q_B, dO_A, dO_B (resident), BW_STAGES x (K 8 KB + V 8 KB)
+constexpr int Q_SQ = 0, Q_SDO = 32768, Q_SKV = 65536;
+constexpr int Q_BAR = Q_SKV + BW_STAGES * 16384;
 constexpr int Q_SMEM = Q_BAR + 256;
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) { return pack_bf16x2(a, b); }
 
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // --------------------------------------------------------------------------------- dK / dV
+// CTA = two 128-key tiles (groups A, B) of one (head, clip); loop over 64-query tiles i.
+// TMEM per group g (256 cols): S^T/P^T [256g, +64)  dP^T/dS^T [256g+64, +64)  dV [256g+128, +64)  dK [256g+192, +64)
+// (P^T / dS^T overwrite the S^T / dP^T columns the same thread has already read.)
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -335,22 +346,21 @@ __global__ void __launch_bounds__(320, 1)
   float* sLD = reinterpret_cast<float*>(smem + D_SLD);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + D_BAR);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qd_full = bars + 1;                  // [KV_STAGES]
-  uint64_t* qd_empty = bars + 1 + KV_STAGES;     // [KV_STAGES]
-  uint64_t* s_full = bars + 1 + 2 * KV_STAGES;
-  uint64_t* ds_ready = s_full + 1;
-  uint64_t* pd_free = s_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
+  uint64_t* qd_full = bars + 1;                   // [BW_STAGES]
+  uint64_t* qd_empty = bars + 1 + BW_STAGES;      // [BW_STAGES]
+  uint64_t* gb = bars + 1 + 2 * BW_STAGES;        // per group: s_full, ds_ready
+  uint64_t* fin = gb + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int kv0 = kt * BT;
-  const int nq_all = (a.N + BT - 1) / BT;
-  const int i0 = a.causal ? kt : 0;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int kv0 = blockIdx.x * 2 * BT;
+  const bool hasB = kv0 + BT < a.N;
+  const int ng = hasB ? 2 : 1;
+  const int nq_all = (a.N + SB - 1) / SB;
+  const int i0 = a.causal ? kv0 / SB : 0;          // first query tile that sees key tile A
   const int nq = nq_all - i0;
   constexpr int kTMA = kBwdCompute, kMMA = kBwdCompute + 1;
-  // TMEM: S^T [0,128) dP^T [128,256) P^T bf16 [256,320) dS^T bf16 [320,384) dV [384,448) dK [448,512)
-  constexpr uint32_t T_ST = 0, T_DPT = 128, T_PT = 256, T_DST = 320, T_DV = 384, T_DK = 448;
 
   if (warp == kTMA && lane == 0) {
     tc::tma_prefetch(&tmQ);
@@ -358,13 +368,15 @@ __global__ void __launch_bounds__(320, 1)
     tc::tma_prefetch(&tmV);
     tc::tma_prefetch(&tmdO);
     tc::mbar_init(kv_full, 1);
-    for (int s = 0; s < KV_STAGES; ++s) {
-      tc::mbar_init(&qd_full[s], 1);
-      tc::mbar_init(&qd_empty[s], 1);
+    for (int st = 0; st < BW_STAGES; ++st) {
+      tc::mbar_init(&qd_full[st], 1);
+      tc::mbar_init(&qd_empty[st], 1);
     }
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(ds_ready, kBwdCompute);
-    tc::mbar_init(pd_free, 1);
+    for (int g = 0; g < 2; ++g) {
+      tc::mbar_init(gb + 2 * g, 1);
+      tc::mbar_init(gb + 2 * g + 1, 4);
+    }
+    tc::mbar_init(fin, 1);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -376,138 +388,142 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == kTMA) {
     if (lane == 0) {
-      tc::mbar_arrive_expect_tx(kv_full, 32768);
-      tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
-      tc::tma_load_3d(sV, &tmV, kv_full, h * HD, kv0, b);
+      tc::mbar_arrive_expect_tx(kv_full, 32768 * ng);
+      for (int g = 0; g < ng; ++g) {
+        tc::tma_load_3d(sK + g * 16384, &tmK, kv_full, h * HD, kv0 + g * BT, b);
+        tc::tma_load_3d(sV + g * 16384, &tmV, kv_full, h * HD, kv0 + g * BT, b);
+      }
       for (int ii = 0; ii < nq; ++ii) {
-        const int i = i0 + ii, st = ii % KV_STAGES;
-        tc::mbar_wait(&qd_empty[st], ((ii / KV_STAGES) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
-        tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
-        tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                         smem_u32(sLD + st * 256)),
-                     "l"(a.lse + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                         smem_u32(sLD + st * 256 + 128)),
-                     "l"(a.delta + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
-                     : "memory");
+        const int i = i0 + ii, st = ii % BW_STAGES;
+        tc::mbar_wait(&qd_empty[st], ((ii / BW_STAGES) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&qd_full[st], 16384 + 512);
+        tc::tma_load_3d(sQD + st * 16384, &tmQ, &qd_full[st], h * HD, i * SB, b);
+        tc::tma_load_3d(sQD + st * 16384 + 8192, &tmdO, &qd_full[st], h * HD, i * SB, b);
+        bulk_copy(sLD + st * 128, a.lse + bh * a.Npad + i * SB, 256, &qd_full[st]);
+        bulk_copy(sLD + st * 128 + 64, a.delta + bh * a.Npad + i * SB, 256, &qd_full[st]);
       }
     }
   } else if (warp == kMMA) {
     if (lane == 0) {
-      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
-      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: A from TMEM, B (dO / Q) MN-major
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto issue_s = [&](int ii) {
-        const int st = ii % KV_STAGES;
-        tc::mbar_wait(&qd_full[st], (ii / KV_STAGES) & 1);
-        tc::tc_fence_after();
-        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, SB, 0, 0);  // S^T, dP^T: M=128 keys, N=64 queries
+      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);   // dV, dK: A from TMEM, B (dO / Q) MN-major
+      auto issue_s = [&](int g, int ii) {
+        const int st = ii % BW_STAGES;
+        const uint32_t aQ = smem_u32(sQD + st * 16384), aDO = aQ + 8192;
+        const uint32_t aK = smem_u32(sK + g * 16384), aV = smem_u32(sV + g * 16384);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + T_ST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
-                          idSS, kk > 0);
+          tc::umma_f16_ss(tmem + 256 * g, tc::sdesc_sw128(aK + kk * 32, 16, 1024),
+                          tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + T_DPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024),
+          tc::umma_f16_ss(tmem + 256 * g + 64, tc::sdesc_sw128(aV + kk * 32, 16, 1024),
                           tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
-        tc::umma_commit(s_full);
+        tc::umma_commit(gb + 2 * g);
       };
       tc::mbar_wait(kv_full, 0);
-      issue_s(0);
+      tc::mbar_wait(&qd_full[0], 0);
+      tc::tc_fence_after();
+      for (int g = 0; g < ng; ++g) issue_s(g, 0);
       for (int ii = 0; ii < nq; ++ii) {
-        tc::mbar_wait(ds_ready, ii & 1);     // P^T/dS^T(ii) in TMEM, S^T/dP^T consumed
-        tc::tc_fence_after();
-        if (ii + 1 < nq) issue_s(ii + 1);
-        const int st = ii % KV_STAGES;
-        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+        const bool more = ii + 1 < nq;
+        if (more) tc::mbar_wait(&qd_full[(ii + 1) % BW_STAGES], ((ii + 1) / BW_STAGES) & 1);
+        const int st = ii % BW_STAGES;
+        const uint32_t aQ = smem_u32(sQD + st * 16384), aDO = aQ + 8192;
+        for (int g = 0; g < ng; ++g) {
+          tc::mbar_wait(gb + 2 * g + 1, ii & 1);    // P^T/dS^T_g(ii) in TMEM
+          tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts(tmem + T_DV, tmem + T_PT + kk * 8, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG,
-                          (ii > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < SB / 16; ++kk)
+            tc::umma_f16_ts(tmem + 256 * g + 128, tmem + 256 * g + kk * 8, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024),
+                            idG, (ii > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts(tmem + T_DK, tmem + T_DST + kk * 8, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG,
-                          (ii > 0 || kk > 0) ? 1u : 0u);
-        tc::umma_commit(pd_free);
+          for (int kk = 0; kk < SB / 16; ++kk)
+            tc::umma_f16_ts(tmem + 256 * g + 192, tmem + 256 * g + 64 + kk * 8,
+                            tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, (ii > 0 || kk > 0) ? 1u : 0u);
+          if (more) issue_s(g, ii + 1);   // in-order tensor pipe: overwrites S^T/P^T after dV/dK read them
+        }
         tc::umma_commit(&qd_empty[st]);
       }
+      tc::umma_commit(fin);
     }
   } else {
-    // compute warps: thread = key row (quadrant), column half of the 128 query columns
-    const int quad = warp & 3, half = warp >> 2;
-    const int row = quad * 32 + lane;
-    const int kvi = kv0 + row;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    for (int ii = 0; ii < nq; ++ii) {
-      const int i = i0 + ii, st = ii % KV_STAGES;
-      const int q0 = i * BT;
-      tc::mbar_wait(s_full, ii & 1);
-      tc::mbar_wait(&qd_full[st], (ii / KV_STAGES) & 1);  // lse/delta landed
-      if (ii > 0) tc::mbar_wait(pd_free, (ii - 1) & 1);    // dV/dK(ii-1) done reading P^T/dS^T
-      tc::tc_fence_after();
-      const float* sl = sLD + st * 256;
-      const float* sd = sl + 128;
+    // compute groups: g = warp >> 2 (key tile), thread = key row
+    const int g = warp >> 2, quad = warp & 3;
+    if (g < ng) {
+      const int row = quad * 32 + lane;
+      const int kvi = kv0 + g * BT + row;
+      const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      const uint32_t tS = tmem + 256 * g + lane_off, tD = tS + 64;
+      for (int ii = 0; ii < nq; ++ii) {
+        const int i = i0 + ii, st = ii % BW_STAGES;
+        const int q0 = i * SB;
+        tc::mbar_wait(gb + 2 * g, ii & 1);
+        tc::mbar_wait(&qd_full[st], (ii / BW_STAGES) & 1);  // lse/delta landed
+        tc::tc_fence_after();
+        const float* sl = sLD + st * 128;
+        const float* sd = sl + 64;
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;
-        uint32_t rs[32], rp[32];
-        tc::tmem_ld_32x32b_x32(tmem + T_ST + lane_off + c * 32, rs);
-        tc::tmem_ld_32x32b_x32(tmem + T_DPT + lane_off + c * 32, rp);
-        tc::tmem_ld_wait();
-        uint32_t pk[16], dk[16];
+        for (int c = 0; c < 2; ++c) {
+          // chunk c: its P^T / dS^T land in columns [16c, 16c+16) of chunk 0, already consumed
+          uint32_t rs[32], rp[32];
+          tc::tmem_ld_32x32b_x32(tS + c * 32, rs);
+          tc::tmem_ld_32x32b_x32(tD + c * 32, rp);
+          tc::tmem_ld_wait();
+          uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 l0 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8);
-          const float4 l1 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8 + 4);
-          const float4 d0 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8);
-          const float4 d1 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8 + 4);
-          const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-          const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-          float p[8], ds[8];
+          for (int u = 0; u < 4; ++u) {
+            const float4 l0 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8);
+            const float4 l1 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8 + 4);
+            const float4 d0 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8);
+            const float4 d1 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8 + 4);
+            const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+            const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+            float p[8], ds[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int qi = q0 + c * 32 + u * 8 + e;
-            const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-            const float pe = ok ? ex2(fmaf(__uint_as_float(rs[u * 8 + e]), a.scale_log2, -lv[e] * kLog2e)) : 0.f;
-            p[e] = pe;
-            ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[u * 8 + e]) - dv[e]) : 0.f;
+            for (int e = 0; e < 8; ++e) {
+              const int qi = q0 + c * 32 + u * 8 + e;
+              const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+              const float pe = ok ? ex2(fmaf(__uint_as_float(rs[u * 8 + e]), a.scale_log2, -lv[e] * kLog2e)) : 0.f;
+              p[e] = pe;
+              ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[u * 8 + e]) - dv[e]) : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              pk[u * 4 + e] = pack2(p[2 * e], p[2 * e + 1]);
+              dk[u * 4 + e] = pack2(ds[2 * e], ds[2 * e + 1]);
+            }
           }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            pk[u * 4 + e] = pack2(p[2 * e], p[2 * e + 1]);
-            dk[u * 4 + e] = pack2(ds[2 * e], ds[2 * e + 1]);
-          }
+          tc::tmem_st_32x32b_x16(tS + c * 16, pk);   // P^T over consumed S^T columns
+          tc::tmem_st_32x32b_x16(tD + c * 16, dk);   // dS^T over consumed dP^T columns
         }
-        tc::tmem_st_32x32b_x16(tmem + T_PT + lane_off + c * 16, pk);
-        tc::tmem_st_32x32b_x16(tmem + T_DST + lane_off + c * 16, dk);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(gb + 2 * g + 1);
       }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ds_ready);
-    }
-    // dK / dV out (thread = key row, its column half)
-    tc::mbar_wait(pd_free, (nq - 1) & 1);
-    tc::tc_fence_after();
+      tc::mbar_wait(fin, 0);
+      tc::tc_fence_after();
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tsrc = tmem + (which ? T_DK : T_DV);
-      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + half * 32;
-      uint32_t r[32];
-      tc::tmem_ld_32x32b_x32(tsrc + lane_off + half * 32, r);
-      tc::tmem_ld_wait();
-      if (kvi < a.N) {
+      for (int which = 0; which < 2; ++which) {
+        const uint32_t tsrc = tmem + 256 * g + 128 + (which ? 64 : 0) + lane_off;
+        __nv_bfloat16* gp = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 v;
-          v.x = pack2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
-          v.y = pack2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
-          v.z = pack2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
-          v.w = pack2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
-          reinterpret_cast<uint4*>(g)[u] = v;
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(tsrc + c * 32, r);
+          tc::tmem_ld_wait();
+          if (kvi < a.N) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              uint4 v;
+              v.x = pack2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+              v.y = pack2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+              v.z = pack2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+              v.w = pack2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+              reinterpret_cast<uint4*>(gp + c * 32)[u] = v;
+            }
+          }
         }
       }
     }
@@ -521,6 +537,8 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // --------------------------------------------------------------------------------- dQ
+// CTA = two 128-query tiles (groups A, B) of one (head, clip); loop over 64-key tiles j.
+// TMEM per group g (224 cols at 256g): S [0,64) dP [64,128) dS bf16 [128,160) dQ [160,224)
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -532,21 +550,20 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sKV = smem + Q_SKV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Q_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;                  // [KV_STAGES]
-  uint64_t* kv_empty = bars + 1 + KV_STAGES;     // [KV_STAGES]
-  uint64_t* s_full = bars + 1 + 2 * KV_STAGES;
-  uint64_t* ds_ready = s_full + 1;
-  uint64_t* ds_free = s_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
+  uint64_t* kv_full = bars + 1;                   // [BW_STAGES]
+  uint64_t* kv_empty = bars + 1 + BW_STAGES;      // [BW_STAGES]
+  uint64_t* gb = bars + 1 + 2 * BW_STAGES;        // per group: s_full, ds_ready
+  uint64_t* fin = gb + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qt * BT;
-  const int nkv_all = (a.N + BT - 1) / BT;
-  const int nkv = a.causal ? min(nkv_all, qt + 1) : nkv_all;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * 2 * BT;
+  const bool hasB = q0 + BT < a.N;
+  const int ng = hasB ? 2 : 1;
+  const int nkv_all = (a.N + SB - 1) / SB;
+  const int nkv = a.causal ? min(nkv_all, (q0 + ng * BT - 1) / SB + 1) : nkv_all;
   constexpr int kTMA = kBwdCompute, kMMA = kBwdCompute + 1;
-  // TMEM: S [0,128) dP [128,256) dS bf16 [256,320) dQ [320,384)
-  constexpr uint32_t T_S = 0, T_DP = 128, T_DS = 256, T_DQ = 320;
 
   if (warp == kTMA && lane == 0) {
     tc::tma_prefetch(&tmQ);
@@ -554,13 +571,15 @@ __global__ void __launch_bounds__(320, 1)
     tc::tma_prefetch(&tmV);
     tc::tma_prefetch(&tmdO);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < KV_STAGES; ++s) {
-      tc::mbar_init(&kv_full[s], 1);
-      tc::mbar_init(&kv_empty[s], 1);
+    for (int st = 0; st < BW_STAGES; ++st) {
+      tc::mbar_init(&kv_full[st], 1);
+      tc::mbar_init(&kv_empty[st], 1);
     }
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(ds_ready, kBwdCompute);
-    tc::mbar_init(ds_free, 1);
+    for (int g = 0; g < 2; ++g) {
+      tc::mbar_init(gb + 2 * g, 1);
+      tc::mbar_init(gb + 2 * g + 1, 4);
+    }
+    tc::mbar_init(fin, 1);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -571,114 +590,129 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == kTMA) {
     if (lane == 0) {
-      tc::mbar_arrive_expect_tx(q_full, 32768);
-      tc::tma_load_3d(sQ, &tmQ, q_full, h * HD, q0, b);
-      tc::tma_load_3d(sDO, &tmdO, q_full, h * HD, q0, b);
+      tc::mbar_arrive_expect_tx(q_full, 32768 * ng);
+      for (int g = 0; g < ng; ++g) {
+        tc::tma_load_3d(sQ + g * 16384, &tmQ, q_full, h * HD, q0 + g * BT, b);
+        tc::tma_load_3d(sDO + g * 16384, &tmdO, q_full, h * HD, q0 + g * BT, b);
+      }
       for (int j = 0; j < nkv; ++j) {
-        const int st = j % KV_STAGES;
-        tc::mbar_wait(&kv_empty[st], ((j / KV_STAGES) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&kv_full[st], 32768);
-        tc::tma_load_3d(sKV + st * 32768, &tmK, &kv_full[st], h * HD, j * BT, b);
-        tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
+        const int st = j % BW_STAGES;
+        tc::mbar_wait(&kv_empty[st], ((j / BW_STAGES) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&kv_full[st], 16384);
+        tc::tma_load_3d(sKV + st * 16384, &tmK, &kv_full[st], h * HD, j * SB, b);
+        tc::tma_load_3d(sKV + st * 16384 + 8192, &tmV, &kv_full[st], h * HD, j * SB, b);
       }
     }
   } else if (warp == kMMA) {
     if (lane == 0) {
-      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
+      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, SB, 0, 0);   // S, dP: M=128 queries, N=64 keys
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 0, 1);    // dQ: A = dS from TMEM, B = K MN-major
-      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO);
-      auto issue_s = [&](int j) {
-        const int st = j % KV_STAGES;
-        tc::mbar_wait(&kv_full[st], (j / KV_STAGES) & 1);
-        tc::tc_fence_after();
-        const uint32_t aK = smem_u32(sKV + st * 32768), aV = aK + 16384;
+      auto issue_s = [&](int g, int j) {
+        const int st = j % BW_STAGES;
+        const uint32_t aK = smem_u32(sKV + st * 16384), aV = aK + 8192;
+        const uint32_t aQ = smem_u32(sQ + g * 16384), aDO = smem_u32(sDO + g * 16384);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + T_S, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024),
-                          idSS, kk > 0);
+          tc::umma_f16_ss(tmem + 256 * g, tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
+                          tc::sdesc_sw128(aK + kk * 32, 16, 1024), idSS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + T_DP, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), tc::sdesc_sw128(aV + kk * 32, 16, 1024),
-                          idSS, kk > 0);
-        tc::umma_commit(s_full);
+          tc::umma_f16_ss(tmem + 256 * g + 64, tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
+                          tc::sdesc_sw128(aV + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_commit(gb + 2 * g);
       };
       tc::mbar_wait(q_full, 0);
-      issue_s(0);
+      tc::mbar_wait(&kv_full[0], 0);
+      tc::tc_fence_after();
+      for (int g = 0; g < ng; ++g) issue_s(g, 0);
       for (int j = 0; j < nkv; ++j) {
-        tc::mbar_wait(ds_ready, j & 1);     // dS(j) in TMEM, S/dP(j) consumed
-        tc::tc_fence_after();
-        if (j + 1 < nkv) issue_s(j + 1);
-        const int st = j % KV_STAGES;
-        const uint32_t aK = smem_u32(sKV + st * 32768);
+        const bool more = j + 1 < nkv;
+        if (more) tc::mbar_wait(&kv_full[(j + 1) % BW_STAGES], ((j + 1) / BW_STAGES) & 1);
+        const int st = j % BW_STAGES;
+        const uint32_t aK = smem_u32(sKV + st * 16384);
+        for (int g = 0; g < ng; ++g) {
+          tc::mbar_wait(gb + 2 * g + 1, j & 1);     // dS_g(j) in TMEM, S/dP_g(j) consumed
+          tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts(tmem + T_DQ, tmem + T_DS + kk * 8, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ,
-                          (j > 0 || kk > 0) ? 1u : 0u);
-        tc::umma_commit(ds_free);
+          for (int kk = 0; kk < SB / 16; ++kk)
+            tc::umma_f16_ts(tmem + 256 * g + 160, tmem + 256 * g + 128 + kk * 8,
+                            tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, (j > 0 || kk > 0) ? 1u : 0u);
+          if (more) issue_s(g, j + 1);
+        }
         tc::umma_commit(&kv_empty[st]);
       }
+      tc::umma_commit(fin);
     }
   } else {
-    // compute warps: thread = query row (quadrant), column half of the 128 key columns
-    const int quad = warp & 3, half = warp >> 2;
-    const int row = quad * 32 + lane;
-    const int qi = q0 + row;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const int64_t bh = (int64_t)b * a.H + h;
-    const float lse2 = (qi < a.N) ? a.lse[bh * a.Npad + qi] * kLog2e : 0.f;
-    const float dlt = (qi < a.N) ? a.delta[bh * a.Npad + qi] : 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int kv0 = j * BT;
-      tc::mbar_wait(s_full, j & 1);
-      if (j > 0) tc::mbar_wait(ds_free, (j - 1) & 1);   // dQ(j-1) MMA done reading dS
-      tc::tc_fence_after();
-      int lim = a.N - kv0;
-      if (a.causal) lim = min(lim, qi - kv0 + 1);
-      if (qi >= a.N) lim = 0;
+    // compute groups: g = warp >> 2 (query tile), thread = query row (its LSE / delta in registers)
+    const int g = warp >> 2, quad = warp & 3;
+    if (g < ng) {
+      const int row = quad * 32 + lane;
+      const int qi = q0 + g * BT + row;
+      const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      const uint32_t tS = tmem + 256 * g + lane_off, tD = tS + 64, tDS = tS + 128;
+      const int64_t bh = (int64_t)b * a.H + h;
+      const float lse2 = (qi < a.N) ? a.lse[bh * a.Npad + qi] * kLog2e : 0.f;
+      const float dlt = (qi < a.N) ? a.delta[bh * a.Npad + qi] : 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        const int kv0 = j * SB;
+        tc::mbar_wait(gb + 2 * g, j & 1);   // S/dP(j); also implies dQ(j-1) has consumed dS(j-1)
+        tc::tc_fence_after();
+        int lim = a.N - kv0;
+        if (a.causal) lim = min(lim, qi - kv0 + 1);
+        if (qi >= a.N) lim = 0;
+        uint32_t rs[2][32], rp[2][32];
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;
-        uint32_t rs[32], rp[32];
-        tc::tmem_ld_32x32b_x32(tmem + T_S + lane_off + c * 32, rs);
-        tc::tmem_ld_32x32b_x32(tmem + T_DP + lane_off + c * 32, rp);
-        tc::tmem_ld_wait();
-        uint32_t dk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int col = c * 32 + e;
-          float d0 = 0.f, d1 = 0.f;
-          if (col < lim) {
-            const float p0 = ex2(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2));
-            d0 = a.scale * p0 * (__uint_as_float(rp[e]) - dlt);
-          }
-          if (col + 1 < lim) {
-            const float p1 = ex2(fmaf(__uint_as_float(rs[e + 1]), a.scale_log2, -lse2));
-            d1 = a.scale * p1 * (__uint_as_float(rp[e + 1]) - dlt);
-          }
-          dk[e >> 1] = pack2(d0, d1);
+        for (int c = 0; c < 2; ++c) {
+          tc::tmem_ld_32x32b_x32(tS + c * 32, rs[c]);
+          tc::tmem_ld_32x32b_x32(tD + c * 32, rp[c]);
         }
-        tc::tmem_st_32x32b_x16(tmem + T_DS + lane_off + c * 16, dk);
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ds_ready);
-    }
-    tc::mbar_wait(ds_free, (nkv - 1) & 1);
-    tc::tc_fence_after();
-    uint32_t r[32];
-    tc::tmem_ld_32x32b_x32(tmem + T_DQ + lane_off + half * 32, r);
-    tc::tmem_ld_wait();
-    if (qi < a.N) {
-      __nv_bfloat16* g = a.dq + (int64_t)b * a.sb_g + (int64_t)qi * a.ld_g + h * HD + half * 32;
+        tc::tmem_ld_wait();
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint4 v;
-        v.x = pack2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
-        v.y = pack2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
-        v.z = pack2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
-        v.w = pack2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
-        reinterpret_cast<uint4*>(g)[u] = v;
+        for (int c = 0; c < 2; ++c) {
+          uint32_t dk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int col = c * 32 + e;
+            float d0 = 0.f, d1 = 0.f;
+            if (col < lim) {
+              const float p0 = ex2(fmaf(__uint_as_float(rs[c][e]), a.scale_log2, -lse2));
+              d0 = a.scale * p0 * (__uint_as_float(rp[c][e]) - dlt);
+            }
+            if (col + 1 < lim) {
+              const float p1 = ex2(fmaf(__uint_as_float(rs[c][e + 1]), a.scale_log2, -lse2));
+              d1 = a.scale * p1 * (__uint_as_float(rp[c][e + 1]) - dlt);
+            }
+            dk[e >> 1] = pack2(d0, d1);
+          }
+          tc::tmem_st_32x32b_x16(tDS + c * 16, dk);
+        }
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(gb + 2 * g + 1);
+      }
+      tc::mbar_wait(fin, 0);
+      tc::tc_fence_after();
+      if (true) {
+        __nv_bfloat16* gp = a.dq + (int64_t)b * a.sb_g + (int64_t)qi * a.ld_g + h * HD;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(tS + 160 + c * 32, r);
+          tc::tmem_ld_wait();
+          if (qi < a.N) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              uint4 v;
+              v.x = pack2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
+              v.y = pack2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
+              v.z = pack2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
+              v.w = pack2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+              reinterpret_cast<uint4*>(gp + c * 32)[u] = v;
+            }
+          }
+        }
       }
     }
   }
@@ -746,8 +780,9 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
   *reinterpret_cast<uint4*>(dq + b * sb + (int64_t)n * ld + h * HD + sub * 8) = v;
 }
 
-int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, int64_t sb) {
-  return avb::make_tmap_3d_bf16(m, p, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)ld, (uint64_t)sb, 64, 128, 1);
+int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, int64_t sb, uint32_t rows = 128) {
+  return avb::make_tmap_3d_bf16(m, p, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)ld, (uint64_t)sb, 64, rows,
+                                1);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -816,12 +851,17 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     int s = avb::launch_status("attn_bwd_pre");
     if (s) return s;
   }
-  CUtensorMap mq, mk, mv, mdo;
+  // resident tiles use 128-row boxes, streamed tiles 64-row boxes
+  CUtensorMap mq128, mk128, mv128, mdo128, mq64, mk64, mv64, mdo64;
   int s;
-  if ((s = make_maps(&mq, q, B, H, N, ld, sb))) return s;
-  if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
-  if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
-  if ((s = make_maps(&mdo, dout, B, H, N, ld_o, sb_o))) return s;
+  if ((s = make_maps(&mq128, q, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mk128, k, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mv128, v, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mdo128, dout, B, H, N, ld_o, sb_o))) return s;
+  if ((s = make_maps(&mq64, q, B, H, N, ld, sb, 64))) return s;
+  if ((s = make_maps(&mk64, k, B, H, N, ld, sb, 64))) return s;
+  if ((s = make_maps(&mv64, v, B, H, N, ld, sb, 64))) return s;
+  if ((s = make_maps(&mdo64, dout, B, H, N, ld_o, sb_o, 64))) return s;
   BwdArgs a;
   a.B = B;
   a.H = H;
@@ -845,9 +885,9 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     if (e != cudaSuccess) return avb::cuda_status(e, "attn_bwd smem attr");
     attr = true;
   }
-  dim3 grid((N + BT - 1) / BT, H, B);
-  attn_bwd_dkdv_kernel<<<grid, 32 * (kBwdCompute + 2), D_SMEM, st>>>(mq, mk, mv, mdo, a);
+  dim3 grid((N + 2 * BT - 1) / (2 * BT), H, B);
+  attn_bwd_dkdv_kernel<<<grid, 32 * (kBwdCompute + 2), D_SMEM, st>>>(mq64, mk128, mv128, mdo64, a);
   if ((s = avb::launch_status("avb_attn_bwd(dkdv)"))) return s;
-  attn_bwd_dq_kernel<<<grid, 32 * (kBwdCompute + 2), Q_SMEM, st>>>(mq, mk, mv, mdo, a);
+  attn_bwd_dq_kernel<<<grid, 32 * (kBwdCompute + 2), Q_SMEM, st>>>(mq128, mk64, mv64, mdo128, a);
   return avb::launch_status("avb_attn_bwd(dq)");
 }
