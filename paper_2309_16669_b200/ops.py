@@ -116,9 +116,10 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
         dq, dk, dv = g[:, :, 0], g[:, :, 1], g[:, :, 2]
     _, _, ld_g, sb_g = _bnhd(dq, "dq", H)
     delta = torch.empty((B * H, npad(N)), dtype=torch.float32, device=q.device)
+    dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device)
     scale = 64 ** -0.5 if scale is None else float(scale)
     st = _lib.load().avb_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(),
-                                  ld_o, sb_o, lse.data_ptr(), delta.data_ptr(), None, dq.data_ptr(),
+                                  ld_o, sb_o, lse.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dq.data_ptr(),
                                   dk.data_ptr(), dv.data_ptr(), ld_g, sb_g, B, H, N, 64, scale, int(causal),
                                   _lib.stream_ptr())
     _lib.check(st, "attn_bwd")
