@@ -139,10 +139,11 @@ int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_
 /* K6: LayerNorm over rows of D (<= 1024, multiple of 8) bf16 elements, fp32 gamma/beta/stats. */
 int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma, const float* beta, void* y,
                       int64_t ldy, float* mean, float* rstd, int M, int D, float eps, void* stream);
-/* dx (=|+=) LN'(dy); dgamma/dbeta (nullable) += column reductions. */
+/* dx (=|+=) LN'(dy); dgamma/dbeta (nullable) += column reductions; dx_colsum (nullable) += column
+ * sums of the resulting dx (the bias gradient of the linear layer whose output is this residual). */
 int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, int64_t ldx, const float* gamma,
                       const float* mean, const float* rstd, void* dx, int64_t lddx, float* dgamma,
-                      float* dbeta, int M, int D, int accumulate, void* stream);
+                      float* dbeta, float* dx_colsum, int M, int D, int accumulate, void* stream);
 
 /* out[n] += sum_m X[m,n] (bias gradients); X bf16 [M, ldx]. */
 int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void* stream);

@@ -34,7 +34,8 @@ EXPORTS: dict[str, tuple] = {
     "avb_rrc_normalize_tubelet": (_i32, [_vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                          _i32, _i32, _f32p, _f32p, _i32, _i32, _i32, _i32, _vp, _vp]),
     "avb_layernorm_fwd": (_i32, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, C.c_float, _vp]),
-    "avb_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _i32, _vp]),
+    "avb_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _i32,
+                                 _vp]),
     "avb_colsum_accum": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "avb_tokens_fwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp]),
     "avb_tokens_bwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp]),

@@ -100,17 +100,17 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
                                                      const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, __nv_bfloat16* dx, int64_t lddx,
-                                                     float* __restrict__ dgamma, float* __restrict__ dbeta, int M, int D,
-                                                     int accumulate) {
-  extern __shared__ float red[];  // [2][D]
+                                                     float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                     float* __restrict__ dsum, int M, int D, int accumulate) {
+  extern __shared__ float red[];  // [3][D]: dgamma, dbeta, column sums of the output dx
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) red[i] = 0.f;
+  for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) red[i] = 0.f;
   __syncthreads();
-  float dg[NC][8], db[NC][8];
+  float dg[NC][8], db[NC][8], cs[NC][8];
 #pragma unroll
   for (int k = 0; k < NC; ++k)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) dg[k][e] = db[k][e] = 0.f;
+    for (int e = 0; e < 8; ++e) dg[k][e] = db[k][e] = cs[k][e] = 0.f;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < M; row += nwarps) {
     const float mu = mean[row], rs = rstd[row];
@@ -161,7 +161,14 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
         const float xh = (xv[e] - mu) * rs;
         o[e] = rs * (dv[e] * gm[e] - m1 - xh * m2) + pv[e];
       }
-      *reinterpret_cast<uint4*>(dx + row * lddx + c) = pack8(o);
+      const uint4 q = pack8(o);
+      *reinterpret_cast<uint4*>(dx + row * lddx + c) = q;
+      if (dsum) {
+        float ob[8];
+        unpack8(q, ob);   // sum what was stored (bf16), like a separate column-sum pass would
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cs[k][e] += ob[e];
+      }
     }
   }
 #pragma unroll
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
       for (int e = 0; e < 8; ++e) {
         atomicAdd(&red[c + e], dg[k][e]);
         atomicAdd(&red[D + c + e], db[k][e]);
+        if (dsum) atomicAdd(&red[2 * D + c + e], cs[k][e]);
       }
     }
   }
@@ -179,6 +187,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
   for (int i = threadIdx.x; i < D; i += blockDim.x) {
     if (dgamma) atomicAdd(dgamma + i, red[i]);
     if (dbeta) atomicAdd(dbeta + i, red[D + i]);
+    if (dsum) atomicAdd(dsum + i, red[2 * D + i]);
   }
 }
 
@@ -212,16 +221,16 @@ extern "C" int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma,
 
 extern "C" int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, int64_t ldx, const float* gamma,
                                  const float* mean, const float* rstd, void* dx, int64_t lddx, float* dgamma,
-                                 float* dbeta, int M, int D, int accumulate, void* stream) {
+                                 float* dbeta, float* dx_colsum, int M, int D, int accumulate, void* stream) {
   AVB_CHECK_ARG(M >= 0 && D >= 8 && D <= 1024 && D % 8 == 0, "LayerNorm needs D % 8 == 0, D <= 1024");
   if (M == 0) return AVB_OK;
   AVB_CHECK_ARG(dy && x && gamma && mean && rstd && dx, "null pointer");
   AVB_CHECK_ARG(lddy % 8 == 0 && ldx % 8 == 0 && lddx % 8 == 0, "row strides must be multiples of 8");
   const int blocks = (int)std::min<int64_t>((M + 7) / 8, (int64_t)avb::sm_count() * 2);
   return dispatch_nc(D, [&](auto nc) {
-    ln_bwd_kernel<decltype(nc)::value><<<blocks, 256, 2 * D * sizeof(float), avb::as_stream(stream)>>>(
+    ln_bwd_kernel<decltype(nc)::value><<<blocks, 256, 3 * D * sizeof(float), avb::as_stream(stream)>>>(
         reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
-        mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, M, D, accumulate);
+        mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, dx_colsum, M, D, accumulate);
     return avb::launch_status("avb_layernorm_bwd");
   });
 }

@@ -139,12 +139,12 @@ def layernorm_fwd(x, gamma, beta, eps=1e-5, out=None, mean=None, rstd=None):
     return out, mean, rstd
 
 
-def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma=None, dbeta=None, accumulate=False):
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma=None, dbeta=None, accumulate=False, dx_colsum=None):
     M, D = x.shape
     st = _lib.load().avb_layernorm_bwd(dy.data_ptr(), _rowmajor(dy, "dy"), x.data_ptr(), _rowmajor(x, "x"),
                                        gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
-                                       _rowmajor(dx, "dx"), _ptr(dgamma), _ptr(dbeta), M, D, int(accumulate),
-                                       _lib.stream_ptr())
+                                       _rowmajor(dx, "dx"), _ptr(dgamma), _ptr(dbeta), _ptr(dx_colsum), M, D,
+                                       int(accumulate), _lib.stream_ptr())
     _lib.check(st, "layernorm_bwd")
     return dx
 

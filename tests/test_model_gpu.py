@@ -92,8 +92,10 @@ def test_layernorm_and_colsum():
     dx0 = dx.float().clone()
     dg = torch.zeros(D, device="cuda")
     db = torch.zeros(D, device="cuda")
-    ops.layernorm_bwd(dy, x, gam, mu, rs, dx, dg, db, accumulate=True)
+    csum = torch.zeros(D, device="cuda")
+    ops.layernorm_bwd(dy, x, gam, mu, rs, dx, dg, db, accumulate=True, dx_colsum=csum)
     assert rel(dx.float() - dx0, xf.grad) < 2e-2
+    assert rel(csum, dx.float().sum(0)) < 1e-4
     assert rel(dg, gf.grad) < 1e-3 and rel(db, bf.grad) < 1e-3
     cs = torch.zeros(D, device="cuda")
     ops.colsum_accum(dy, cs)
