@@ -26,14 +26,31 @@ __device__ __forceinline__ void st8f(__nv_bfloat16* p, const float (&f)[8]) {
   *reinterpret_cast<uint4*>(p) = q;
 }
 
-// out[n] += sum_m X[m, n]; block (64, 4): 64 column-octets x 4 row lanes
+// out[n] += sum_m X[m, n]; block (64, 4): 64 column-octets x 4 row lanes, 4 rows in flight per thread
 __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t ldx, int M, int N, float* __restrict__ out) {
   __shared__ float red[4][64 * 8 + 4];
   const int c8 = blockIdx.x * 64 + threadIdx.x;
   const int col = c8 * 8;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (col < N) {
-    for (int64_t r = (int64_t)blockIdx.y * 4 + threadIdx.y; r < M; r += (int64_t)gridDim.y * 4) {
+    const int64_t step = (int64_t)gridDim.y * 4;
+    int64_t r = (int64_t)blockIdx.y * 4 + threadIdx.y;
+    for (; r + 3 * step < M; r += 4 * step) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = ld_nc_v4(X + (r + u * step) * ldx + col);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
+        }
+      }
+    }
+    for (; r < M; r += step) {
       float f[8];
       ld8f(X + r * ldx + col, f);
 #pragma unroll
