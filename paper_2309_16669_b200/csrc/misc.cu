@@ -38,7 +38,7 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t ldx, 
     for (; r + 3 * step < M; r += 4 * step) {
       uint4 q[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] = ld_nc_v4(X + (r + u * step) * ldx + col);
+      for (int u = 0; u < 4; ++u) q[u] = *reinterpret_cast<const uint4*>(X + (r + u * step) * ldx + col);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
