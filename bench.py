@@ -2,7 +2,7 @@
 """Benchmark driver (contract: one JSON line from rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload train|augment]
+                    [--workload train|augment|clip]
 
 Workloads
   train    (default) BASELINE.json configs[3]: ViT-B/16 fine-tune, 16x224^2 clips,
@@ -11,6 +11,9 @@ Workloads
            attention) + CE loss + AdamW; data-parallel over N GPUs (NCCL all-reduce).
   augment  BASELINE.json configs[1]: K1 on 64 synthetic uint8 16x320x568 clips ->
            bf16 16x224^2 with the reference sampler's boxes.
+  clip     BASELINE.json configs[2]: ViT-B/16 CLIP dual encoder, 4x224^2 clips + 77-token
+           captions, 128 pairs per GPU, embedding all_gather + fused InfoNCE.
+  train-l14 BASELINE.json configs[4]: ViT-L/14 16x224^2 (N=2049, D=1024, 24 layers), 24 clips/GPU.
 
 `--impl reference` times the CPU restatement (oracle/, the reference has no GPU
 path) on this host's cores, rank 0 only.
@@ -272,7 +275,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="train", choices=["train", "augment"])
+    ap.add_argument("--workload", default="train", choices=["train", "augment", "clip", "train-l14"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -289,10 +292,15 @@ def main():
     rank, world, local = dist_setup(args.gpus)
     if args.workload == "augment":
         line = run_augment(args, rank, world, local)
+    elif args.workload == "clip":
+        from paper_2309_16669_b200 import clip_bench
+
+        line = clip_bench.run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks)
     else:
         from paper_2309_16669_b200 import train_bench
 
-        line = train_bench.run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks)
+        line = train_bench.run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks,
+                               large=(args.workload == "train-l14"))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .vit import CONFIG4_VIT_B_16F, FineTuneModel
+from .vit import CONFIG4_VIT_B_16F, CONFIG5_VIT_L_16F, FineTuneModel
 
 CLIPS_PER_GPU = 64
 NUM_CLASSES = 3806
@@ -61,9 +61,10 @@ def golden_boxes(n: int, offset: int = 0):
     return np.ascontiguousarray(g[idx, :4]), np.ascontiguousarray(g[idx, 4].astype(np.uint8))
 
 
-def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
-    cfg = CONFIG4_VIT_B_16F
-    B = CLIPS_PER_GPU
+def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, large: bool = False):
+    """large=False: configs[3] ViT-B/16 (64 clips/GPU); large=True: configs[4] ViT-L/14 (24 clips/GPU)."""
+    cfg = CONFIG5_VIT_L_16F if large else CONFIG4_VIT_B_16F
+    B = 24 if large else CLIPS_PER_GPU
     dev = torch.device("cuda", torch.cuda.current_device())
     model = FineTuneModel(cfg, NUM_CLASSES, device=dev, seed=0)   # identical init on every rank
     boxes, flips = golden_boxes(B, offset=rank * B)
@@ -204,13 +205,15 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     for n, fn in orig.items():
         setattr(ops, n, fn)
     line = {
-        "metric": "train clips/sec ViT-B/16 16x224^2 (fine-tune step); attn TFLOP/s vs bf16 peak",
+        "metric": ("train clips/sec ViT-L/14 16x224^2 (long-sequence stress)" if large else
+                   "train clips/sec ViT-B/16 16x224^2 (fine-tune step); attn TFLOP/s vs bf16 peak"),
         "value": value, "unit": "clips/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic uint8 16x320x568 clips (device randint) -> K1 RRC boxes from the reference sampler; "
                 "random-init weights; random labels over 3806 classes",
-        "config": {"workload": "configs[3] ViT-B/16 fine-tune 16x224^2, tubelet 2x16x16 (N=1569), FlashAttention "
-                               "fwd/bwd", "clips_per_gpu": B, "global_batch": B * world, "seq_len": N,
+        "config": {"workload": ("configs[4] ViT-L/14 16x224^2, tubelet 2x14x14 (N=2049), D=1024, L=24" if large else
+                                "configs[3] ViT-B/16 fine-tune 16x224^2, tubelet 2x16x16 (N=1569), FlashAttention "
+                                "fwd/bwd"), "clips_per_gpu": B, "global_batch": B * world, "seq_len": N,
                    "parallelism": f"dp{world}", "optimizer": "AdamW (fused kernel)",
                    "l2": "per-step working set (activations ~30 GB) >> 126 MB L2; no flush needed"},
         "attn_tflops": attn_tflops,
