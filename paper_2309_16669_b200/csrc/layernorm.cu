@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   }
 }
 
-template <int NC>
+template <int NC, bool SUM>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
                                                      const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ mean,
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
       }
       const uint4 q = pack8(o);
       *reinterpret_cast<uint4*>(dx + row * lddx + c) = q;
-      if (dsum) {
+      if (SUM) {
         float ob[8];
         unpack8(q, ob);   // sum what was stored (bf16), like a separate column-sum pass would
 #pragma unroll
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
       for (int e = 0; e < 8; ++e) {
         atomicAdd(&red[c + e], dg[k][e]);
         atomicAdd(&red[D + c + e], db[k][e]);
-        if (dsum) atomicAdd(&red[2 * D + c + e], cs[k][e]);
+        if (SUM) atomicAdd(&red[2 * D + c + e], cs[k][e]);
       }
     }
   }
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
   for (int i = threadIdx.x; i < D; i += blockDim.x) {
     if (dgamma) atomicAdd(dgamma + i, red[i]);
     if (dbeta) atomicAdd(dbeta + i, red[D + i]);
-    if (dsum) atomicAdd(dsum + i, red[2 * D + i]);
+    if (SUM) atomicAdd(dsum + i, red[2 * D + i]);
   }
 }
 
@@ -228,9 +228,15 @@ extern "C" int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, in
   AVB_CHECK_ARG(lddy % 8 == 0 && ldx % 8 == 0 && lddx % 8 == 0, "row strides must be multiples of 8");
   const int blocks = (int)std::min<int64_t>((M + 7) / 8, (int64_t)avb::sm_count() * 2);
   return dispatch_nc(D, [&](auto nc) {
-    ln_bwd_kernel<decltype(nc)::value><<<blocks, 256, 3 * D * sizeof(float), avb::as_stream(stream)>>>(
-        reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
-        mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, dx_colsum, M, D, accumulate);
+    constexpr int NCv = decltype(nc)::value;
+    if (dx_colsum)
+      ln_bwd_kernel<NCv, true><<<blocks, 256, 3 * D * sizeof(float), avb::as_stream(stream)>>>(
+          reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
+          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, dx_colsum, M, D, accumulate);
+    else
+      ln_bwd_kernel<NCv, false><<<blocks, 256, 3 * D * sizeof(float), avb::as_stream(stream)>>>(
+          reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
+          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, nullptr, M, D, accumulate);
     return avb::launch_status("avb_layernorm_bwd");
   });
 }
