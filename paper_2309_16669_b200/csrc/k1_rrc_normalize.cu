@@ -747,7 +747,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
       for (int64_t i = 0; i < B; ++i) min_ch = std::min(min_ch, (int)boxes_host[4 * i + 3]);
     }
     // envelope of the streaming ring: target height <= 7x the crop height (checked when host boxes exist)
-    if ((!boxes_host || (int64_t)min_ch * 7 >= Ht) && !getenv("AVB_K1_V2")) {
+    if ((!boxes_host || (int64_t)min_ch * 7 >= Ht) && getenv("AVB_K1_V3")) {
       size_t head = sizeof(float) * ((size_t)q.cps * tx_cap + (size_t)Ht * ty_cap) +
                     sizeof(int) * (2 * (size_t)q.cps + 2 * (size_t)Ht + 2 * SCH);
       head = (head + 15) & ~size_t(15);
