@@ -51,22 +51,25 @@ struct FwdArgs {
   int causal;
 };
 
-constexpr int F_STAGES = 3;
+constexpr int FKB = 64;                               // key tile
+constexpr int F_STAGES = 4;
 constexpr int F_SQ = 0;                               // 2 Q tiles (A, B) x 16 KB
-constexpr int F_SKV = 32768;                          // F_STAGES x (K 16 KB + V 16 KB)
-constexpr int F_BAR = F_SKV + F_STAGES * 32768;
-constexpr int F_SMEM = F_BAR + 256;
-static_assert(F_SMEM <= 232448, "attn fwd smem");
+constexpr int F_SKV = 32768;                          // F_STAGES x (K 8 KB + V 8 KB)
+constexpr int F_BAR = F_SKV + F_STAGES * 16384;
+constexpr int F_SMEM = F_BAR + 256 + 1024;   // + alignment slack
+static_assert(F_SMEM <= 115712, "attn fwd: two CTAs per SM");
 
-// TMEM (512 columns, 1 CTA/SM), per query tile g in {0,1}:
-//   S_g fp32 [128g*... ] at 128*g, P_g bf16x2 at 256 + 64*g, O_g fp32 at 384 + 64*g
+// TMEM (256 columns per CTA, 2 CTAs/SM -> four softmax groups per SM), per query tile g in {0,1}:
+//   S_g fp32 [64 key columns] at 64*g, overwritten in place by P_g (bf16 pairs, 32 columns) as the
+//   same thread consumes it; O_g fp32 at 128 + 64*g
 constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only when the running max grows by > 2^8
 
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(320, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // two CTAs per SM: align the 128B-swizzled tiles to 1 KB inside the window ourselves
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + F_SQ;
   uint8_t* sKV = smem + F_SKV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + F_BAR);
@@ -81,8 +84,8 @@ __global__ void __launch_bounds__(320, 1)
   const int q0 = blockIdx.x * 2 * BT;
   const bool hasB = q0 + BT < a.N;
   const int ng = hasB ? 2 : 1;
-  const int nkv_all = (a.N + BT - 1) / BT;
-  const int nkv = a.causal ? min(nkv_all, (q0 + ng * BT - 1) / BT + 1) : nkv_all;
+  const int nkv_all = (a.N + FKB - 1) / FKB;
+  const int nkv = a.causal ? min(nkv_all, (q0 + ng * BT - 1) / FKB + 1) : nkv_all;
 
   if (warp == 8 && lane == 0) {
     tc::tma_prefetch(&tmQ);
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     tc::fence_barrier_init();
   }
-  if (warp == 9) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tc::tmem_alloc(tmem_slot, 256);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -115,29 +118,29 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < nkv; ++j) {
         const int st = j % F_STAGES;
         tc::mbar_wait(&kv_empty[st], ((j / F_STAGES) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&kv_full[st], 32768);
-        tc::tma_load_3d(sKV + st * 32768, &tmK, &kv_full[st], h * HD, j * BT, b);
-        tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
+        tc::mbar_arrive_expect_tx(&kv_full[st], 16384);
+        tc::tma_load_3d(sKV + st * 16384, &tmK, &kv_full[st], h * HD, j * FKB, b);
+        tc::tma_load_3d(sKV + st * 16384 + 8192, &tmV, &kv_full[st], h * HD, j * FKB, b);
       }
     }
   } else if (warp == 9) {
     if (lane == 0) {
-      constexpr uint32_t idS = tc::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idS = tc::idesc_bf16_f32(128, FKB, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16_f32(128, 64, 0, 1);   // A = P from TMEM, B = V MN-major
       const uint32_t aQ = smem_u32(sQ);
       auto issue_s = [&](int g, int j) {
-        const uint32_t aK = smem_u32(sKV + (j % F_STAGES) * 32768);
+        const uint32_t aK = smem_u32(sKV + (j % F_STAGES) * 16384);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + 128 * g, tc::sdesc_sw128(aQ + g * 16384 + kk * 32, 16, 1024),
+          tc::umma_f16_ss(tmem + 64 * g, tc::sdesc_sw128(aQ + g * 16384 + kk * 32, 16, 1024),
                           tc::sdesc_sw128(aK + kk * 32, 16, 1024), idS, kk > 0);
         tc::umma_commit(gb + 4 * g + 0);
       };
       auto issue_pv = [&](int g, int j) {
-        const uint32_t aV = smem_u32(sKV + (j % F_STAGES) * 32768 + 16384);
+        const uint32_t aV = smem_u32(sKV + (j % F_STAGES) * 16384 + 8192);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts(tmem + 384 + 64 * g, tmem + 256 + 64 * g + kk * 8,
+        for (int kk = 0; kk < FKB / 16; ++kk)
+          tc::umma_f16_ts(tmem + 128 + 64 * g, tmem + 64 * g + kk * 8,
                           tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
         tc::umma_commit(gb + 4 * g + 3);
       };
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(320, 1)
       uint64_t* s_full = gb + 4 * g;
       uint64_t* p_full = s_full + 2;
       uint64_t* o_full = s_full + 3;
-      const uint32_t tS = tmem + 128 * g, tP = tmem + 256 + 64 * g, tO = tmem + 384 + 64 * g;
+      const uint32_t tS = tmem + 64 * g, tP = tS, tO = tmem + 128 + 64 * g;
       const int row = quad * 32 + lane;
       const int qi = q0 + g * BT + row;
       const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -172,19 +175,18 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < nkv; ++j) {
         tc::mbar_wait(s_full, j & 1);
         tc::tc_fence_after();
-        const int kv0 = j * BT;
+        const int kv0 = j * FKB;
         int lim = a.N - kv0;
         if (a.causal) lim = min(lim, qi - kv0 + 1);
-        // pass 1: row max (two TMEM round trips of 64 columns), 8 independent max chains
-        const bool full = lim >= BT;   // warp-uniform in the non-causal case: no per-element masking
+        // pass 1: row max (one TMEM round trip of 64 columns), 8 independent max chains
+        const bool full = lim >= FKB;  // warp-uniform in the non-causal case: no per-element masking
         float mxa[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mxa[k] = -INFINITY;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        {
           uint32_t r0[32], r1[32];
-          tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64, r0);
-          tc::tmem_ld_32x32b_x32(tS + lane_off + hh * 64 + 32, r1);
+          tc::tmem_ld_32x32b_x32(tS + lane_off, r0);
+          tc::tmem_ld_32x32b_x32(tS + lane_off + 32, r1);
           tc::tmem_ld_wait();
           if (full) {
 #pragma unroll
@@ -195,8 +197,8 @@ __global__ void __launch_bounds__(320, 1)
           } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
-              if (hh * 64 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r0[e]));
-              if (hh * 64 + 32 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r1[e]));
+              if (e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r0[e]));
+              if (32 + e < lim) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(r1[e]));
             }
           }
         }
@@ -226,14 +228,15 @@ __global__ void __launch_bounds__(320, 1)
           m_run = m_new;
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        // pass 2: p = exp2(s*scale - m), row sum (4 chains), bf16 pack straight into the TMEM P tile
+        // pass 2: p = exp2(s*scale - m), row sum (4 chains), bf16 P packed over the consumed S columns
+        // (P chunk c -> columns [16c, 16c+16), inside S chunk 0 which this thread has already read)
         float sm4[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t rb[2][32];
         tc::tmem_ld_32x32b_x32(tS + lane_off, rb[0]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < FKB / 32; ++c) {
           tc::tmem_ld_wait();
-          if (c + 1 < 4) tc::tmem_ld_32x32b_x32(tS + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
+          if (c + 1 < FKB / 32) tc::tmem_ld_32x32b_x32(tS + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   if (warp == 9) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    tc::tmem_dealloc(tmem, 256);
   }
 }
 
@@ -636,8 +639,9 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
   *reinterpret_cast<uint4*>(dq + b * sb + (int64_t)n * ld + h * HD + sub * 8) = v;
 }
 
-int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, int64_t sb) {
-  return avb::make_tmap_3d_bf16(m, p, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)ld, (uint64_t)sb, 64, 128, 1);
+int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, int64_t sb, uint32_t rows = 128) {
+  return avb::make_tmap_3d_bf16(m, p, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)ld, (uint64_t)sb, 64, rows,
+                                1);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -658,8 +662,8 @@ extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t
   CUtensorMap mq, mk, mv;
   int s;
   if ((s = make_maps(&mq, q, B, H, N, ld, sb))) return s;
-  if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
-  if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
+  if ((s = make_maps(&mk, k, B, H, N, ld, sb, FKB))) return s;
+  if ((s = make_maps(&mv, v, B, H, N, ld, sb, FKB))) return s;
   FwdArgs a;
   a.B = B;
   a.H = H;
