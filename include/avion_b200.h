@@ -110,10 +110,14 @@ int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_d
  *   bias: fp32 [N] or NULL.  aux/aux_out: bf16 [M, ldaux] (see AVB_EPI_*).
  * Used for patch-embed (K2), QKV / out-proj / fc1 / fc2 forward, dgrad (A K-major, B MN-major)
  * and wgrad (both MN-major, EPI_F32_ACCUM, split_k over the token dimension).
+ *   a_rowsum: fp32 [M] or NULL (fp32 epilogues only): a_rowsum[m] += sum_k A[m,k], unscaled --
+ *   for a wgrad (A = dY^T) that is the bias gradient, computed on the tensor cores from the
+ *   A tiles already in shared memory instead of a second pass over dY.
  */
 int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, int64_t ldb, int b_major,
              void* C, int64_t ldc, int M, int N, int K, int epilogue, const float* bias,
-             const void* aux, int64_t ldaux, void* aux_out, float alpha, int split_k, void* stream);
+             const void* aux, int64_t ldaux, void* aux_out, float alpha, int split_k,
+             float* a_rowsum, void* stream);
 
 /*
  * K4: blockwise attention forward, head_dim 64, fp32 online softmax, O(N) memory.
@@ -129,7 +133,7 @@ int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t ld, int64_
 /*
  * K5: blockwise attention backward (recomputes P from lse; no N x N storage).
  *   o, dout share (ld_o, sb_o); dq, dk, dv share (ld_g, sb_g).
- *   delta:  fp32 scratch [B*H, Npad];  dq_acc: fp32 scratch [B, N, H, 64].
+ *   delta:  fp32 scratch [2, B*H, Npad] (-rowsum(dO*O), -lse*log2e);  dq_acc: fp32 scratch [B, N, H, 64].
  */
 int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb,
                  const void* o, const void* dout, int64_t ld_o, int64_t sb_o, const float* lse,

@@ -22,6 +22,8 @@
 //   red.global.add.v4.f32 into an fp32 accumulator, converted to bf16 by a tiny kernel.
 #include "tc_common.cuh"
 
+#include <type_traits>
+
 namespace {
 
 constexpr int HD = 64;
@@ -33,6 +35,29 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return r;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
 }
 
 // write 8 consecutive bf16 (one 16B unit) of row `row` into a K-major SW128 tile set
@@ -295,8 +320,8 @@ __global__ void __launch_bounds__(320, 2)
 struct BwdArgs {
   int B, H, N, Npad;
   float scale, scale_log2;
-  const float* lse;
-  const float* delta;
+  const float* nlse2;     // -lse * log2(e)   [B*H, Npad] (written by the pre kernel)
+  const float* ndelta;    // -rowsum(dO * O)  [B*H, Npad]
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   int64_t ld_g, sb_g;     // strides of dk/dv
@@ -357,8 +382,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* s_full = bars + 5;
   uint64_t* ds_ready = bars + 6;
   uint64_t* mma_done = bars + 7;
-  uint64_t* dq_free = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* dq_free = bars + 8;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -382,7 +407,8 @@ __global__ void __launch_bounds__(320, 1)
     tc::mbar_init(s_full, 1);
     tc::mbar_init(ds_ready, kBwdCompute);
     tc::mbar_init(mma_done, 1);
-    tc::mbar_init(dq_free, kBwdCompute);
+    tc::mbar_init(&dq_free[0], kBwdCompute);
+    tc::mbar_init(&dq_free[1], kBwdCompute);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -390,6 +416,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM: S^T | dP^T | dV | dK | dQ x2 (double-buffered so dQ(i+1) accumulates while dQ(i) drains)
   const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384;
   const int64_t bh = (int64_t)b * a.H + h;
 
@@ -404,8 +431,8 @@ __global__ void __launch_bounds__(320, 1)
         tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
         tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
         tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
-        const float* gl = a.lse + bh * a.Npad + i * BT;
-        const float* gd = a.delta + bh * a.Npad + i * BT;
+        const float* gl = a.nlse2 + bh * a.Npad + i * BT;
+        const float* gd = a.ndelta + bh * a.Npad + i * BT;
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
                          smem_u32(sLD + st * 256)),
                      "l"(gl), "r"(smem_u32(&qd_full[st]))
@@ -446,7 +473,8 @@ __global__ void __launch_bounds__(320, 1)
           const int ps = (ii - 1) & 1;
           const uint32_t aQ = smem_u32(sQD + ps * 32768), aDO = aQ + 16384;
           const uint32_t aPT = smem_u32(sPT + ps * 32768), aDS = smem_u32(sDS + ps * 32768);
-          if (ii > 1) tc::mbar_wait(dq_free, (ii - 2) & 1);
+          const int use = (ii - 1) >> 1;   // use count of dQ buffer ps
+          if (use > 0) tc::mbar_wait(&dq_free[ps], (use & 1) ^ 1);
           tc::tc_fence_after();
           const uint32_t acc = (ii > 1) ? 1u : 0u;
 #pragma unroll
@@ -464,7 +492,7 @@ __global__ void __launch_bounds__(320, 1)
             // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
             // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
             const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
-            tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
+            tc::umma_f16_ss(tDQ + ps * 64, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
           }
           tc::umma_commit(mma_done);
           tc::umma_commit(&qd_empty[ps]);
@@ -478,19 +506,19 @@ __global__ void __launch_bounds__(320, 1)
     const int row = quad * 32 + lane;
     const int kvi = kv0 + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
     for (int ii = 0; ii < nq; ++ii) {
       const int i = i0 + ii, st = ii & 1;
       const int q0 = i * BT;
       uint8_t* pt = sPT + st * 32768;
       uint8_t* ds_t = sDS + st * 32768;
       if (ii >= 2) {
-        // this P^T slot staged dQ(ii-2): its TMA reduce must have read the smem (all warps)
+        // this warp's 4 KB of the P^T slot staged dQ(ii-2): its TMA reduce must have read it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        named_bar(1, 32 * kBwdCompute);
       }
       tc::mbar_wait(s_full, ii & 1);
-      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // lse/delta landed
+      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // -lse*log2e / -delta landed
       tc::tc_fence_after();
       const float* sl = sLD + st * 256;
       const float* sd = sl + 128;
@@ -500,64 +528,76 @@ __global__ void __launch_bounds__(320, 1)
         uint32_t rs[32], rp[32];
         tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
         tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+        // warp-uniform: does any element of this 32 x 32 block need masking?
+        const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
+                          (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
         tc::tmem_ld_wait();
+        auto body = [&](auto edge_tag) {
+          constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float4 l0 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8);
           const float4 l1 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8 + 4);
           const float4 d0 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8);
           const float4 d1 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8 + 4);
-          const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-          const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-          float p[8], ds[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int qc = c * 32 + u * 8 + e;
-            const int qi = q0 + qc;
-            const bool ok = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-            const float pe = ok ? ex2(fmaf(__uint_as_float(rs[u * 8 + e]), a.scale_log2, -lv[e] * kLog2e)) : 0.f;
-            p[e] = pe;
-            ds[e] = ok ? a.scale * pe * (__uint_as_float(rp[u * 8 + e]) - dv[e]) : 0.f;
-          }
+          const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                make_float2(l1.z, l1.w)};
+          const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
+                                make_float2(d1.z, d1.w)};
           uint4 v, w;
-          v.x = pack_bf16x2(p[0], p[1]);
-          v.y = pack_bf16x2(p[2], p[3]);
-          v.z = pack_bf16x2(p[4], p[5]);
-          v.w = pack_bf16x2(p[6], p[7]);
-          w.x = pack_bf16x2(ds[0], ds[1]);
-          w.y = pack_bf16x2(ds[2], ds[3]);
-          w.z = pack_bf16x2(ds[4], ds[5]);
-          w.w = pack_bf16x2(ds[6], ds[7]);
+          uint32_t* vp = &v.x;
+          uint32_t* wp = &w.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
+            const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
+            const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
+            float2 p = make_float2(ex2(arg.x), ex2(arg.y));
+            if (EDGE) {
+              const int qi = q0 + c * 32 + u * 8 + 2 * e;
+              const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+              const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
+              p.x = ok0 ? p.x : 0.f;
+              p.y = ok1 ? p.y : 0.f;
+            }
+            const float2 ds = f2mul(p, f2add(dp, nd[e]));   // P (dP - delta); softmax scale folded into dK / dQ
+            vp[e] = pack_bf16x2(p.x, p.y);
+            wp[e] = pack_bf16x2(ds.x, ds.y);
+          }
           st_sw128(pt, row, c * 4 + u, v);
           st_sw128(ds_t, row, c * 4 + u, w);
         }
+        };
+        if (edge)
+          body(std::true_type{});
+        else
+          body(std::false_type{});
       }
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_ready);
       if (ii > 0) {
-        // dQ(ii-1): TMEM lanes = query rows of tile i-1; stage into the P^T slot it no longer needs
+        // dQ(ii-1): TMEM lanes = query rows of tile i-1; stage into this warp's 4 KB of the P^T slot it no longer needs
+        const int pb = (ii - 1) & 1;
         tc::mbar_wait(mma_done, (ii - 1) & 1);
         tc::tc_fence_after();
-        drain_dq(tDQ + lane_off + half * 32, sPT + ((ii - 1) & 1) * 32768 + warp * 4096, &tmDQ, lane,
+        drain_dq(tDQ + pb * 64 + lane_off + half * 32, sPT + pb * 32768 + warp * 4096, &tmDQ, lane,
                  h * HD + half * 32, q0 - BT + quad * 32, b);
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(dq_free);
+        if (lane == 0) tc::mbar_arrive(&dq_free[pb]);
       }
     }
     // last dQ + dK/dV out
     tc::mbar_wait(mma_done, (nq - 1) & 1);
     tc::tc_fence_after();
-    if (nq >= 2) {
-      // the slot of tile nq-1 staged dQ(nq-3)? no: it held P(nq-1); staging dQ(nq-1) reuses it after mma_done
-    }
-    drain_dq(tDQ + lane_off + half * 32, sPT + ((nq - 1) & 1) * 32768 + warp * 4096, &tmDQ, lane, h * HD + half * 32,
-             (i0 + nq - 1) * BT + quad * 32, b);
+    drain_dq(tDQ + ((nq - 1) & 1) * 64 + lane_off + half * 32, sPT + ((nq - 1) & 1) * 32768 + warp * 4096, &tmDQ,
+             lane, h * HD + half * 32, (i0 + nq - 1) * BT + quad * 32, b);
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const uint32_t tsrc = which ? tDK : tDV;
+      const float osc = which ? a.scale : 1.f;   // dS was stored without the softmax scale
       __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + half * 32;
       uint32_t r[32];
       tc::tmem_ld_32x32b_x32(tsrc + lane_off + half * 32, r);
@@ -566,10 +606,10 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]), __uint_as_float(r[u * 8 + 1]));
-          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]), __uint_as_float(r[u * 8 + 3]));
-          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]), __uint_as_float(r[u * 8 + 5]));
-          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]), __uint_as_float(r[u * 8 + 7]));
+          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
+          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
+          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * osc, __uint_as_float(r[u * 8 + 5]) * osc);
+          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * osc, __uint_as_float(r[u * 8 + 7]) * osc);
           reinterpret_cast<uint4*>(g)[u] = v;
         }
       }
@@ -585,10 +625,12 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-// delta[b,h,n] = sum_d dO*O (fp32, padded rows); also zeroes the dQ accumulator rows.
+// ndelta[b,h,n] = -sum_d dO*O and nlse2[b,h,n] = -lse*log2(e) (fp32, padded rows), both in the
+// caller's delta workspace; also zeroes the dQ accumulator rows.
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o, int64_t sb_o,
                                     const __nv_bfloat16* __restrict__ dout, int64_t ld_do, int64_t sb_do,
-                                    float* __restrict__ delta, float* __restrict__ dq_acc, int B, int H, int N, int Npad) {
+                                    const float* __restrict__ lse, float* __restrict__ delta,
+                                    float* __restrict__ dq_acc, int B, int H, int N, int Npad) {
   // 8 threads per (b, n, h) row of 64 elements
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t item = gid >> 3;
@@ -612,14 +654,18 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
   s += __shfl_xor_sync(0xffffffff, s, 1);
   s += __shfl_xor_sync(0xffffffff, s, 2);
   s += __shfl_xor_sync(0xffffffff, s, 4);
-  if (sub == 0) delta[((int64_t)b * H + h) * Npad + n] = s;
+  if (sub == 0) {
+    const int64_t r = ((int64_t)b * H + h) * Npad + n;
+    delta[r] = -s;
+    delta[(int64_t)B * H * Npad + r] = -lse[r] * kLog2e;
+  }
   float4* z = reinterpret_cast<float4*>(dq_acc + item * HD + sub * 8);
   z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
   z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int64_t ld,
-                                       int64_t sb, int B, int H, int N) {
+                                       int64_t sb, int B, int H, int N, float scale) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one thread per 8 elements
   const int64_t total = (int64_t)B * N * H * 8;
   if (gid >= total) return;
@@ -632,10 +678,10 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
   const float4* s = reinterpret_cast<const float4*>(dq_acc + item * HD + sub * 8);
   const float4 x = s[0], y = s[1];
   uint4 v;
-  v.x = pack_bf16x2(x.x, x.y);
-  v.y = pack_bf16x2(x.z, x.w);
-  v.z = pack_bf16x2(y.x, y.y);
-  v.w = pack_bf16x2(y.z, y.w);
+  v.x = pack_bf16x2(x.x * scale, x.y * scale);
+  v.y = pack_bf16x2(x.z * scale, x.w * scale);
+  v.z = pack_bf16x2(y.x * scale, y.y * scale);
+  v.w = pack_bf16x2(y.z * scale, y.w * scale);
   *reinterpret_cast<uint4*>(dq + b * sb + (int64_t)n * ld + h * HD + sub * 8) = v;
 }
 
@@ -705,7 +751,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     const int64_t threads = (int64_t)B * N * H * 8;
     attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(o), ld_o, sb_o, reinterpret_cast<const __nv_bfloat16*>(dout), ld_o,
-        sb_o, delta, dq_acc, B, H, N, Npad);
+        sb_o, lse, delta, dq_acc, B, H, N, Npad);
     int s = avb::launch_status("attn_bwd_pre");
     if (s) return s;
   }
@@ -726,8 +772,8 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.Npad = Npad;
   a.scale = softmax_scale;
   a.scale_log2 = softmax_scale * kLog2e;
-  a.lse = lse;
-  a.delta = delta;
+  a.ndelta = delta;
+  a.nlse2 = delta + (int64_t)B * H * Npad;
   a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   a.ld_g = ld_g;
@@ -744,6 +790,6 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-      dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N);
+      dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N, softmax_scale);
   return avb::launch_status("attn_dq_convert");
 }

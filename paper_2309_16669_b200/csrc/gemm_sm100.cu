@@ -43,6 +43,7 @@ struct GemmArgs {
   int tma_out;           // bf16 C (and aux_out) written by TMA stores from swizzled smem
   int tma_aux;           // aux (residual / pre-activation) tiles TMA-prefetched into a smem ring
   float alpha;
+  float* rowsum;         // fp32 [M] or null: rowsum[m] += sum_k A[m,k] (the bias gradient of a wgrad)
 };
 
 template <int BN, bool A_MN, bool B_MN, int EK>
@@ -59,6 +60,7 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static_assert(SMEM <= 232448, "gemm smem");
   static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+  static constexpr uint32_t IDESC_RS = tc::idesc_bf16_f32(BM, 16, A_MN ? 1 : 0, 0);   // A x ones[16,K]
 };
 
 __device__ __forceinline__ void store_row_chunk(const GemmArgs& a, int row, int col, float (&v)[32]) {
@@ -195,6 +197,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.num_m * a.num_n * a.splits;
+  // Row sums of A ride along as a second accumulator: per K=16 step one extra M=128,N=16 MMA
+  // against a constant all-ones B tile (placed in the epilogue staging area, unused by fp32
+  // epilogues).  The accumulator sits at TMEM column BN, so the tile accumulator is
+  // single-buffered in this mode (wgrad launches own <= 1 tile per CTA anyway).
+  const bool rs_mode = a.rowsum != nullptr;
+  if (rs_mode) {
+    uint32_t* ones = reinterpret_cast<uint32_t*>(smem_epi);
+    for (int i = threadIdx.x; i < 512; i += kThreads) ones[i] = 0x3F803F80u;  // bf16 1.0 pairs, 16x64
+    tc::fence_proxy_async();
+  }
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
@@ -264,11 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int split = t / (a.num_m * a.num_n);
         const int kb0 = split * a.kb_per_split;
         const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = rs_mode ? 0 : (it & 1);
+        const uint32_t acc_phase = rs_mode ? (it & 1) : ((it >> 1) & 1);
+        const bool do_rs = rs_mode && (t % a.num_n) == 0;   // row sums once per row block (n-tile 0)
         tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
+        const uint32_t ones_u32 = smem_u32(smem_epi);
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::tc_fence_after();
@@ -279,6 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t da = A_MN ? tc::sdesc_sw128(sa + k * 2048, 8192, 1024) : tc::sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t db = B_MN ? tc::sdesc_sw128(sb + k * 2048, 8192, 1024) : tc::sdesc_sw128(sb + k * 32, 16, 1024);
             tc::umma_f16_ss(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (do_rs)
+              tc::umma_f16_ss(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
+                              (kb > kb0 || k > 0) ? 1u : 0u);
           }
           tc::umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
@@ -306,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       const int mn = t % (a.num_m * a.num_n);
       const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN + eh * (BN / 2);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = rs_mode ? 0 : (it & 1);
+      const uint32_t acc_phase = rs_mode ? (it & 1) : ((it >> 1) & 1);
       const int row0 = m0 + ew * 32;
       if (tma_aux && lane == 0) {
         // prefetch this tile's first XS aux chunks (the ring slots were freed by the last tile)
@@ -322,6 +339,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_after();
       const int row = row0 + lane;
       const uint32_t tbase = tmem + acc * BN + tlane + eh * (BN / 2);
+      if (rs_mode && eh == 0 && (mn % a.num_n) == 0) {
+        uint32_t rs;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rs) : "r"(tmem + BN + tlane));
+        tc::tmem_ld_wait();
+        if (row < a.M) atomicAdd(a.rowsum + row, __uint_as_float(rs));
+      }
       uint32_t rbuf[2][32];
       tc::tmem_ld_32x32b_x32(tbase, rbuf[0]);
 #pragma unroll
@@ -531,7 +554,7 @@ int make_tmap_3d_f32(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1
 
 extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, int64_t ldb, int b_major, void* C,
                         int64_t ldc, int M, int N, int K, int epilogue, const float* bias, const void* aux,
-                        int64_t ldaux, void* aux_out, float alpha, int split_k, void* stream) {
+                        int64_t ldaux, void* aux_out, float alpha, int split_k, float* a_rowsum, void* stream) {
   AVB_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "negative GEMM dims");
   if (M == 0 || N == 0) return AVB_OK;
   AVB_CHECK_ARG(K >= 1, "K must be >= 1");
@@ -548,6 +571,9 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   AVB_CHECK_ARG(epilogue != AVB_EPI_DGELU || aux, "DGELU needs aux (pre-activation)");
   AVB_CHECK_ARG(split_k >= 1, "split_k must be >= 1");
   AVB_CHECK_ARG(split_k == 1 || epilogue == AVB_EPI_F32_ACCUM, "split_k > 1 needs EPI_F32_ACCUM");
+  AVB_CHECK_ARG(!a_rowsum || epilogue == AVB_EPI_F32 || epilogue == AVB_EPI_F32_ACCUM,
+                "a_rowsum needs an fp32 epilogue (EPI_F32 / EPI_F32_ACCUM)");
+  AVB_CHECK_ARG(!a_rowsum || (reinterpret_cast<uintptr_t>(a_rowsum) & 3) == 0, "a_rowsum must be 4-byte aligned");
 
   const int BN = (N <= 128) ? 128 : 256;
   CUtensorMap ta, tb;
@@ -575,6 +601,7 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   g.ldaux = ldaux;
   g.aux_out = aux_out;
   g.alpha = alpha;
+  g.rowsum = a_rowsum;
   g.num_m = (M + BM - 1) / BM;
   g.num_n = (N + BN - 1) / BN;
   g.num_kb = (K + BK - 1) / BK;

@@ -27,10 +27,12 @@ def _rowmajor(t: torch.Tensor, name: str) -> int:
 
 def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = False, out: torch.Tensor | None = None,
          epilogue: int = EPI_BF16, bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
-         aux_out: torch.Tensor | None = None, alpha: float = 1.0, split_k: int = 1) -> torch.Tensor:
+         aux_out: torch.Tensor | None = None, alpha: float = 1.0, split_k: int = 1,
+         a_rowsum: torch.Tensor | None = None) -> torch.Tensor:
     """C = epi(alpha * A @ B^T) on the tcgen05 GEMM.
 
     a: [M,K] (a_mn=False) or [K,M] (a_mn=True); b: [N,K] (b_mn=False) or [K,N] (b_mn=True).
+    a_rowsum: fp32 [M], accumulated with sum_k A[m,k] (bias gradient of a wgrad; fp32 epilogues).
     """
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
         raise InputError("gemm operands must be bf16")
@@ -58,12 +60,15 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
             if t.dtype != torch.bfloat16 or tuple(t.shape) != (M, N):
                 raise InputError(f"{nm} must be bf16 [{M},{N}]")
             ldaux = _rowmajor(t, nm)
+    if a_rowsum is not None and (a_rowsum.dtype != torch.float32 or a_rowsum.numel() != M
+                                 or not a_rowsum.is_contiguous()):
+        raise InputError(f"a_rowsum must be contiguous fp32 [{M}]")
     if aux is not None and aux_out is not None and aux.stride(0) != aux_out.stride(0):
         raise InputError("aux and aux_out must share a leading dimension")
     lib = _lib.load()
     st = lib.avb_gemm(a.data_ptr(), lda, int(a_mn), b.data_ptr(), ldb, int(b_mn), out.data_ptr(), ldc, M, N, K,
                       epilogue, _ptr(bias), _ptr(aux), ldaux, _ptr(aux_out), float(alpha), int(split_k),
-                      _lib.stream_ptr())
+                      _ptr(a_rowsum), _lib.stream_ptr())
     _lib.check(st, "gemm")
     return out
 
@@ -115,7 +120,7 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
         g = torch.empty((B, N, 3, H * 64), dtype=torch.bfloat16, device=q.device)
         dq, dk, dv = g[:, :, 0], g[:, :, 1], g[:, :, 2]
     _, _, ld_g, sb_g = _bnhd(dq, "dq", H)
-    delta = torch.empty((B * H, npad(N)), dtype=torch.float32, device=q.device)
+    delta = torch.empty((2, B * H, npad(N)), dtype=torch.float32, device=q.device)
     dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device)
     scale = 64 ** -0.5 if scale is None else float(scale)
     st = _lib.load().avb_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(),

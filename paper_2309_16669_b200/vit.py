@@ -170,9 +170,25 @@ class ParamStore:
         return a, (b + self.ALIGN - 1) // self.ALIGN * self.ALIGN
 
 
-def wgrad_split(m_out: int, n_out: int, sms: int = 148) -> int:
+def wgrad_split(m_out: int, n_out: int, k_tokens: int | None = None, sms: int = 148) -> int:
+    """Split-K factor for a wgrad over k_tokens: minimise waves x (k-blocks per item + epilogue).
+
+    The fused bias-gradient mode runs a single-buffered accumulator, so every extra work item
+    per CTA pays its fp32 reduce epilogue (~35 k-block equivalents) un-overlapped.
+    """
     tiles = ((m_out + 127) // 128) * ((n_out + 255) // 256 if n_out > 128 else 1)
-    return max(1, sms // tiles)
+    if k_tokens is None:
+        return max(1, sms // tiles)
+    kb = (k_tokens + 63) // 64
+    best, best_cost = 1, None
+    for s in range(1, 17):
+        if s > kb:
+            break
+        waves = -(-tiles * s // sms)
+        cost = waves * (-(-kb // s) + 35)
+        if best_cost is None or cost < best_cost:
+            best, best_cost = s, cost
+    return best
 
 
 # ----------------------------------------------------------------------------- blocks
@@ -236,13 +252,11 @@ class TransformerStack:
             x, h1, mu1, rs1, qkv, o2, lse, x2, h2, mu2, rs2, pre, a = saved[l]
             # fc2: x3 = x2 + a W2^T + b2
             ops.gemm(dx, a, a_mn=True, b_mn=True, out=s.g(f"{g}.fc2.w"), epilogue=ops.EPI_F32_ACCUM,
-                     split_k=wgrad_split(D, Hd))
-            ops.colsum_accum(dx, s.g(f"{g}.fc2.b"))
+                     split_k=wgrad_split(D, Hd, M), a_rowsum=s.g(f"{g}.fc2.b"))
             dpre = ops.gemm(dx, s.w(f"{g}.fc2.w"), b_mn=True, epilogue=ops.EPI_DGELU, aux=pre)
             # fc1: pre = h2 W1^T + b1
             ops.gemm(dpre, h2, a_mn=True, b_mn=True, out=s.g(f"{g}.fc1.w"), epilogue=ops.EPI_F32_ACCUM,
-                     split_k=wgrad_split(Hd, D))
-            ops.colsum_accum(dpre, s.g(f"{g}.fc1.b"))
+                     split_k=wgrad_split(Hd, D, M), a_rowsum=s.g(f"{g}.fc1.b"))
             dh2 = ops.gemm(dpre, s.w(f"{g}.fc1.w"), b_mn=True)
             del dpre
             ops.layernorm_bwd(dh2, x2, s.p(f"{g}.ln2.g"), mu2, rs2, dx, s.g(f"{g}.ln2.g"), s.g(f"{g}.ln2.b"),
@@ -250,8 +264,7 @@ class TransformerStack:
             del dh2
             # proj: x2 = x + o Wo^T + bo
             ops.gemm(dx, o2, a_mn=True, b_mn=True, out=s.g(f"{g}.proj.w"), epilogue=ops.EPI_F32_ACCUM,
-                     split_k=wgrad_split(D, D))
-            ops.colsum_accum(dx, s.g(f"{g}.proj.b"))
+                     split_k=wgrad_split(D, D, M), a_rowsum=s.g(f"{g}.proj.b"))
             do = ops.gemm(dx, s.w(f"{g}.proj.w"), b_mn=True)
             q3 = qkv.view(B, N, 3 * D)
             dqkv = torch.empty((M, 3 * D), dtype=torch.bfloat16, device=dev)
@@ -260,8 +273,7 @@ class TransformerStack:
                          H, causal=self.causal, dq=d3[:, :, :D], dk=d3[:, :, D:2 * D], dv=d3[:, :, 2 * D:])
             del do
             ops.gemm(dqkv, h1, a_mn=True, b_mn=True, out=s.g(f"{g}.qkv.w"), epilogue=ops.EPI_F32_ACCUM,
-                     split_k=wgrad_split(3 * D, D))
-            ops.colsum_accum(dqkv, s.g(f"{g}.qkv.b"))
+                     split_k=wgrad_split(3 * D, D, M), a_rowsum=s.g(f"{g}.qkv.b"))
             dh1 = ops.gemm(dqkv, s.w(f"{g}.qkv.w"), b_mn=True)
             del dqkv
             ops.layernorm_bwd(dh1, x, s.p(f"{g}.ln1.g"), mu1, rs1, dx, s.g(f"{g}.ln1.g"), s.g(f"{g}.ln1.b"),
@@ -313,8 +325,7 @@ class VideoEncoder:
         dpe = torch.empty((B * Np, D), dtype=torch.bfloat16, device=dx.device)
         ops.tokens_bwd(dx, dpe, s.g(f"{P}.cls"), s.g(f"{P}.pos"), B, Np)
         ops.gemm(dpe, ctx["patches"], a_mn=True, b_mn=True, out=s.g(f"{P}.pe.w"), epilogue=ops.EPI_F32_ACCUM,
-                 split_k=wgrad_split(D, cfg.patch_dim))
-        ops.colsum_accum(dpe, s.g(f"{P}.pe.b"))
+                 split_k=wgrad_split(D, cfg.patch_dim, B * Np), a_rowsum=s.g(f"{P}.pe.b"))
         if on_layer_done is not None:
             on_layer_done(f"{P}.embed")
 
@@ -384,8 +395,8 @@ class ClassifierHead:
         logits = ops.gemm(z, s.w(f"{P}.w"), epilogue=ops.EPI_F32, bias=s.p(f"{P}.b"))
         dlogits = torch.zeros((B, self.Cp), dtype=torch.bfloat16, device=dev)
         ops.xent(logits[:, :self.C], labels, loss_scale, loss, dlogits)
-        ops.gemm(dlogits, z, a_mn=True, b_mn=True, out=s.g(f"{P}.w"), epilogue=ops.EPI_F32_ACCUM)
-        ops.colsum_accum(dlogits, s.g(f"{P}.b"))
+        ops.gemm(dlogits, z, a_mn=True, b_mn=True, out=s.g(f"{P}.w"), epilogue=ops.EPI_F32_ACCUM,
+                 a_rowsum=s.g(f"{P}.b"))
         dz = ops.gemm(dlogits, s.w(f"{P}.w"), b_mn=True)
         dx = torch.zeros((B * N, D), dtype=torch.bfloat16, device=dev)
         ops.layernorm_bwd(dz, cls, s.p(f"{P}.ln.g"), mu, rs, dx.view(B, N, D)[:, 0], s.g(f"{P}.ln.g"),

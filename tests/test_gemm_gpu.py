@@ -8,6 +8,7 @@ import pytest
 import torch
 
 from paper_2309_16669_b200 import ops
+from paper_2309_16669_b200.errors import InputError
 
 pytestmark = pytest.mark.gpu
 
@@ -81,3 +82,29 @@ def test_odd_n_unaligned_head():
     out = torch.empty(M, 3808, dtype=torch.float32, device="cuda")[:, :N]
     ops.gemm(A, B, out=out, epilogue=ops.EPI_F32)
     assert rel(out, A.float() @ B.float().t()) < 1e-4
+
+
+@pytest.mark.parametrize("Mtok,Nout,Kin,splits", [(100416 // 8, 768, 3072, 2), (12552, 3072, 768, 2),
+                                                  (1000, 200, 136, 1), (777, 2304, 768, 5), (64, 3808, 768, 1)])
+def test_wgrad_rowsum_bias_grad(Mtok, Nout, Kin, splits):
+    # fused bias gradient: a_rowsum[n] += sum_tokens dY[token, n] alongside dW = dY^T X
+    dY, X = mk(Mtok, Nout, seed=16), mk(Mtok, Kin, seed=17)
+    acc = torch.zeros((Nout, Kin), device="cuda")
+    db = torch.full((Nout,), 0.5, device="cuda")
+    ops.gemm(dY, X, a_mn=True, b_mn=True, out=acc, epilogue=ops.EPI_F32_ACCUM, split_k=splits, a_rowsum=db)
+    assert rel(acc, dY.float().t() @ X.float()) < 1e-4
+    ref = dY.float().sum(0) + 0.5
+    assert (db - ref).abs().max().item() < 1e-3 * max(1.0, ref.abs().max().item())
+    # a second call accumulates
+    ops.gemm(dY, X, a_mn=True, b_mn=True, out=acc, epilogue=ops.EPI_F32_ACCUM, split_k=splits, a_rowsum=db)
+    assert (db - (2 * dY.float().sum(0) + 0.5)).abs().max().item() < 2e-3 * max(1.0, ref.abs().max().item())
+
+
+def test_rowsum_k_major_and_rejects_bf16_epilogue():
+    A, B = mk(300, 520, seed=18), mk(256, 520, seed=19)
+    rs = torch.zeros(300, device="cuda")
+    out = ops.gemm(A, B, epilogue=ops.EPI_F32, a_rowsum=rs)
+    assert rel(out, A.float() @ B.float().t()) < 1e-4
+    assert (rs - A.float().sum(1)).abs().max().item() < 1e-3 * max(1.0, A.float().sum(1).abs().max().item())
+    with pytest.raises(InputError):
+        ops.gemm(A, B, a_rowsum=rs)
