@@ -177,7 +177,7 @@ def run_augment(args, rank, world, local):
     stream = torch.cuda.current_stream()
 
     def step():
-        TR.transform(frames, boxes_d, flips_d, out=out, validate=False)
+        TR.transform(frames, boxes_d, flips_d, out=out, crops_host=boxes)
 
     for _ in range(args.warmup):
         step()
@@ -208,7 +208,7 @@ def run_augment(args, rank, world, local):
 
     def e2e_step():
         dev_in.copy_(host, non_blocking=True)
-        o = TR.transform(dev_in, boxes_d, flips_d, out=out, validate=False)
+        o = TR.transform(dev_in, boxes_d, flips_d, out=out, crops_host=boxes)
         res.copy_(o.view(B, -1)[:, :1].float().view(B), non_blocking=True)
 
     for _ in range(2):

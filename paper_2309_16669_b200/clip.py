@@ -38,12 +38,12 @@ class CLIPModel:
         self.opt = opt or AdamWConfig()
         self.step_num = 0
 
-    def patches_from_clips(self, frames, boxes, flips, out=None):
+    def patches_from_clips(self, frames, boxes, flips, out=None, boxes_host=None):
         from . import transform as TR
 
         c = self.vcfg
         return TR.transform(frames, boxes, flips, (c.height, c.width), out=out, layout="tubelet",
-                            tubelet=(c.cube_t, c.cube_h, c.cube_w), validate=False)
+                            tubelet=(c.cube_t, c.cube_h, c.cube_w), validate=False, crops_host=boxes_host)
 
     def _head_fwd(self, rows, ln_g, ln_b, proj):
         s = self.store

@@ -42,7 +42,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     def step():
         store.grad.zero_()
         loss.zero_()
-        TR.transform(frames, boxes_d, flips_d, (vc.height, vc.width), out=patches, layout="tubelet",
+        TR.transform(frames, boxes_d, flips_d, (vc.height, vc.width), out=patches, layout="tubelet", crops_host=boxes,
                      tubelet=(vc.cube_t, vc.cube_h, vc.cube_w), validate=False)
         model.forward_backward(patches, tokens, eot, loss, on_layer_done=reducer.on_layer_done)
         reducer.finish()

@@ -18,10 +18,14 @@
 //      mirror), then y = v*inv_std/255 - mean*inv_std, packed bf16x2 / float2 stores,
 //      coalesced along Wt.
 #include "common.cuh"
+#include "tc_common.cuh"
 
 #include <algorithm>
 #include <math.h>
 #include <stdlib.h>
+
+#include <type_traits>
+#include <vector>
 
 namespace {
 
@@ -46,6 +50,7 @@ struct K1Params {
   int rowb_cap;   // staged bytes per row (multiple of 16)
   int fast;       // interleaved RGB (s_c == 1, s_w == 3)
   int tt, tph, tpw;  // tubelet (AVB_LAYOUT_TUBELET)
+  int only_upscale;  // 1: skip clips that are downscales in both axes (v4 did them)
 };
 
 // Exact-integer tap range + fp64 tent weights (torch/PIL antialias rule).
@@ -137,6 +142,7 @@ __global__ void __launch_bounds__(kThreads) k1_rrc_normalize_kernel(const K1Para
   const int x0 = box.x, y0 = box.y, cw = box.z, ch = box.w;
   // device-side containment re-check (CropRect.contained_in, rrc.py:81-85)
   if (x0 < 0 || y0 < 0 || cw < 1 || ch < 1 || x0 + cw > p.W || y0 + ch > p.H) return;
+  if (p.only_upscale && cw >= p.Wt && ch >= p.Ht) return;
   const bool flip = p.flips ? (p.flips[b] != 0) : false;
 
   // ---- shared-memory carve-up ----
@@ -294,6 +300,7 @@ struct K1v2Params {
   int tx_cap, ty_cap;           // tap-table strides
   int rows_cap, rowb_cap;       // staging rows per band, staged bytes per row (multiple of 16)
   int64_t total_bytes;          // bytes of the source tensor (cp.async zero-fill guard)
+  int only_upscale;             // 1: skip clips that are downscales in both axes (v4 did them)
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -329,6 +336,7 @@ __global__ void __launch_bounds__(kThreads) k1v2_kernel(const K1v2Params p) {
   const int4 box = *reinterpret_cast<const int4*>(p.boxes + 4 * b);
   const int x0 = box.x, y0 = box.y, cw = box.z, ch = box.w;
   if (x0 < 0 || y0 < 0 || cw < 1 || ch < 1 || x0 + cw > p.W || y0 + ch > p.H) return;
+  if (p.only_upscale && cw >= p.Wt && ch >= p.Ht) return;
   const bool flip = p.flips ? (p.flips[b] != 0) : false;
   // this strip, in unflipped column space jj; output column j = flip ? Wt-1-jj : jj
   const int jj0 = strip * p.cps;
@@ -629,6 +637,419 @@ __global__ void __launch_bounds__(kThreads) k1v3_kernel(const K1v2Params p) {
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// K1 v4 (default for downscales of interleaved RGB): horizontal-first streaming.
+//
+//   grid = (frame groups, B): a CTA owns FPC frames of one clip (they share every tap; Wt = 224
+//   gives FPC = 2, whose 224 column pairs fill exactly 7 warps) and streams the crop's source
+//   rows top to bottom exactly once:
+//   * one producer thread (warp `ncomp/32`) keeps a V4_RS-deep ring of staged rows full with one
+//     `cp.async.bulk` per (row, frame) from the 16-byte-aligned-down row start (rows past
+//     `tail_y`, whose rounded copy could cross the tensor end, take zero-filled 16-byte
+//     cp.async); completion on a per-slot `full` mbarrier, release by the 7 compute warps on an
+//     `empty` mbarrier;
+//   * every compute lane owns two adjacent OUTPUT columns (j, j+1) of one frame for the whole
+//     frame, with its horizontal taps (NT, zero-padded) in registers.  Per source row it reads
+//     its two tap windows (funnel-shifted words), converts bytes to floats (PRMT into
+//     0x4B0000xx, FADD2 -2^23) and filters the three channels of both columns with FFMA2 -- no
+//     shared-memory traffic for intermediate values;
+//   * the vertical pass is a push: the (<= NOPEN) output rows whose windows contain the source
+//     row accumulate w * h in registers; a row is normalised, cast and stored the moment its
+//     window closes.  The per-source-row weights / emission counts are a per-clip table built in
+//     the prologue in O(1) per row, identical for every lane, so control flow is block-uniform.
+//   No __syncthreads in the main loop; each source byte is read from HBM once.
+constexpr int V4_RS = 16;  // staged-row ring depth (one row of every frame of the CTA per stage)
+
+struct K1v4Params {
+  const uint8_t* src;
+  int64_t s_clip, s_t, s_h;
+  int T, H, W, Ht, Wt;
+  const int32_t* boxes;
+  const uint8_t* flips;
+  float scale[3], bias[3];
+  void* dst;
+  int out_dtype, out_layout, tt, tph, tpw;
+  int fpc;         // frames per CTA
+  int tpf;         // column pairs (compute lanes) per frame = ceil(Wt / 2)
+  int ncomp;       // compute threads (multiple of 32); the producer warp follows
+  int slot_bytes;  // bytes per staged row (multiple of 16)
+  int64_t total_bytes;
+};
+
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+
+// NT-tap (zero-padded) register copy of the exact-integer taps of output column i (same fp64 math
+// and summation order as k1_taps, so the weights are bit-identical).  Downscale only.
+template <int NT>
+__device__ __forceinline__ void k1_taps_reg(int crop, int tgt, int i, float (&w)[NT], int& lo_out) {
+  const long long c2 = 2LL * tgt;
+  long long lo = floordiv_i64((long long)crop * (2 * i - 1) + tgt, c2);
+  long long hi = floordiv_i64((long long)crop * (2 * i + 3) + tgt, c2);
+  if (lo < 0) lo = 0;
+  if (hi > crop) hi = crop;
+  const int n = static_cast<int>(hi - lo);
+  const double s = static_cast<double>(crop) / tgt;
+  const double inv = 1.0 / s;
+  const double c = s * (i + 0.5);
+  double wd[NT];
+  double tot = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const double d = fabs((lo + k + 0.5 - c) * inv);
+    wd[k] = (k < n && d < 1.0) ? 1.0 - d : 0.0;
+    tot += wd[k];
+  }
+  const double r = tot > 0.0 ? 1.0 / tot : 0.0;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) w[k] = static_cast<float>(wd[k] * r);
+  lo_out = static_cast<int>(lo);
+}
+
+// Weight of source row y in output row i (downscale rule; 0 outside the row's window).
+__device__ __forceinline__ float k1_row_weight(int crop, int tgt, int i, int y) {
+  const long long c2 = 2LL * tgt;
+  long long lo = floordiv_i64((long long)crop * (2 * i - 1) + tgt, c2);
+  long long hi = floordiv_i64((long long)crop * (2 * i + 3) + tgt, c2);
+  if (lo < 0) lo = 0;
+  if (hi > crop) hi = crop;
+  if (y < lo || y >= hi) return 0.f;
+  const double s = static_cast<double>(crop) / tgt;
+  const double inv = 1.0 / s;
+  const double c = s * (i + 0.5);
+  double tot = 0.0, wy = 0.0;
+  for (long long k = 0; k < hi - lo; ++k) {
+    const double d = fabs((lo + k + 0.5 - c) * inv);
+    const double w = d < 1.0 ? 1.0 - d : 0.0;
+    tot += w;
+    if (lo + k == y) wy = w;
+  }
+  return static_cast<float>(wy * (tot > 0.0 ? 1.0 / tot : 0.0));
+}
+
+// #{output rows i : hi_i <= y} for source row y < crop (rows whose window ended before y).
+__device__ __forceinline__ int k1_rows_done(int crop, int tgt, int y) {
+  // hi_i <= y  <=>  crop*(2i+3) + tgt < 2*tgt*(y+1)  <=>  i < N / (2 crop)
+  const long long N = 2LL * tgt * (y + 1) - tgt - 3LL * crop;
+  if (N <= 0) return 0;
+  const long long n = (N + 2LL * crop - 1) / (2LL * crop);
+  return n > tgt ? tgt : static_cast<int>(n);
+}
+
+// The 4*NW bytes starting at byte offset o of a staged row, as NW words (o may be unaligned).
+template <int NW>
+__device__ __forceinline__ void k1_window(const uint8_t* slot, int o, uint32_t (&s)[NW]) {
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(slot + (o & ~3));
+  const uint32_t sh = (o & 3) * 8;
+  uint32_t u[NW + 1];
+#pragma unroll
+  for (int k = 0; k <= NW; ++k) u[k] = wp[k];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) s[k] = __funnelshift_r(u[k], u[k + 1], sh);
+}
+
+// byte q of a word stream -> 2^23 + byte as a float bit pattern (exact)
+template <int Q, int NW>
+__device__ __forceinline__ float k1_magic(const uint32_t (&s)[NW]) {
+  return __uint_as_float(__byte_perm(s[Q >> 2], 0x4B000000u, 0x7440u | (Q & 3)));
+}
+
+template <int NT, int C, int K = 0>
+struct K1HTap {
+  template <int NW>
+  __device__ __forceinline__ static void run(const uint32_t (&s0)[NW], const uint32_t (&s1)[NW], const float2 (&wp)[NT],
+                                             float2& h) {
+    if constexpr (K < NT) {
+      const float2 f = fadd2(make_float2(k1_magic<3 * K + C>(s0), k1_magic<3 * K + C>(s1)),
+                             make_float2(-8388608.f, -8388608.f));
+      h = ffma2(wp[K], f, h);
+      K1HTap<NT, C, K + 1>::run(s0, s1, wp, h);
+    }
+  }
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NT, int NOPEN>
+__global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int NW = (3 * NT + 3) / 4;
+  static_assert(NOPEN <= 3, "emission count lives in rowtab.w");
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.y;
+  const int t0 = blockIdx.x * p.fpc;
+  const int4 box = *reinterpret_cast<const int4*>(p.boxes + 4 * b);
+  const int x0 = box.x, y0 = box.y, cw = box.z, ch = box.w;
+  if (x0 < 0 || y0 < 0 || cw < p.Wt || ch < p.Ht || x0 + cw > p.W || y0 + ch > p.H) return;
+  const bool flip = p.flips ? (p.flips[b] != 0) : false;
+
+  // ---- smem: full [RS] | empty [RS] | rowtab [H] | ring [RS][fpc][slot_bytes]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + V4_RS;
+  float4* rowtab = reinterpret_cast<float4*>(empty + V4_RS);
+  uint8_t* ring = reinterpret_cast<uint8_t*>(rowtab + p.H);
+  const size_t stage_stride = (size_t)p.fpc * p.slot_bytes;
+
+  // ---- per-source-row push table: weights of the NOPEN open output rows, rows completed after it
+  for (int y = tid; y < ch; y += blockDim.x) {
+    const int base = k1_rows_done(ch, p.Ht, y);
+    const int next = (y + 1 < ch) ? k1_rows_done(ch, p.Ht, y + 1) : p.Ht;
+    float w[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < NOPEN; ++q)
+      if (base + q < p.Ht) w[q] = k1_row_weight(ch, p.Ht, base + q, y);
+    rowtab[y] = make_float4(w[0], w[1], w[2], __int_as_float(next - base));
+  }
+  if (tid == 0) {
+    for (int s = 0; s < V4_RS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], p.ncomp / 32);
+    }
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (tid >= p.ncomp) {
+    // ================= producer: one lane, one bulk copy per (source row, frame)
+    if (tid != p.ncomp) return;
+    const uint8_t* src_end = p.src + p.total_bytes;
+    const uint8_t* row0 = p.src + b * p.s_clip + (int64_t)t0 * p.s_t + (int64_t)y0 * p.s_h + (int64_t)x0 * 3;
+    const int nf = min(p.fpc, p.T - t0);
+    const uint32_t span = 3u * cw;
+    // first row whose rounded-up copy (of the last frame) could reach past the tensor end
+    int tail_y = ch;
+    {
+      const uint8_t* last = row0 + (int64_t)(nf - 1) * p.s_t;
+      for (int y = ch - 1; y >= 0 && last + (int64_t)y * p.s_h + span + 15 > src_end; --y) tail_y = y;
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    const uint8_t* a_row = row0;
+    for (int y = 0; y < ch; ++y, a_row += p.s_h) {
+      if (y >= V4_RS) tc::mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* dst = ring + (size_t)s * stage_stride;
+      if (y < tail_y) {
+        uint32_t tx = 0;
+        const uint8_t* a = a_row;
+        for (int f = 0; f < nf; ++f, a += p.s_t) tx += (((uint32_t)(uintptr_t)a & 15u) + span + 15u) & ~15u;
+        tc::mbar_arrive_expect_tx(&full[s], tx);
+        a = a_row;
+        for (int f = 0; f < nf; ++f, a += p.s_t) {
+          const uint32_t mis = (uint32_t)(uintptr_t)a & 15u;
+          bulk_g2s(dst + (size_t)f * p.slot_bytes, a - mis, (mis + span + 15u) & ~15u, &full[s]);
+        }
+      } else {  // bytes past the tensor end would fault: zero-filled 16-byte cp.async instead
+        const uint8_t* a = a_row;
+        for (int f = 0; f < nf; ++f, a += p.s_t) {
+          const uint8_t* al = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15));
+          const uint32_t nb = ((uint32_t)(a - al) + span + 15u) & ~15u;
+          for (uint32_t k = 0; k < nb; k += 16) {
+            const int64_t left = src_end - (al + k);
+            const int n = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
+            cp_async16(dst + (size_t)f * p.slot_bytes + k, n ? al + k : p.src, n);
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+      }
+      if (++s == V4_RS) { s = 0; ph ^= 1; }
+    }
+    return;
+  }
+
+  // ================= compute lanes: output columns (j0, j0+1) of frame t
+  const int f = tid / p.tpf;
+  const int m = tid - f * p.tpf;
+  const int t = t0 + f;
+  const bool active = f < p.fpc && t < p.T;
+  const int j0 = 2 * m;
+  const bool has1 = active && j0 + 1 < p.Wt;
+  float2 wp[NT];
+  int o0 = 0, o1 = 0;
+  {
+    float w0[NT], w1[NT];
+    int lo0 = 0, lo1 = 0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) w0[k] = w1[k] = 0.f;
+    if (active) k1_taps_reg<NT>(cw, p.Wt, flip ? p.Wt - 1 - j0 : j0, w0, lo0);
+    if (has1) k1_taps_reg<NT>(cw, p.Wt, flip ? p.Wt - 2 - j0 : j0 + 1, w1, lo1);
+    else lo1 = lo0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) wp[k] = make_float2(w0[k], w1[k]);
+    o0 = 3 * lo0;
+    o1 = 3 * lo1;
+  }
+  // output: element offset obase + rowoff(row) + c * cstride (32-bit within a clip, all layouts)
+  int64_t obase;
+  int cstride, small_step, big_step, rph = 0, ph_rows;
+  {
+    const int tt = active ? t : t0;
+    const int plane = p.Ht * p.Wt;
+    if (p.out_layout == AVB_LAYOUT_CTHW) {
+      obase = (b * 3 * p.T + tt) * (int64_t)plane + j0;
+      cstride = p.T * plane;
+      small_step = big_step = p.Wt;
+      ph_rows = 1 << 30;
+    } else if (p.out_layout == AVB_LAYOUT_TCHW) {
+      obase = (b * p.T + tt) * 3 * (int64_t)plane + j0;
+      cstride = plane;
+      small_step = big_step = p.Wt;
+      ph_rows = 1 << 30;
+    } else {
+      const int npy = p.Ht / p.tph, npx = p.Wt / p.tpw;
+      const int64_t Np = (int64_t)(p.T / p.tt) * npy * npx;
+      const int F = 3 * p.tt * p.tph * p.tpw;
+      obase = b * Np * F + ((int64_t)(tt / p.tt) * npy * npx + j0 / p.tpw) * F + (tt % p.tt) * p.tph * p.tpw +
+              j0 % p.tpw;
+      cstride = p.tt * p.tph * p.tpw;
+      small_step = p.tpw;
+      big_step = npx * F - (p.tph - 1) * p.tpw;
+      ph_rows = p.tph;
+    }
+  }
+  const bool pair_store = has1 && (p.Wt & 1) == 0;
+  const bool bf16 = p.out_dtype == AVB_DTYPE_BF16;
+  uint8_t* dbase = reinterpret_cast<uint8_t*>(p.dst) + obase * (bf16 ? 2 : 4);
+  // low bits of each row's global address (its misalignment inside the 16-byte-aligned copy)
+  uint32_t alo = (uint32_t)reinterpret_cast<uintptr_t>(p.src + b * p.s_clip + (int64_t)(active ? t : t0) * p.s_t +
+                                                       (int64_t)y0 * p.s_h + (int64_t)x0 * 3);
+  const uint32_t sh_lo = (uint32_t)p.s_h;
+  const uint8_t* slot = ring + (size_t)(active ? f : 0) * p.slot_bytes;
+  const uint8_t* slot0 = slot;
+  const int lane = tid & 31;
+
+  float2 acc[NOPEN][3];
+#pragma unroll
+  for (int q = 0; q < NOPEN; ++q)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[q][c] = make_float2(0.f, 0.f);
+  int rowoff = 0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int y = 0; y < ch; ++y) {
+    tc::mbar_wait(&full[s], ph);
+    const float4 rw = rowtab[y];
+    float2 h[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    {
+      const int mis = (int)(alo & 15u);
+      uint32_t s0[NW], s1[NW];
+      k1_window<NW>(slot, mis + o0, s0);
+      k1_window<NW>(slot, mis + o1, s1);
+      K1HTap<NT, 0>::run(s0, s1, wp, h[0]);
+      K1HTap<NT, 1>::run(s0, s1, wp, h[1]);
+      K1HTap<NT, 2>::run(s0, s1, wp, h[2]);
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&empty[s]);
+    alo += sh_lo;
+    slot += stage_stride;
+    if (++s == V4_RS) { s = 0; ph ^= 1; slot = slot0; }
+    const float wq[3] = {rw.x, rw.y, rw.z};
+#pragma unroll
+    for (int q = 0; q < NOPEN; ++q)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[q][c] = ffma2(make_float2(wq[q], wq[q]), h[c], acc[q][c]);
+    const int ne = __float_as_int(rw.w);
+    for (int e = 0; e < ne; ++e) {
+      if (active) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float2 v = ffma2(acc[0][c], make_float2(p.scale[c], p.scale[c]), make_float2(p.bias[c], p.bias[c]));
+          const int oc = rowoff + c * cstride;
+          if (bf16) {
+            __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dbase) + oc;
+            if (pair_store) {
+              *reinterpret_cast<uint32_t*>(d) = pack_bf16x2(v.x, v.y);
+            } else {
+              d[0] = __float2bfloat16_rn(v.x);
+              if (has1) d[1] = __float2bfloat16_rn(v.y);
+            }
+          } else {
+            float* d = reinterpret_cast<float*>(dbase) + oc;
+            if (pair_store) {
+              *reinterpret_cast<float2*>(d) = v;
+            } else {
+              d[0] = v.x;
+              if (has1) d[1] = v.y;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q + 1 < NOPEN; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[q][c] = acc[q + 1][c];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[NOPEN - 1][c] = make_float2(0.f, 0.f);
+      if (++rph == ph_rows) { rph = 0; rowoff += big_step; } else { rowoff += small_step; }
+    }
+  }
+}
+
+// Host-side envelope for v4, in the exact-integer tap ranges of k1_taps: the most taps of any output
+// column (nt) and the most output rows whose vertical windows share one source row (nopen).
+static void k1_range(int crop, int tgt, int i, int& lo, int& hi) {
+  const long long c2 = 2LL * tgt;
+  auto fd = [](long long a, long long d) { long long q = a / d; if ((a % d != 0) && (a < 0)) --q; return q; };
+  const long long l = fd((long long)crop * (2 * i - 1) + tgt, c2);
+  const long long h = fd((long long)crop * (2 * i + 3) + tgt, c2);
+  lo = (int)std::max(0LL, l);
+  hi = (int)std::min((long long)crop, h);
+}
+static int k1_max_taps(int crop, int tgt) {
+  int nt = 0;
+  for (int j = 0; j < tgt; ++j) {
+    int l, h;
+    k1_range(crop, tgt, j, l, h);
+    nt = std::max(nt, h - l);
+  }
+  return nt;
+}
+static int k1_max_open(int crop, int tgt) {
+  std::vector<int> lo(tgt), hi(tgt);
+  for (int i = 0; i < tgt; ++i) k1_range(crop, tgt, i, lo[i], hi[i]);
+  int nlo = 0, base = 0, no = 0;  // open rows at source row y: base(y) .. #{lo <= y} - 1
+  for (int y = 0; y < crop; ++y) {
+    while (nlo < tgt && lo[nlo] <= y) ++nlo;
+    while (base < tgt && hi[base] <= y) ++base;
+    no = std::max(no, nlo - base);
+  }
+  return no;
+}
+// boxes given: exact over the batch; false if some box is not a downscale in both axes.
+static bool k1v4_envelope(const int32_t* boxes, int64_t B, int Ht, int Wt, int& nt, int& nopen) {
+  nt = 0;
+  nopen = 0;
+  for (int64_t bi = 0; bi < B; ++bi) {
+    const int cw = boxes[4 * bi + 2], ch = boxes[4 * bi + 3];
+    if (cw < Wt || ch < Ht) return false;
+    nt = std::max(nt, k1_max_taps(cw, Wt));
+    nopen = std::max(nopen, k1_max_open(ch, Ht));
+  }
+  return true;
+}
+// device-only boxes: worst case over every downscale crop that fits the frame (cached per geometry).
+static void k1v4_envelope_all(int H, int W, int Ht, int Wt, int& nt, int& nopen) {
+  struct Entry { int H, W, Ht, Wt, nt, nopen; };
+  static thread_local std::vector<Entry> cache;
+  for (const Entry& e : cache)
+    if (e.H == H && e.W == W && e.Ht == Ht && e.Wt == Wt) { nt = e.nt; nopen = e.nopen; return; }
+  nt = 0;
+  nopen = 0;
+  for (int cw = Wt; cw <= W; ++cw) nt = std::max(nt, k1_max_taps(cw, Wt));
+  for (int ch = Ht; ch <= H; ++ch) nopen = std::max(nopen, k1_max_open(ch, Ht));
+  cache.push_back({H, W, Ht, Wt, nt, nopen});
+}
+
 }  // namespace
 
 extern "C" int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_dev,
@@ -713,6 +1134,62 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     cudaFuncSetAttribute(k1v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
+  // v4: streaming kernel for interleaved RGB downscales (every config-2 crop).  With host boxes
+  //     the tap envelope is exact; with device-only boxes it is the worst case over every
+  //     downscale crop and a complement launch of v2 covers any upscale clip.
+  bool v4_done = false, v4_partial = false;
+  if (p.fast && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && !getenv("AVB_K1_V1") &&
+      !getenv("AVB_K1_V2") && !getenv("AVB_K1_V3") && Ht <= H && Wt <= W && Wt <= 448 && T <= 65535 &&
+      B <= 65535 && 3LL * T * Ht * Wt < (1LL << 31)) {
+    int nt = 0, nopen = 0, cw_max = W;
+    bool ok = true;
+    if (boxes_host) {
+      ok = k1v4_envelope(boxes_host, B, Ht, Wt, nt, nopen);
+      cw_max = 0;
+      for (int64_t i = 0; i < B; ++i) cw_max = std::max(cw_max, (int)boxes_host[4 * i + 2]);
+    } else {
+      k1v4_envelope_all(H, W, Ht, Wt, nt, nopen);
+      v4_partial = true;
+    }
+    if (ok && nt <= 8 && nopen <= 3) {
+      const int NT = nt <= 4 ? 4 : nt <= 5 ? 5 : nt <= 6 ? 6 : 8;
+      const int NOPEN = nopen <= 2 ? 2 : 3;
+      const int NW = (3 * NT + 3) / 4;
+      K1v4Params q;
+      q.src = src; q.s_clip = s_clip; q.s_t = s_t; q.s_h = s_h;
+      q.T = T; q.H = H; q.W = W; q.Ht = Ht; q.Wt = Wt;
+      q.boxes = boxes_dev; q.flips = hflip_dev;
+      for (int c = 0; c < 3; ++c) { q.scale[c] = p.scale[c]; q.bias[c] = p.bias[c]; }
+      q.dst = dst; q.out_dtype = out_dtype; q.out_layout = out_layout; q.tt = tt; q.tph = tph; q.tpw = tpw;
+      q.tpf = (Wt + 1) / 2;
+      q.fpc = std::max(1, std::min(T, 224 / q.tpf));
+      q.ncomp = ((q.fpc * q.tpf + 31) / 32) * 32;
+      // a window read ends <= 15 (misalignment) + 3*cw + 4*(NW+1) bytes into the slot
+      q.slot_bytes = ((3 * cw_max + 4 * (NW + 1) + 15 + 15) / 16) * 16;
+      q.total_bytes = (B - 1) * s_clip + (int64_t)(T - 1) * s_t + (int64_t)(H - 1) * s_h + (int64_t)W * 3;
+      const size_t smem4 = sizeof(uint64_t) * 2 * V4_RS + sizeof(float4) * (size_t)H +
+                           (size_t)V4_RS * q.fpc * q.slot_bytes;
+      if (smem4 <= 200 * 1024) {
+        dim3 g4((T + q.fpc - 1) / q.fpc, (unsigned)B);
+        auto launch = [&](auto kern) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+          kern<<<g4, q.ncomp + 32, smem4, avb::as_stream(stream)>>>(q);
+        };
+        auto by_nt = [&](auto nopen_c) {
+          constexpr int NO = decltype(nopen_c)::value;
+          if (NT == 4) launch(k1v4_kernel<4, NO>);
+          else if (NT == 5) launch(k1v4_kernel<5, NO>);
+          else if (NT == 6) launch(k1v4_kernel<6, NO>);
+          else launch(k1v4_kernel<8, NO>);
+        };
+        if (NOPEN == 2) by_nt(std::integral_constant<int, 2>{});
+        else by_nt(std::integral_constant<int, 3>{});
+        const int st = avb::launch_status("avb_rrc_normalize");
+        if (st != AVB_OK || !v4_partial) return st;
+        v4_done = true;
+      }
+    }
+  }
   const bool v2ok = p.fast && (s_h % 4 == 0) && (s_t % 4 == 0) && (s_clip % 4 == 0) &&
                     ((reinterpret_cast<uintptr_t>(src) & 3) == 0) && !getenv("AVB_K1_V1");
   if (v2ok) {
@@ -724,6 +1201,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     q.dst = dst; q.out_dtype = out_dtype; q.out_layout = out_layout; q.tt = tt; q.tph = tph; q.tpw = tpw;
     q.tx_cap = tx_cap; q.ty_cap = ty_cap;
     q.total_bytes = (B - 1) * s_clip + (int64_t)(T - 1) * s_t + (int64_t)(H - 1) * s_h + (int64_t)W * 3;
+    q.only_upscale = v4_done ? 1 : 0;
     q.strips = Wt >= 160 ? 2 : 1;
     q.cps = (Wt + q.strips - 1) / q.strips;
     // worst-case strip source width: every column of a full-width crop
@@ -769,6 +1247,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
       return avb::launch_status("avb_rrc_normalize");
     }
   }
+  p.only_upscale = v4_done ? 1 : 0;
   dim3 grid((Ht + R - 1) / R, T, (unsigned)B);
   AVB_CHECK_ARG(B <= 65535 && T <= 65535, "B and T must be <= 65535");
   k1_rrc_normalize_kernel<<<grid, kThreads, smem, avb::as_stream(stream)>>>(p);

@@ -117,7 +117,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
         counts["n"] += 2  # grad memset + transform
         zero()
         loss.zero_()
-        k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet",
+        k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
            tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
         model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
         reducer.finish()
@@ -218,7 +218,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
                 h2d(slot ^ 1)                      # prefetch the next step's clips
             stream.wait_event(ready[slot])
             nonlocal_frames = dbuf[slot]
-            k1(nonlocal_frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet",
+            k1(nonlocal_frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
                tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
             consumed[slot].record(stream)
             zero()

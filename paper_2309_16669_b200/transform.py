@@ -49,7 +49,7 @@ def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] =
               mean: Sequence[float] = CLIP_MEAN, std: Sequence[float] = CLIP_STD, *,
               out: torch.Tensor | None = None, out_dtype: torch.dtype = torch.bfloat16,
               layout: str = "cthw", channels_last: bool = True, validate: bool = True,
-              tubelet: tuple[int, int, int] = (2, 16, 16)) -> torch.Tensor:
+              tubelet: tuple[int, int, int] = (2, 16, 16), crops_host=None) -> torch.Tensor:
     """Crop -> hflip -> antialiased bilinear -> normalize -> cast, on the GPU.
 
     frames:  uint8 CUDA tensor, [B,T,H,W,3] (channels_last, decoded RGB24) or
@@ -62,6 +62,9 @@ def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] =
     validate: check every box on the host first (needs a host copy of the boxes;
              pass False inside CUDA-graph capture with device boxes -- the kernel
              still skips out-of-frame boxes).
+    crops_host: optional host copy of CUDA `crops` (the sampler's own boxes): used for
+             validation and for the kernel's exact tap envelope without a device->host
+             read.  Without any host copy the kernel assumes the worst-case envelope.
     Returns `out` (layout "cthw" = [B,3,T,Ht,Wt]; "tchw" = [B,T,3,Ht,Wt]; "tubelet" = the
     patch-embed GEMM operand [B*Np, 3*tt*ph*pw] for `tubelet=(tt, ph, pw)`).
     """
@@ -91,7 +94,11 @@ def transform(frames: torch.Tensor, crops, hflip=None, target: tuple[int, int] =
     boxes_host = None
     if isinstance(crops, torch.Tensor) and crops.is_cuda:
         boxes_dev = crops.to(torch.int32).contiguous().view(-1, 4)
-        if validate:
+        if crops_host is not None:
+            boxes_host = _boxes_to_host(crops_host)
+            if boxes_host.shape != tuple(boxes_dev.shape):
+                raise InputError(f"crops_host shape {boxes_host.shape} != crops {tuple(boxes_dev.shape)}")
+        elif validate:
             boxes_host = _boxes_to_host(crops)
     else:
         boxes_host = _boxes_to_host(crops)

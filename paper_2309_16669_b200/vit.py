@@ -429,12 +429,12 @@ class FineTuneModel:
         self.opt = opt or AdamWConfig()
         self.step_num = 0
 
-    def patches_from_clips(self, frames, boxes, flips, out=None):
+    def patches_from_clips(self, frames, boxes, flips, out=None, boxes_host=None):
         from . import transform as TR
 
         cfg = self.cfg
         return TR.transform(frames, boxes, flips, (cfg.height, cfg.width), out=out, layout="tubelet",
-                            tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
+                            tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False, crops_host=boxes_host)
 
     def forward_backward(self, patches: torch.Tensor, labels: torch.Tensor, B: int, loss: torch.Tensor,
                          loss_scale: float | None = None, on_layer_done=None):

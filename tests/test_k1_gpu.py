@@ -130,3 +130,96 @@ def test_full_config2_size_properties():
     # flipping the flip bit mirrors the output columns (up to bf16 rounding of equal values)
     out2 = T.transform(fr, boxes, 1 - flips)
     assert (out2.float() - out.float().flip(-1)).abs().max().item() <= 0.02
+
+
+# ---------------------------------------------------------------- v4 (default streaming kernel) coverage
+class _Env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("Tn", [1, 3, 4])
+def test_v4_matches_v2_and_oracle(Tn):
+    """v4 (default) and v2 (AVB_K1_V2) agree to fp32 rounding; odd T leaves a partial frame group."""
+    B = 5
+    fr = frames_u8(B, Tn, 320, 568, seed=7)
+    boxes, flips = CFG2[8:8 + B, :4], CFG2[8:8 + B, 4]
+    ref = O.transform_batch(fr.numpy(), boxes, flips)
+    d = fr.cuda()
+    o4 = T.transform(d, boxes, flips, out_dtype=torch.float32)
+    with _Env(AVB_K1_V2="1"):
+        o2 = T.transform(d, boxes, flips, out_dtype=torch.float32)
+    assert np.abs(o4.cpu().numpy() - ref).max() <= 1e-3
+    assert (o4 - o2).abs().max().item() <= 2e-5
+
+
+def test_v4_tubelet_layout():
+    B, Tn = 3, 4
+    fr = frames_u8(B, Tn, 320, 568, seed=8)
+    boxes, flips = CFG2[20:20 + B, :4], CFG2[20:20 + B, 4]
+    ref = O.transform_batch(fr.numpy(), boxes, flips)                      # [B,3,T,224,224]
+    tub = T.transform(fr.cuda(), boxes, flips, out_dtype=torch.float32, layout="tubelet", tubelet=(2, 16, 16))
+    # [B, T/2, 14, 14, 3, 2, 16, 16] -> rows (t', py, px), features (c, dt, y, x)
+    r = ref.reshape(B, 3, Tn // 2, 2, 14, 16, 14, 16).transpose(0, 2, 4, 6, 1, 3, 5, 7).reshape(-1, 1536)
+    assert np.abs(tub.cpu().numpy() - r).max() <= 1e-3
+
+
+@pytest.mark.parametrize("H,W,Ht,Wt,box,flip", [
+    (120, 200, 57, 81, (3, 5, 150, 101), 1),     # odd target width (last thread has one column)
+    (90, 180, 30, 64, (1, 2, 171, 87), 0),       # many frames per CTA, ~2.7x down (NT 6)
+    (64, 64, 60, 62, (0, 1, 63, 63), 1),         # barely-downscale
+    (50, 70, 50, 70, (0, 0, 70, 50), 1),         # identity scale (crop == target)
+    (260, 900, 64, 240, (5, 7, 881, 250), 0),    # 3.7x down horizontally (NT 8)
+])
+def test_v4_shapes(H, W, Ht, Wt, box, flip):
+    Tn = 5
+    fr = frames_u8(2, Tn, H, W, seed=9)
+    boxes = np.asarray([box, box], dtype=np.int32)
+    flips = np.asarray([flip, 1 - flip])
+    ref = O.transform_batch(fr.numpy(), boxes, flips, (Ht, Wt))
+    out = T.transform(fr.cuda(), boxes, flips, (Ht, Wt), out_dtype=torch.float32)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+    o16 = T.transform(fr.cuda(), boxes, flips, (Ht, Wt)).float().cpu().numpy()
+    assert np.all(np.abs(o16 - ref) <= bf16_ulp(ref) + 1e-6)
+
+
+def test_v4_strided_view_and_tensor_end():
+    """A sliced (non-contiguous-clip) view; the last row of the last frame ends at the tensor end."""
+    full = frames_u8(4, 3, 300, 410, seed=10)                              # row pitch 1230 = 14 mod 16
+    boxes = np.asarray([[0, 0, 405, 280], [100, 50, 305, 230]], dtype=np.int32)
+    flips = np.asarray([0, 1])
+    fd = full.cuda()
+    for sl in (np.s_[2:4], np.s_[1:3, :, 20:, 5:]):                        # 16B-aligned slice / unaligned view
+        view = full[sl]
+        ref = O.transform_batch(view.numpy(), boxes, flips)
+        out = T.transform(fd[sl], boxes, flips, out_dtype=torch.float32)
+        assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+    tail = frames_u8(1, 2, 230, 300, seed=11)                               # box touches the last byte
+    b2 = np.asarray([[76, 6, 224, 224]], dtype=np.int32)
+    out = T.transform(tail.cuda(), b2, [1], out_dtype=torch.float32)
+    ref = O.transform_batch(tail.numpy(), b2, np.asarray([1]))
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+
+
+def test_v4_device_boxes_mixed_scales():
+    """Device-only boxes (validate=False): v4 takes the downscale clips with the worst-case tap
+    envelope, a complement v2 launch takes the upscale clip; every clip matches the oracle."""
+    fr = frames_u8(3, 3, 320, 568, seed=12)
+    boxes = np.asarray([[65, 15, 392, 303], [300, 200, 150, 100], [0, 0, 568, 320]], dtype=np.int32)
+    flips = np.asarray([1, 0, 1])
+    ref = O.transform_batch(fr.numpy(), boxes, flips)
+    bd = torch.from_numpy(boxes).cuda()
+    fd = torch.from_numpy(flips.astype(np.uint8)).cuda()
+    out = T.transform(fr.cuda(), bd, fd, out_dtype=torch.float32, validate=False)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
