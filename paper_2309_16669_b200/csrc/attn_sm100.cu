@@ -22,6 +22,7 @@
 //   red.global.add.v4.f32 into an fp32 accumulator, converted to bf16 by a tiny kernel.
 #include "tc_common.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace {
@@ -52,6 +53,25 @@ __device__ __forceinline__ float2 f2add(float2 a, float2 b) {
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
   return r;
 }
+// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): round-to-nearest split x = j + f with the
+// 1.5*2^23 magic add, a degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max rel. error 7.5e-5,
+// far below the bf16 rounding of P), and j added straight into the exponent bits.
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c);
+__device__ __forceinline__ float2 f2add(float2 a, float2 b);
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = f2add(x, make_float2(12582912.f, 12582912.f));
+  const float2 j = f2add(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = f2fma(j, make_float2(-1.f, -1.f), x);
+  float2 p = f2fma(f, make_float2(0.055157460272312164f, 0.055157460272312164f),
+                   make_float2(0.24261002242565155f, 0.24261002242565155f));
+  p = f2fma(p, f, make_float2(0.693263590335846f, 0.693263590335846f));
+  p = f2fma(p, f, make_float2(0.9999282360076904f, 0.9999282360076904f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x)),
+                     __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y)));
+}
+
 __device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
   float2 r;
   asm("mul.rn.f32x2 %0, %1, %2;"
@@ -253,30 +273,41 @@ __global__ void __launch_bounds__(320, 2)
           m_run = m_new;
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        // pass 2: p = exp2(s*scale - m), row sum (4 chains), bf16 P packed over the consumed S columns
-        // (P chunk c -> columns [16c, 16c+16), inside S chunk 0 which this thread has already read)
-        float sm4[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t rb[2][32];
-        tc::tmem_ld_32x32b_x32(tS + lane_off, rb[0]);
+        // pass 2: p = exp2(s*scale - m) (3 of every 8 pairs on the FMA pipe, the rest on MUFU), row sum
+        // (2 f32x2 chains), bf16 P packed over the consumed S columns (P chunk c -> columns [16c, 16c+16),
+        // inside S chunk 0 which this thread has already read)
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sl2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-m_use, -m_use);
+        auto pass2 = [&](auto full_tag) {
+          constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-        for (int c = 0; c < FKB / 32; ++c) {
-          tc::tmem_ld_wait();
-          if (c + 1 < FKB / 32) tc::tmem_ld_32x32b_x32(tS + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
-          uint32_t pk[16];
+          for (int c = 0; c < FKB / 32; ++c) {
+            uint32_t rb[1][32];
+            tc::tmem_ld_32x32b_x32(tS + lane_off + c * 32, rb[0]);
+            tc::tmem_ld_wait();
+            uint32_t pk[16];
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int col = c * 32 + e;
-            float p0 = ex2(fmaf(__uint_as_float(rb[c & 1][e]), a.scale_log2, -m_use));
-            float p1 = ex2(fmaf(__uint_as_float(rb[c & 1][e + 1]), a.scale_log2, -m_use));
-            if (!full) {
-              p0 = (col < lim) ? p0 : 0.f;
-              p1 = (col + 1 < lim) ? p1 : 0.f;
+            for (int e2 = 0; e2 < 16; ++e2) {
+              const int col = c * 32 + 2 * e2;
+              const float2 x = f2fma(make_float2(__uint_as_float(rb[0][2 * e2]), __uint_as_float(rb[0][2 * e2 + 1])),
+                                     sl2, nm2);
+              float2 p = ((e2 & 7) >= 5) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+              if (!FULL) {
+                p.x = (col < lim) ? p.x : 0.f;
+                p.y = (col + 1 < lim) ? p.y : 0.f;
+              }
+              sum2[e2 & 1] = f2add(sum2[e2 & 1], p);
+              pk[e2] = pack_bf16x2(p.x, p.y);
             }
-            sm4[(e >> 1) & 3] += p0 + p1;
-            pk[e >> 1] = pack_bf16x2(p0, p1);
+            tc::tmem_st_32x32b_x16(tP + lane_off + c * 16, pk);
           }
-          tc::tmem_st_32x32b_x16(tP + lane_off + c * 16, pk);
-        }
+        };
+        if (__all_sync(0xffffffffu, full))  // tcgen05.ld/st are warp-collective: branch warp-uniformly
+          pass2(std::true_type{});
+        else
+          pass2(std::false_type{});
+        const float2 sm2 = f2add(sum2[0], sum2[1]);
+        const float sm4[4] = {sm2.x, sm2.y, 0.f, 0.f};
         l += (sm4[0] + sm4[1]) + (sm4[2] + sm4[3]);
         tc::tmem_st_wait();
         tc::tc_fence_before();
@@ -326,44 +357,49 @@ struct BwdArgs {
   __nv_bfloat16* dv;
   int64_t ld_g, sb_g;     // strides of dk/dv
   int causal;
+  long long* trace;       // debug: per-step clock64 events of CTA (0,0,0) (AVB_ATTN_TRACE), else null
+  int dbg;                // debug experiment flags (AVB_ATTN_DBG): 1 = skip the dQ drain
 };
 
-// smem (dynamic base must be 1 KB aligned; checked): all 128B-swizzled bf16 tiles first
+// smem (dynamic base must be 1 KB aligned; checked): all 128B-swizzled bf16 tiles first.
+// dS^T is the only tile the compute warps stage in smem (A operand of dK and, seen MN-major, of
+// dQ); once dK/dQ of a step have completed, its buffer doubles as the fp32 staging of that
+// step's dQ drain.
+constexpr int B_QD_STAGES = 3;
 constexpr int B_SK = 0, B_SV = 16384;
-constexpr int B_SQD = 32768;                  // 2 stages x (Q 16K + dO 16K)
-constexpr int B_SPT = B_SQD + 2 * 32768;      // 2 buffers x P^T 32K (also dQ fp32 staging)
-constexpr int B_SDS = B_SPT + 2 * 32768;      // 2 buffers x dS^T 32K
-constexpr int B_SLD = B_SDS + 2 * 32768;      // 2 stages x (lse 512 + delta 512)
-constexpr int B_BAR = B_SLD + 2 * 1024;
-constexpr int B_SMEM = B_BAR + 128;
+constexpr int B_SQD = 32768;                               // 3 stages x (Q 16K + dO 16K)
+constexpr int B_SDS = B_SQD + B_QD_STAGES * 32768;         // 2 buffers x dS^T 32K (then dQ staging)
+constexpr int B_SLD = B_SDS + 2 * 32768;                   // 3 stages x (lse 512 + delta 512)
+constexpr int B_BAR = B_SLD + B_QD_STAGES * 1024;
+constexpr int B_SMEM = B_BAR + 256;
 static_assert(B_SMEM <= 232448, "attn bwd smem");
-constexpr int kBwdCompute = 8;               // compute warps (2 per TMEM lane quadrant)
+constexpr int kBwdCompute = 16;              // compute warps: 4 per TMEM lane quadrant (one 32-query chunk each)
+constexpr int kBwdDrain = 4;                 // dQ drain warps: one per TMEM lane quadrant
+constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
+
+#define BWD_TRACE(ev, ii)                                                                       \
+  do {                                                                                          \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && ii < 32) \
+      a.trace[(ii) * 16 + (ev)] = clock64();                                                      \
+  } while (0)
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// drain one warp's share of the dQ tile (32 query rows x 32 columns) from TMEM through a
-// 128B-swizzled fp32 staging block and reduce-add it into the fp32 accumulator with TMA
-__device__ __forceinline__ void drain_dq(uint32_t taddr, uint8_t* stage, const CUtensorMap* tmDQ, int lane, int c0,
-                                         int q0, int b) {
-  uint32_t r[32];
-  tc::tmem_ld_32x32b_x32(taddr, r);
-  tc::tmem_ld_wait();
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-    *reinterpret_cast<uint4*>(stage + lane * 128 + ((u ^ (lane & 7)) << 4)) =
-        make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
-  tc::fence_proxy_async();
-  __syncwarp();
-  if (lane == 0) {
-    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(tmDQ)),
-                 "r"(smem_u32(stage)), "r"(c0), "r"(q0), "r"(b)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
+__device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
+  return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
 }
 
-__global__ void __launch_bounds__(320, 1)
+// One CTA per (128-key tile, head, clip), 1 CTA/SM, 22 warps.  Per query tile i (TMEM lanes = keys):
+//   MMA warp, after ds_ready(i):   S_{i+1}^T = K Q_{i+1}^T  -> s_full      (compute i+1 starts here)
+//                                  dV += P_i^T dO_i (A = P^T from TMEM) -> pv_done
+//                                  dP_{i+1}^T = V dO_{i+1}^T -> dp_full
+//                                  dK += dS_i^T Q_i;  dQ_i = dS_i K (dS^T smem tile, MN-major) -> mma_done
+//   compute warps 0-15 (quadrant w&3, query chunk w>>2):  P = exp2(S^T*scale*log2e - lse*log2e)
+//        -> bf16 P^T into its own TMEM region (after pv_done of i-1);  dS^T = P (dP^T - delta) -> smem
+//   drain warps 16-19: dQ_i TMEM -> 128B-swizzled fp32 staging (the dS^T_i buffer) -> TMA reduce-add
+//   warp 20 TMA (K, V once; Q/dO/-lse/-delta 3-stage ring), warp 21 MMA.
+// So the exp work of tile i+1 overlaps dV_i / dP_{i+1} / dK_i / dQ_i on the tensor core.
+__global__ void __launch_bounds__(32 * kBwdWarps, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
@@ -372,18 +408,21 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sK = smem + B_SK;
   uint8_t* sV = smem + B_SV;
   uint8_t* sQD = smem + B_SQD;
-  uint8_t* sPT = smem + B_SPT;
   uint8_t* sDS = smem + B_SDS;
   float* sLD = reinterpret_cast<float*>(smem + B_SLD);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_ready = bars + 6;
-  uint64_t* mma_done = bars + 7;
-  uint64_t* dq_free = bars + 8;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* qd_full = bars + 1;                  // [3]
+  uint64_t* qd_empty = bars + 1 + B_QD_STAGES;   // [3]
+  uint64_t* s_full = bars + 1 + 2 * B_QD_STAGES;
+  uint64_t* pv_done = s_full + 1;
+  uint64_t* dp_full = s_full + 2;
+  uint64_t* ds_ready = s_full + 3;
+  uint64_t* mma_done = s_full + 4;
+  uint64_t* dq_free = s_full + 5;
+  uint64_t* stage_free = s_full + 6;             // [2]
+  uint64_t* fin_done = s_full + 8;               // every MMA of the CTA complete (dK / dV final)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -391,7 +430,7 @@ __global__ void __launch_bounds__(320, 1)
   const int nq_all = (a.N + BT - 1) / BT;
   const int i0 = a.causal ? kt : 0;  // first query tile that sees this key tile
   const int nq = nq_all - i0;
-  constexpr int kTMA = kBwdCompute, kMMA = kBwdCompute + 1;
+  constexpr int kDrain0 = kBwdCompute, kTMA = kBwdCompute + kBwdDrain, kMMA = kTMA + 1;
 
   if (warp == kTMA && lane == 0) {
     tc::tma_prefetch(&tmQ);
@@ -400,15 +439,19 @@ __global__ void __launch_bounds__(320, 1)
     tc::tma_prefetch(&tmdO);
     tc::tma_prefetch(&tmDQ);
     tc::mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < B_QD_STAGES; ++s) {
       tc::mbar_init(&qd_full[s], 1);
       tc::mbar_init(&qd_empty[s], 1);
     }
     tc::mbar_init(s_full, 1);
+    tc::mbar_init(pv_done, 1);
+    tc::mbar_init(dp_full, 1);
     tc::mbar_init(ds_ready, kBwdCompute);
     tc::mbar_init(mma_done, 1);
-    tc::mbar_init(&dq_free[0], kBwdCompute);
-    tc::mbar_init(&dq_free[1], kBwdCompute);
+    tc::mbar_init(dq_free, kBwdDrain);
+    tc::mbar_init(&stage_free[0], kBwdDrain);
+    tc::mbar_init(&stage_free[1], kBwdDrain);
+    tc::mbar_init(fin_done, 1);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -416,8 +459,9 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T | dP^T | dV | dK | dQ x2 (double-buffered so dQ(i+1) accumulates while dQ(i) drains)
-  const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384;
+  // TMEM: S^T | dP^T | dV | dK | dQ | P^T (bf16 pairs)
+  const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384,
+                 tPT = tmem + 448;
   const int64_t bh = (int64_t)b * a.H + h;
 
   if (warp == kTMA) {
@@ -426,8 +470,8 @@ __global__ void __launch_bounds__(320, 1)
       tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
       tc::tma_load_3d(sV, &tmV, kv_full, h * HD, kv0, b);
       for (int ii = 0; ii < nq; ++ii) {
-        const int i = i0 + ii, st = ii & 1;
-        tc::mbar_wait(&qd_empty[st], ((ii >> 1) & 1) ^ 1);
+        const int i = i0 + ii, st = ii % B_QD_STAGES;
+        if (ii >= B_QD_STAGES) tc::mbar_wait(&qd_empty[st], ((ii / B_QD_STAGES) - 1) & 1);
         tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
         tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
         tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
@@ -446,165 +490,215 @@ __global__ void __launch_bounds__(320, 1)
   } else if (warp == kMMA) {
     if (lane == 0) {
       constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
-      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: B (dO / Q) MN-major
+      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV (A = P^T in TMEM), dK: B (dO / Q) MN-major
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+      auto issue_s = [&](int ii) {      // S_ii^T = K Q_ii^T
+        const int st = ii % B_QD_STAGES;
+        tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t aQ = smem_u32(sQD + st * 32768);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS,
+                          kk > 0);
+        tc::umma_commit(s_full);
+      };
+      auto issue_dp = [&](int ii) {     // dP_ii^T = V dO_ii^T (qd_full(ii) already observed)
+        const uint32_t aDO = smem_u32(sQD + (ii % B_QD_STAGES) * 32768) + 16384;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::umma_f16_ss(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
+                          idSS, kk > 0);
+        tc::umma_commit(dp_full);
+      };
       tc::mbar_wait(kv_full, 0);
-      for (int ii = 0; ii <= nq; ++ii) {
-        if (ii < nq) {
-          const int st = ii & 1;
-          tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);
-          if (ii > 0) tc::mbar_wait(ds_ready, (ii - 1) & 1);
-          tc::tc_fence_after();
-          const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+      issue_s(0);
+      issue_dp(0);
+      for (int ii = 0; ii < nq; ++ii) {
+        const int st = ii % B_QD_STAGES, pb = ii & 1;
+        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+        const uint32_t aDS = smem_u32(sDS + pb * 32768);
+        const uint32_t acc = (ii > 0) ? 1u : 0u;
+        tc::mbar_wait(ds_ready, ii & 1);   // P_i^T in TMEM, dS_i^T in smem, S_i^T / dP_i^T consumed
+        tc::tc_fence_after();
+        BWD_TRACE(0, ii);
+        if (ii + 1 < nq) issue_s(ii + 1);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::umma_f16_ss(tST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
-                            idSS, kk > 0);
+        for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16)
+          tc::umma_f16_ts(tDV, tPT + 8 * kk, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
+        tc::umma_commit(pv_done);
+        if (ii + 1 < nq) issue_dp(ii + 1);
+        BWD_TRACE(1, ii);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::umma_f16_ss(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
-                            idSS, kk > 0);
-          tc::umma_commit(s_full);
-        } else {
-          tc::mbar_wait(ds_ready, (ii - 1) & 1);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t dS = tc::sdesc_sw128(aDS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          tc::umma_f16_ss(tDK, dS, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
         }
-        if (ii > 0) {
-          const int ps = (ii - 1) & 1;
-          const uint32_t aQ = smem_u32(sQD + ps * 32768), aDO = aQ + 16384;
-          const uint32_t aPT = smem_u32(sPT + ps * 32768), aDS = smem_u32(sDS + ps * 32768);
-          const int use = (ii - 1) >> 1;   // use count of dQ buffer ps
-          if (use > 0) tc::mbar_wait(&dq_free[ps], (use & 1) ^ 1);
-          tc::tc_fence_after();
-          const uint32_t acc = (ii > 1) ? 1u : 0u;
+        if (ii >= 1) tc::mbar_wait(dq_free, (ii - 1) & 1);   // dQ_{i-1} read out of TMEM
+        tc::tc_fence_after();
+        BWD_TRACE(2, ii);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t dP = tc::sdesc_sw128(aPT + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-            tc::umma_f16_ss(tDV, dP, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t dS = tc::sdesc_sw128(aDS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-            tc::umma_f16_ss(tDK, dS, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
-            // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
-            const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
-            tc::umma_f16_ss(tDQ + ps * 64, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
-          }
-          tc::umma_commit(mma_done);
-          tc::umma_commit(&qd_empty[ps]);
+        for (int kk = 0; kk < 8; ++kk) {
+          // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
+          // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
+          const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
+          tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
         }
+        tc::umma_commit(mma_done);
+        tc::umma_commit(&qd_empty[st]);
       }
+      tc::umma_commit(fin_done);
     }
+  } else if (warp >= kDrain0) {
+    // ------------------------------------------------------------ dQ drain warps (one per TMEM lane quadrant)
+    const int quad = warp & 3;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    for (int ii = 0; ii < nq; ++ii) {
+      const int pb = ii & 1;
+      tc::mbar_wait(mma_done, ii & 1);   // dK_i / dQ_i complete: dQ_i final, dS^T_i buffer free
+      tc::tc_fence_after();
+      uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tDQ + lane_off + hh * 32, r);
+        tc::tmem_ld_wait();
+        if (hh == 1) {
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(dq_free);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(stage + hh * 4096 + lane * 128 + ((u ^ (lane & 7)) << 4)) =
+              make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        const int q0 = (i0 + ii) * BT + quad * 32;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&tmDQ)),
+              "r"(smem_u32(stage + hh * 4096)), "r"(h * HD + hh * 32), "r"(q0), "r"(b)
+              : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        tc::mbar_arrive(&stage_free[pb]);   // the buffer may take dS^T_{i+2}
+      }
+      __syncwarp();
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   } else {
     // ------------------------------------------------------------ compute warps
-    // warp w: TMEM lane quadrant (w & 3) -> key rows; column half (w >> 2) of the 128 query columns
-    const int quad = warp & 3, half = warp >> 2;
+    // warp w: TMEM lane quadrant (w & 3) -> key rows; query chunk c = w >> 2 (32 of the 128 columns)
+    const int quad = warp & 3, c = warp >> 2;
     const int row = quad * 32 + lane;
     const int kvi = kv0 + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
     for (int ii = 0; ii < nq; ++ii) {
-      const int i = i0 + ii, st = ii & 1;
+      const int i = i0 + ii, st = ii % B_QD_STAGES;
       const int q0 = i * BT;
-      uint8_t* pt = sPT + st * 32768;
-      uint8_t* ds_t = sDS + st * 32768;
-      if (ii >= 2) {
-        // this warp's 4 KB of the P^T slot staged dQ(ii-2): its TMA reduce must have read it
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
-      }
+      uint8_t* ds_t = sDS + (ii & 1) * 32768;
+      if (warp == 0) BWD_TRACE(4, ii);
       tc::mbar_wait(s_full, ii & 1);
-      tc::mbar_wait(&qd_full[st], (ii >> 1) & 1);  // -lse*log2e / -delta landed
+      tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);  // -lse*log2e / -delta landed
       tc::tc_fence_after();
-      const float* sl = sLD + st * 256;
-      const float* sd = sl + 128;
-#pragma unroll 1
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;
-        uint32_t rs[32], rp[32];
+      if (warp == 0) BWD_TRACE(5, ii);
+      const float* sl = sLD + st * 256 + c * 32;
+      const float* sd = sLD + st * 256 + 128 + c * 32;
+      // warp-uniform: does any element of this 32 x 32 block need masking?
+      const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
+                        (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
+      uint32_t pk[16];
+      {
+        uint32_t rs[32];
         tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
-        tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-        // warp-uniform: does any element of this 32 x 32 block need masking?
-        const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
-                          (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
         tc::tmem_ld_wait();
-        auto body = [&](auto edge_tag) {
+        auto pbody = [&](auto edge_tag) {
           constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
+            const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
+            const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                  make_float2(l1.z, l1.w)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
+              const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
+              float2 p = (e == 3) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+              if (EDGE) {
+                const int qi = q0 + c * 32 + u * 8 + 2 * e;
+                const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+                const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
+                p.x = ok0 ? p.x : 0.f;
+                p.y = ok1 ? p.y : 0.f;
+              }
+              pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
+            }
+          }
+        };
+        if (edge)
+          pbody(std::true_type{});
+        else
+          pbody(std::false_type{});
+      }
+      if (ii >= 1) tc::mbar_wait(pv_done, (ii - 1) & 1);   // dV_{i-1} has read the previous P^T
+      tc::tc_fence_after();
+      tc::tmem_st_32x32b_x16(tPT + lane_off + c * 16, pk);
+      tc::mbar_wait(dp_full, ii & 1);
+      tc::tc_fence_after();
+      if (warp == 0) BWD_TRACE(6, ii);
+      if (ii >= 2) tc::mbar_wait(&stage_free[ii & 1], ((ii - 2) >> 1) & 1);  // dQ_{i-2} staging read out
+      {
+        uint32_t rp[32];
+        tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+        tc::tmem_ld_wait();
+#pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4 l0 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8);
-          const float4 l1 = *reinterpret_cast<const float4*>(sl + c * 32 + u * 8 + 4);
-          const float4 d0 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8);
-          const float4 d1 = *reinterpret_cast<const float4*>(sd + c * 32 + u * 8 + 4);
-          const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                make_float2(l1.z, l1.w)};
+          const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
+          const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
           const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
                                 make_float2(d1.z, d1.w)};
-          uint4 v, w;
-          uint32_t* vp = &v.x;
+          uint4 w;
           uint32_t* wp = &w.x;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
             const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
-            const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
-            float2 p = make_float2(ex2(arg.x), ex2(arg.y));
-            if (EDGE) {
-              const int qi = q0 + c * 32 + u * 8 + 2 * e;
-              const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-              const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
-              p.x = ok0 ? p.x : 0.f;
-              p.y = ok1 ? p.y : 0.f;
-            }
-            const float2 ds = f2mul(p, f2add(dp, nd[e]));   // P (dP - delta); softmax scale folded into dK / dQ
-            vp[e] = pack_bf16x2(p.x, p.y);
+            const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
             wp[e] = pack_bf16x2(ds.x, ds.y);
           }
-          st_sw128(pt, row, c * 4 + u, v);
           st_sw128(ds_t, row, c * 4 + u, w);
         }
-        };
-        if (edge)
-          body(std::true_type{});
-        else
-          body(std::false_type{});
       }
+      tc::tmem_st_wait();
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_ready);
-      if (ii > 0) {
-        // dQ(ii-1): TMEM lanes = query rows of tile i-1; stage into this warp's 4 KB of the P^T slot it no longer needs
-        const int pb = (ii - 1) & 1;
-        tc::mbar_wait(mma_done, (ii - 1) & 1);
-        tc::tc_fence_after();
-        drain_dq(tDQ + pb * 64 + lane_off + half * 32, sPT + pb * 32768 + warp * 4096, &tmDQ, lane,
-                 h * HD + half * 32, q0 - BT + quad * 32, b);
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&dq_free[pb]);
-      }
+      if (warp == 0) BWD_TRACE(7, ii);
     }
-    // last dQ + dK/dV out
-    tc::mbar_wait(mma_done, (nq - 1) & 1);
+    // dK / dV out (softmax scale folded into dK: dS was stored without it).  A dedicated barrier:
+    // these warps skip mma_done phases, so a parity wait on it could be satisfied by an older phase.
+    tc::mbar_wait(fin_done, 0);
     tc::tc_fence_after();
-    drain_dq(tDQ + ((nq - 1) & 1) * 64 + lane_off + half * 32, sPT + ((nq - 1) & 1) * 32768 + warp * 4096, &tmDQ,
-             lane, h * HD + half * 32, (i0 + nq - 1) * BT + quad * 32, b);
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const uint32_t tsrc = which ? tDK : tDV;
-      const float osc = which ? a.scale : 1.f;   // dS was stored without the softmax scale
-      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + half * 32;
-      uint32_t r[32];
-      tc::tmem_ld_32x32b_x32(tsrc + lane_off + half * 32, r);
+      const float osc = which ? a.scale : 1.f;
+      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + c * 16;
+      uint32_t r[16];
+      tc::tmem_ld_32x32b_x16(tsrc + lane_off + c * 16, r);
       tc::tmem_ld_wait();
       if (kvi < a.N) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 2; ++u) {
           uint4 v;
           v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
           v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
@@ -614,8 +708,6 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    __syncwarp();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -636,7 +728,18 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
   const int64_t item = gid >> 3;
   const int sub = gid & 7;
   const int64_t total = (int64_t)B * N * H;
-  if (item >= total) return;
+  if (item >= total) {
+    // padded rows [N, Npad) of every (b, h): delta = lse term = 0, so masked elements stay finite
+    const int64_t pi = gid - total * 8;
+    const int npad = Npad - N;
+    if (pi < (int64_t)B * H * npad) {
+      const int64_t bh = pi / npad;
+      const int64_t r = bh * Npad + N + (pi - bh * npad);
+      delta[r] = 0.f;
+      delta[(int64_t)B * H * Npad + r] = 0.f;
+    }
+    return;
+  }
   const int h = item % H;
   const int64_t bn = item / H;
   const int n = bn % N;
@@ -748,7 +851,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   cudaStream_t st = avb::as_stream(stream);
   const int Npad = (N + BT - 1) / BT * BT;
   {
-    const int64_t threads = (int64_t)B * N * H * 8;
+    const int64_t threads = (int64_t)B * N * H * 8 + (int64_t)B * H * (Npad - N);
     attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(o), ld_o, sb_o, reinterpret_cast<const __nv_bfloat16*>(dout), ld_o,
         sb_o, lse, delta, dq_acc, B, H, N, Npad);
@@ -763,7 +866,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   if ((s = make_maps(&mdo, dout, B, H, N, ld_o, sb_o))) return s;
   CUtensorMap mdq;
   if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
-                                 (uint64_t)N * H * HD, 32, 32, 1)))
+                                 (uint64_t)N * H * HD, 32, 32, 1, 128)))
     return s;
   BwdArgs a;
   a.B = B;
@@ -779,6 +882,9 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.ld_g = ld_g;
   a.sb_g = sb_g;
   a.causal = causal;
+  a.trace = nullptr;
+  if (const char* tr = getenv("AVB_ATTN_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
+  a.dbg = getenv("AVB_ATTN_DBG") ? atoi(getenv("AVB_ATTN_DBG")) : 0;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
@@ -786,7 +892,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     attr = true;
   }
   dim3 grid((N + BT - 1) / BT, H, B);
-  attn_bwd_kernel<<<grid, 32 * (kBwdCompute + 2), B_SMEM, st>>>(mq, mk, mv, mdo, mdq, a);
+  attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, a);
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(

@@ -534,7 +534,7 @@ int make_tmap_2d_bf16_sw(CUtensorMap* map, const void* ptr, uint64_t inner, uint
 }
 
 int make_tmap_3d_f32(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_elems,
-                     uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2) {
+                     uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2, int swizzle_bytes) {
   int s = get_encode();
   if (s) return s;
   cuuint64_t dims[3] = {d0, d1, d2};
@@ -542,7 +542,7 @@ int make_tmap_3d_f32(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1
   cuuint32_t box[3] = {b0, b1, b2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, (swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled(3d f32) failed (%d)", (int)r);

@@ -221,7 +221,7 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 int make_tmap_3d_bf16(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_elems,
                       uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2);
 int make_tmap_3d_f32(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_elems,
-                     uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2);
+                     uint64_t s2_elems, uint32_t b0, uint32_t b1, uint32_t b2, int swizzle_bytes = 128);
 int make_tmap_2d_bf16_sw(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                          uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 }  // namespace avb

@@ -1,0 +1,28 @@
+"""Per-step event timeline of K5 for CTA (0,0,0) on the config-4 shape (AVB_ATTN_TRACE debug hook)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+B, N, H = 64, 1569, 12
+tr = torch.zeros(32 * 16, dtype=torch.int64, device="cuda")
+os.environ["AVB_ATTN_TRACE"] = str(tr.data_ptr())
+from paper_2309_16669_b200 import ops
+D = H * 64
+qkv = (torch.randn(B, N, 3 * D, device="cuda") * 0.5).to(torch.bfloat16)
+q, k, v = qkv[:, :, :D], qkv[:, :, D:2 * D], qkv[:, :, 2 * D:]
+o, lse = ops.attn_fwd(q, k, v, H)
+do = torch.randn_like(o)
+for _ in range(3):
+    ops.attn_bwd(q, k, v, o, do, lse, H)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    ops.attn_bwd(q, k, v, o, do, lse, H)
+e1.record(); torch.cuda.synchronize()
+print("bwd ms", e0.elapsed_time(e1) / 3)
+t = tr.view(32, 16).cpu()
+t0 = int(t[0, 4])
+names = {0: "mma:ds_ready", 1: "mma:S(i+1)issued", 2: "mma:dq_free", 3: "cw0:reduce_read", 4: "cw0:bar_done",
+         5: "cw0:s_full", 6: "cw0:qd_full", 7: "cw0:ds_arrive", 8: "cw0:mma_done", 9: "cw0:drain_issued", 10: "mma:dV_issued"}
+for ii in range(13):
+    print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in range(11) if int(t[ii, e]) != 0))
