@@ -19,6 +19,8 @@
 // restated from PAPER.md:258-260,727).
 #include "tc_common.cuh"
 
+#include <algorithm>
+
 #include <stdlib.h>
 #include <string.h>
 
@@ -26,7 +28,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 384;   // warps 0-3 producer/MMA/alloc/spare, warps 4-11 epilogue
+constexpr int kThreads = 384;   // warps 0-7 epilogue, 8 TMA producer, 9 MMA issuer, 10 TMEM alloc, 11 spare
+// (the scheduler prefers the highest warp id: producer and MMA issuer outrank the epilogue)
+constexpr int kWProd = 8, kWMma = 9, kWAlloc = 10;
 constexpr int kEpiWarps = 8;
 
 struct GemmArgs {
@@ -46,21 +50,23 @@ struct GemmArgs {
   float* rowsum;         // fp32 [M] or null: rowsum[m] += sum_k A[m,k] (the bias gradient of a wgrad)
 };
 
-template <int BN, bool A_MN, bool B_MN, int EK>
+// PAIR: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a 256 x BN tile; each CTA loads its
+// own 128 A rows and half of the BN B rows, so a stage is half as large and the ring twice as deep.
+template <int BN, bool A_MN, bool B_MN, int EK, bool PAIR = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;               // 16 KB
-  static constexpr int B_BYTES = BN * BK * 2;               // 32 KB (BN=256)
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;   // 32 KB (BN=256), 16 KB per CTA of a pair
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? (EK ? 3 : 4) : 6;
+  static constexpr int STAGES = PAIR ? (EK == 0 ? 5 : (EK == 1 ? 4 : 5)) : ((BN == 256) ? (EK ? 3 : 4) : 6);
   // EK 0: plain; 1: bf16 aux read (residual / GELU pre-activation); 2: second bf16 output (BIAS_GELU)
-  static constexpr int SSLOTS = EK == 0 ? 2 : (EK == 1 ? 2 : 4);  // TMA-store staging slots per epilogue warp
+  static constexpr int SSLOTS = EK == 0 ? (PAIR ? 4 : 2) : (EK == 1 ? 2 : 4);  // TMA-store staging slots per epilogue warp
   static constexpr int XSLOTS = EK == 1 ? 3 : 1;                   // TMA-load aux ring slots per epilogue warp
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_BYTES = (SSLOTS + (EK == 1 ? XSLOTS : 0)) * kEpiWarps * 2048;  // 2 KB slots per epilogue warp
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static_assert(SMEM <= 232448, "gemm smem");
-  static constexpr uint32_t IDESC = tc::idesc_bf16_f32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-  static constexpr uint32_t IDESC_RS = tc::idesc_bf16_f32(BM, 16, A_MN ? 1 : 0, 0);   // A x ones[16,K]
+  static constexpr uint32_t IDESC = tc::idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+  static constexpr uint32_t IDESC_RS = tc::idesc_bf16_f32(PAIR ? 2 * BM : BM, 16, A_MN ? 1 : 0, 0);   // A x ones[16,K]
 };
 
 __device__ __forceinline__ void store_row_chunk(const GemmArgs& a, int row, int col, float (&v)[32]) {
@@ -152,6 +158,50 @@ __device__ __forceinline__ void store_aux_chunk(const GemmArgs& a, int row, int 
   }
 }
 
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (a local smem object) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA 2D load into this CTA's smem, completion (tx bytes) signalled on an mbarrier of the pair leader
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_ss_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the same-offset mbarrier in both CTAs of the pair once this thread's MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
 // Stage 32 rows x 32 bf16 (thread = row) into a 64B-swizzled 2 KB block and TMA-store it.
 template <int PENDING>
 __device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap* map, int lane, const float (&v)[32],
@@ -180,11 +230,18 @@ __device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap*
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EK>
+template <int BN, bool A_MN, bool B_MN, int EK, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const GemmArgs a) {
-  using C = Cfg<BN, A_MN, B_MN, EK>;
+  using C = Cfg<BN, A_MN, B_MN, EK, PAIR>;
+  static_assert(!PAIR || BN == 256, "pair mode: BN 256");
+  // pair mode: tiles are 256 rows (num_m counts 256-row blocks), CTA `rank` owns rows 128*rank..
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int ctas = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;   // tile workers (pairs or CTAs)
+  const int cta_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  constexpr int TM = PAIR ? 2 * BM : BM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_epi = smem + C::STAGES * C::STAGE_BYTES;
@@ -208,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::fence_proxy_async();
   }
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kWProd && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
     if (a.tma_out) tc::tma_prefetch(&tmC);
@@ -219,34 +276,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], kEpiWarps);
+      tc::mbar_init(&tempty[s], PAIR ? 2 * kEpiWarps : kEpiWarps);   // pair: both CTAs' epilogues drain
     }
     for (int s = 0; s < kEpiWarps * C::XSLOTS; ++s) tc::mbar_init(&aux_bar[s], 1);
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == kWAlloc) {
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+    }
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == kWProd) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cta_id; t < total; t += ctas) {
         const int mn = t % (a.num_m * a.num_n);
         const int split = t / (a.num_m * a.num_n);
-        const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN;
+        const int m0 = (mn / a.num_n) * TM + (int)rank * BM, n0 = (mn % a.num_n) * BN;
         const int kb0 = split * a.kb_per_split;
         const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           const int k0 = kb * BK;
+          if constexpr (PAIR) {
+            // both CTAs' bytes complete on the leader's full barrier; the leader arms it for both
+            const uint32_t fb = map_rank(&full[stage], 0);
+            if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if (A_MN) {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_cg2(sa + j * 8192, &tmA, fb, m0 + 64 * j, k0);
+            } else {
+              tma_load_2d_cg2(sa, &tmA, fb, k0, m0);
+            }
+            const int nb = n0 + (int)rank * (BN / 2);
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 128; ++j) tma_load_2d_cg2(sb + j * 8192, &tmB, fb, nb + 64 * j, k0);
+            } else {
+              tma_load_2d_cg2(sb, &tmB, fb, k0, nb);
+            }
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           if (A_MN) {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tc::tma_load_2d(sa + j * 8192, &tmA, &full[stage], m0 + 64 * j, k0);
@@ -266,13 +355,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
+  } else if (warp == kWMma) {
+    if (lane == 0 && leader) {
+      // ------------------------------------------------ MMA issuer (pair mode: the leader CTA only)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t da0 = A_MN ? tc::sdesc_sw128(s0, 8192, 1024) : tc::sdesc_sw128(s0, 16, 1024);
+      const uint64_t db0 = B_MN ? tc::sdesc_sw128(s0 + C::A_BYTES, 8192, 1024) : tc::sdesc_sw128(s0 + C::A_BYTES, 16, 1024);
+      for (int t = cta_id; t < total; t += ctas, ++it) {
         const int split = t / (a.num_m * a.num_n);
         const int kb0 = split * a.kb_per_split;
         const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
@@ -286,30 +378,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
-          const uint32_t sb = sa + C::A_BYTES;
+          // descriptors differ only in the start-address field (bits 0-13, 16-byte units)
+          const uint64_t soff = (uint64_t)((stage * C::STAGE_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t da = A_MN ? tc::sdesc_sw128(sa + k * 2048, 8192, 1024) : tc::sdesc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t db = B_MN ? tc::sdesc_sw128(sb + k * 2048, 8192, 1024) : tc::sdesc_sw128(sb + k * 32, 16, 1024);
+            const uint64_t da = da0 + soff + (uint64_t)((A_MN ? k * 2048 : k * 32) >> 4);
+            const uint64_t db = db0 + soff + (uint64_t)((B_MN ? k * 2048 : k * 32) >> 4);
+            if constexpr (PAIR) {
+              umma_f16_ss_cg2(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+              if (do_rs)   // ones tile: each CTA supplies 8 of the 16 B rows (all ones)
+                umma_f16_ss_cg2(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
+                                (kb > kb0 || k > 0) ? 1u : 0u);
+              continue;
+            }
             tc::umma_f16_ss(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
             if (do_rs)
               tc::umma_f16_ss(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
                               (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          tc::umma_commit(&empty[stage]);
+          if (PAIR) umma_commit_pair(&empty[stage]); else tc::umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc::umma_commit(&tfull[acc]);
+        if (PAIR) umma_commit_pair(&tfull[acc]); else tc::umma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < kEpiWarps) {
     // ------------------------------------------------ epilogue
     // warp w: TMEM lane quadrant (w & 3) = rows 32q..32q+31, column half (w-4)/4 of the tile
-    const int ew = warp & 3, eh = (warp - 4) >> 2, ei = warp - 4;
+    const int ew = warp & 3, eh = warp >> 2, ei = warp;
     constexpr int SS = C::SSLOTS, XS = C::XSLOTS;
     constexpr int NCH = BN / 64;                       // 32-column chunks per warp
     uint8_t* stg = smem_epi + ei * SS * 2048;                            // TMA-store staging slots
@@ -320,9 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tma_aux = (EK == 1) && a.tma_aux != 0;
     const uint32_t tlane = (uint32_t)(ew * 32) << 16;
     int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    const uint32_t tempty_leader0 = PAIR ? map_rank(&tempty[0], 0) : 0u;
+    for (int t = cta_id; t < total; t += ctas, ++it) {
       const int mn = t % (a.num_m * a.num_n);
-      const int m0 = (mn / a.num_n) * BM, n0 = (mn % a.num_n) * BN + eh * (BN / 2);
+      const int m0 = (mn / a.num_n) * TM + (int)rank * BM, n0 = (mn % a.num_n) * BN + eh * (BN / 2);
       const int acc = rs_mode ? 0 : (it & 1);
       const uint32_t acc_phase = rs_mode ? (it & 1) : ((it >> 1) & 1);
       const int row0 = m0 + ew * 32;
@@ -426,33 +526,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(tempty_leader0 + acc * 8u); else tc::mbar_arrive(&tempty[acc]);
+      }
     }
   }
 
-  if (warp >= 4 && a.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (warp < kEpiWarps && a.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncwarp();
-  __syncthreads();
-  if (warp == 2) {
+  tc::tc_fence_before();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
+  if (warp == kWAlloc) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, C::TMEM_COLS);
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+    else
+      tc::tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EK>
+template <int BN, bool A_MN, bool B_MN, int EK, bool PAIR = false>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, const CUtensorMap& tx,
            const GemmArgs& a, cudaStream_t st) {
-  using C = Cfg<BN, A_MN, B_MN, EK>;
+  using C = Cfg<BN, A_MN, B_MN, EK, PAIR>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EK, PAIR>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return avb::cuda_status(e, "gemm: set smem attribute");
+    if (PAIR) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      (void)e;
+    }
     attr = true;
   }
   const int total = a.num_m * a.num_n * a.splits;
-  const int grid = total < avb::sm_count() ? total : avb::sm_count();
-  gemm_kernel<BN, A_MN, B_MN, EK><<<grid, kThreads, C::SMEM, st>>>(ta, tb, tcm, tx, a);
+  if (!PAIR) {
+    const int grid = total < avb::sm_count() ? total : avb::sm_count();
+    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, tcm, tx, a);
+    return avb::launch_status("avb_gemm");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr2[1];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;
+  attr2[0].val.clusterDim.x = 2;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 1;
+  // persistent pairs: as many as can be co-resident (a TPC with a harvested SM hosts no pair)
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cfg.gridDim = dim3(avb::sm_count(), 1, 1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
+      (void)cudaGetLastError();
+      n = avb::sm_count() / 2;
+    }
+    max_pairs = n;
+  }
+  const int pairs = std::min(total, max_pairs);
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tx, a);
+  if (e != cudaSuccess) return avb::cuda_status(e, "avb_gemm (pair launch)");
   return avb::launch_status("avb_gemm");
 }
 
@@ -576,6 +716,8 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   AVB_CHECK_ARG(!a_rowsum || (reinterpret_cast<uintptr_t>(a_rowsum) & 3) == 0, "a_rowsum must be 4-byte aligned");
 
   const int BN = (N <= 128) ? 128 : 256;
+  // CTA pairs (cta_group::2, 256 x 256 tiles) for the large-M forward / dgrad shapes
+  const bool pair = BN == 256 && M > 128 && !getenv("AVB_GEMM_NO_PAIR");
   CUtensorMap ta, tb;
   int s;
   if (a_major == 0)
@@ -584,7 +726,7 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
     s = avb::make_tmap_2d_bf16(&ta, A, M, K, lda, 64, 64);
   if (s) return s;
   if (b_major == 0)
-    s = avb::make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, BN);
+    s = avb::make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, pair ? BN / 2 : BN);
   else
     s = avb::make_tmap_2d_bf16(&tb, B, N, K, ldb, 64, 64);
   if (s) return s;
@@ -602,7 +744,7 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   g.aux_out = aux_out;
   g.alpha = alpha;
   g.rowsum = a_rowsum;
-  g.num_m = (M + BM - 1) / BM;
+  g.num_m = (M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   g.num_n = (N + BN - 1) / BN;
   g.num_kb = (K + BK - 1) / BK;
   int splits = split_k;
@@ -635,6 +777,22 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   // aux / store rings so TMA latency is covered while the epilogue streams 32-column chunks
   const bool heavy = BN == 256 && a_major == 0 && (g.tma_aux || (g.tma_out && epilogue == AVB_EPI_BIAS_GELU)) &&
                      !getenv("AVB_GEMM_NO_HEAVY");
+  if (pair) {
+    if (heavy && g.tma_aux) {
+      if (b_major == 0) return launch<256, false, false, 1, true>(ta, tb, tcm, tx, g, st);
+      return launch<256, false, true, 1, true>(ta, tb, tcm, tx, g, st);
+    }
+    if (heavy) {
+      if (b_major == 0) return launch<256, false, false, 2, true>(ta, tb, tcm, tx, g, st);
+      return launch<256, false, true, 2, true>(ta, tb, tcm, tx, g, st);
+    }
+    switch ((a_major << 1) | b_major) {
+      case 0: return launch<256, false, false, 0, true>(ta, tb, tcm, tx, g, st);
+      case 1: return launch<256, false, true, 0, true>(ta, tb, tcm, tx, g, st);
+      case 2: return launch<256, true, false, 0, true>(ta, tb, tcm, tx, g, st);
+      default: return launch<256, true, true, 0, true>(ta, tb, tcm, tx, g, st);
+    }
+  }
   if (heavy) {
     if (g.tma_aux) {
       if (b_major == 0) return launch<256, false, false, 1>(ta, tb, tcm, tx, g, st);

@@ -176,7 +176,10 @@ def wgrad_split(m_out: int, n_out: int, k_tokens: int | None = None, sms: int = 
     The fused bias-gradient mode runs a single-buffered accumulator, so every extra work item
     per CTA pays its fp32 reduce epilogue (~35 k-block equivalents) un-overlapped.
     """
-    tiles = ((m_out + 127) // 128) * ((n_out + 255) // 256 if n_out > 128 else 1)
+    if n_out > 128 and m_out > 128:   # CTA-pair GEMM: 256 x 256 tiles, one worker per SM pair
+        tiles, sms = ((m_out + 255) // 256) * ((n_out + 255) // 256), sms // 2
+    else:
+        tiles = ((m_out + 127) // 128) * ((n_out + 255) // 256 if n_out > 128 else 1)
     if k_tokens is None:
         return max(1, sms // tiles)
     kb = (k_tokens + 63) // 64

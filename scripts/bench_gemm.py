@@ -10,11 +10,14 @@ shapes = [  # name, M, N, K, a_mn, b_mn, epi
     ("qkv_fwd", M, 3 * D, D, False, False, ops.EPI_BF16),
     ("proj_fwd", M, D, D, False, False, ops.EPI_BF16),
     ("fc1_fwd", M, 4 * D, D, False, False, ops.EPI_BF16),
+    ("fc1_fwd_gelu", M, 4 * D, D, False, False, ops.EPI_BIAS_GELU),
+    ("fc2_dgrad_dgelu", M, 4 * D, D, False, True, ops.EPI_DGELU),
     ("fc2_fwd", M, D, 4 * D, False, False, ops.EPI_BF16),
     ("fc1_dgrad", M, D, 4 * D, False, True, ops.EPI_BF16),
     ("fc2_dgrad", M, 4 * D, D, False, True, ops.EPI_BF16),
     ("fc1_wgrad", 4 * D, D, M, True, True, ops.EPI_F32_ACCUM),
     ("qkv_wgrad", 3 * D, D, M, True, True, ops.EPI_F32_ACCUM),
+    ("proj_wgrad", D, D, M, True, True, ops.EPI_F32_ACCUM),
     ("sq8192", 8192, 8192, 8192, False, False, ops.EPI_BF16),
 ]
 res = []
@@ -24,9 +27,14 @@ for name, m, n, k, amn, bmn, epi in shapes:
     out = torch.zeros((m, n), device="cuda", dtype=torch.float32 if epi == ops.EPI_F32_ACCUM else torch.bfloat16)
     split = 1
     if epi == ops.EPI_F32_ACCUM:
-        tiles = ((m + 127) // 128) * ((n + 255) // 256)
-        split = max(1, 148 // tiles)
-    f = lambda: ops.gemm(A, B, a_mn=amn, b_mn=bmn, out=out, epilogue=epi, split_k=split)
+        from paper_2309_16669_b200.vit import wgrad_split
+        split = wgrad_split(m, n, k)
+    kw = {}
+    if epi == ops.EPI_BIAS_GELU:
+        kw = dict(bias=torch.randn(n, device="cuda"), aux_out=torch.empty((m, n), device="cuda", dtype=torch.bfloat16))
+    if epi == ops.EPI_DGELU:
+        kw = dict(aux=torch.randn((m, n), device="cuda").to(torch.bfloat16))
+    f = lambda: ops.gemm(A, B, a_mn=amn, b_mn=bmn, out=out, epilogue=epi, split_k=split, **kw)
     for _ in range(3): f()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -4,7 +4,7 @@ import torch
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 from test_attn_gpu import packed, ref_attn, rel
 from paper_2309_16669_b200 import ops
-for (B, N, H) in [(2, 300, 1)] * 12 + [(2, 197, 3)] * 6:
+for (B, N, H) in [(1, 128, 1), (2, 197, 3), (2, 300, 1), (1, 1569, 2), (2, 300, 1), (2, 785, 2)]:
     qkv = packed(B, N, H, seed=7 + N)
     q, k, v = (qkv[:, :, i].contiguous() for i in range(3))
     D = H * 64

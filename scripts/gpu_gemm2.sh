@@ -1,4 +1,6 @@
-set -x
-timeout 300 python -m pytest tests/test_gemm_gpu.py tests/test_model_gpu.py -x -q 2>&1 | tail -5
-timeout 300 python scripts/bench_gemm.py 2>&1 | tail -12
-timeout 900 python bench.py --workload train --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -2
+python - <<'PY'
+import torch, ctypes
+print("SMs", torch.cuda.get_device_properties(0).multi_processor_count)
+PY
+timeout 240 python -m pytest tests/test_gemm_gpu.py -x -q 2>&1 | tail -2
+timeout 240 python scripts/bench_gemm.py 2>&1 | tail -13 | cut -c1-140

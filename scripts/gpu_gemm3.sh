@@ -1,4 +1,4 @@
-set -x
-timeout 300 python -m pytest tests/test_gemm_gpu.py tests/test_model_gpu.py -x -q 2>&1 | tail -5
-timeout 900 python bench.py --workload train --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step']); print(json.dumps(d['gemm_shapes'])); print(json.dumps(d['kernels']))"
+timeout 240 python -m pytest tests/test_gemm_gpu.py -x -q 2>&1 | tail -2
+timeout 240 python scripts/bench_gemm.py 2>&1 | tail -13 | cut -c1-125
+echo NOPAIR
+AVB_GEMM_NO_PAIR=1 timeout 240 python scripts/bench_gemm.py 2>&1 | grep -E "qkv_fwd|sq8192|fc2_fwd|wgrad" | cut -c1-110

@@ -21,8 +21,8 @@ for _ in range(3):
 e1.record(); torch.cuda.synchronize()
 print("bwd ms", e0.elapsed_time(e1) / 3)
 t = tr.view(32, 16).cpu()
-t0 = int(t[0, 4])
-names = {0: "mma:ds_ready", 1: "mma:S(i+1)issued", 2: "mma:dq_free", 3: "cw0:reduce_read", 4: "cw0:bar_done",
-         5: "cw0:s_full", 6: "cw0:qd_full", 7: "cw0:ds_arrive", 8: "cw0:mma_done", 9: "cw0:drain_issued", 10: "mma:dV_issued"}
+t0 = int(t[0, 9])
+names = {0: "m:p_rdy", 1: "m:dV_iss", 2: "m:ds_rdy", 3: "m:dK_iss", 4: "m:dPS_iss", 9: "c:top", 5: "c:s_full",
+         6: "c:p_arr", 7: "c:dp_full", 8: "c:ds_arr"}
 for ii in range(13):
-    print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in range(11) if int(t[ii, e]) != 0))
+    print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in (9, 5, 6, 0, 1, 7, 8, 2, 3, 4) if int(t[ii, e]) != 0))
