@@ -38,6 +38,20 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed `ncu --set full` capture
+    (profiles/r01/traffic.json, written by scripts/traffic_from_ncu.py), or None."""
+    try:
+        with open(TRAFFIC_PATH) as fh:
+            ent = json.load(fh).get(kernel)
+        return None if ent is None else float(ent["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def peaks() -> tuple[dict, str]:
     try:
         with open(PEAKS_PATH) as fh:
@@ -230,7 +244,7 @@ def run_augment(args, rank, world, local):
         "config": {"workload": "configs[1] fused GPU augmentation", "clips_per_gpu": B, "frames": AUG_T,
                    "src_hw": [AUG_H, AUG_W], "target_hw": [224, 224], "l2": "input 558 MB > 126 MB L2 (no flush)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": src,
+                     "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic("k1_rrc_normalize"), "peak_source": src,
                      "algorithmic_bytes_per_launch": algo},
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "clips/s",
                 "h2d_bytes_per_step": int(host.numel()), "d2h_bytes_per_step": int(res.numel() * 4)},

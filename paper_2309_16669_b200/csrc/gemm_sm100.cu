@@ -744,7 +744,7 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   g.aux_out = aux_out;
   g.alpha = alpha;
   g.rowsum = a_rowsum;
-  g.num_m = (M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
+  g.num_m = (M + BM - 1) / BM;   // pair mode re-derives it below
   g.num_n = (N + BN - 1) / BN;
   g.num_kb = (K + BK - 1) / BK;
   int splits = split_k;
@@ -777,11 +777,8 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   // aux / store rings so TMA latency is covered while the epilogue streams 32-column chunks
   const bool heavy = BN == 256 && a_major == 0 && (g.tma_aux || (g.tma_out && epilogue == AVB_EPI_BIAS_GELU)) &&
                      !getenv("AVB_GEMM_NO_HEAVY");
-  if (pair) {
-    if (heavy && g.tma_aux) {
-      if (b_major == 0) return launch<256, false, false, 1, true>(ta, tb, tcm, tx, g, st);
-      return launch<256, false, true, 1, true>(ta, tb, tcm, tx, g, st);
-    }
+  if (pair && !(heavy && g.tma_aux)) {   // aux-reading epilogues keep single-CTA tiles (measured faster)
+    g.num_m = (M + 2 * BM - 1) / (2 * BM);
     if (heavy) {
       if (b_major == 0) return launch<256, false, false, 2, true>(ta, tb, tcm, tx, g, st);
       return launch<256, false, true, 2, true>(ta, tb, tcm, tx, g, st);
@@ -792,6 +789,9 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
       case 2: return launch<256, true, false, 0, true>(ta, tb, tcm, tx, g, st);
       default: return launch<256, true, true, 0, true>(ta, tb, tcm, tx, g, st);
     }
+  }
+  if (pair && b_major == 0) {   // single-CTA fallback of a pair-eligible launch: full-height B boxes
+    if ((s = avb::make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, BN))) return s;
   }
   if (heavy) {
     if (g.tma_aux) {

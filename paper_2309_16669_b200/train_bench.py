@@ -61,6 +61,13 @@ def golden_boxes(n: int, offset: int = 0):
     return np.ascontiguousarray(g[idx, :4]), np.ascontiguousarray(g[idx, 4].astype(np.uint8))
 
 
+def traffic(kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture (or None)."""
+    import bench  # noqa: the driver script's helper (profiles/r01/traffic.json)
+
+    return bench.ncu_traffic(kernel)
+
+
 def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, large: bool = False):
     """large=False: configs[3] ViT-B/16 (64 clips/GPU); large=True: configs[4] ViT-L/14 (24 clips/GPU)."""
     cfg = CONFIG5_VIT_L_16F if large else CONFIG4_VIT_B_16F
@@ -183,7 +190,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     else:
         ach = kern[dom]["tflops"]
     roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_tflops_sustained"],
-            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": None,
+            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": traffic(dom),
             "share_of_step": cands[dom] / args.steps / ms,
             "algorithmic_flops_per_launch": (att_b if dom == "attn_bwd" else att_f if dom == "attn_fwd" else None),
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
