@@ -267,7 +267,14 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
         "gpu_launches": launches // max(1, args.steps) * args.steps,
         "clocks": clocks,
         "loss": float(loss_h.item()),
+        "memory": {"peak_bytes": int(torch.cuda.max_memory_allocated()), "clips_per_gpu": B},
     }
+    try:  # the reference planners fed with this measurement
+        from .perf_models import b200_report
+
+        line["pipeline_model"] = b200_report({"value": line["value"], "n_gpus": world, "memory": line["memory"]}, cfg)
+    except Exception as e:  # noqa: BLE001 -- a planner failure must not void the measurement
+        line["pipeline_model"] = f"unavailable: {e}"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import vit_oracle as VO
 
