@@ -995,6 +995,65 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   }
 }
 
+// K1 identity: the reference's fused-decode path (decoder.py:137-211,
+// PAPER.md:666-668) hands over frames the CPU already cropped and scaled to the target -- the
+// planar Batch.frames layout [B,T,3,Ht,Wt] (loader.py:99-116).  Full-frame boxes at identity scale
+// reduce K1 to flip + normalize + cast + re-layout: one thread per 16 pixels of one channel row,
+// one 16-byte load, two 16-byte bf16 stores (16 output columns are contiguous in every layout).
+__global__ void __launch_bounds__(256) k1_identity_kernel(const K1Params p, int64_t nchunks) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= nchunks) return;
+  const int cpr = p.Wt >> 4;                        // 16-pixel chunks per row
+  const int xc = (int)(gid % cpr);
+  int64_t r = gid / cpr;                            // ((b*T + t)*3 + c)*Ht + y
+  const int y = (int)(r % p.Ht);
+  r /= p.Ht;
+  const int c = (int)(r % 3);
+  r /= 3;
+  const int t = (int)(r % p.T);
+  const int64_t b = r / p.T;
+  const bool flip = p.flips ? (p.flips[b] != 0) : false;
+  const int x0 = flip ? p.Wt - 16 * (xc + 1) : 16 * xc;   // source chunk (mirrored when flipped)
+  const uint8_t* src = p.src + b * p.s_clip + (int64_t)t * p.s_t + (int64_t)c * p.s_c + (int64_t)y * p.s_h + x0;
+  uint4 v = *reinterpret_cast<const uint4*>(src);
+  if (flip) {  // reverse the 16 bytes
+    const uint32_t w0 = __byte_perm(v.w, 0, 0x0123), w1 = __byte_perm(v.z, 0, 0x0123),
+                   w2 = __byte_perm(v.y, 0, 0x0123), w3 = __byte_perm(v.x, 0, 0x0123);
+    v = make_uint4(w0, w1, w2, w3);
+  }
+  const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+  const float sc = p.scale[c], bi = p.bias[c];
+  float f[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) f[k] = fmaf((float)((wd[k >> 2] >> (8 * (k & 3))) & 0xffu), sc, bi);
+  const int j = 16 * xc;
+  int64_t o;
+  const int64_t plane = (int64_t)p.Ht * p.Wt;
+  if (p.out_layout == AVB_LAYOUT_CTHW) {
+    o = ((b * 3 + c) * p.T + t) * plane + (int64_t)y * p.Wt + j;
+  } else if (p.out_layout == AVB_LAYOUT_TCHW) {
+    o = ((b * p.T + t) * 3 + c) * plane + (int64_t)y * p.Wt + j;
+  } else {
+    const int npy = p.Ht / p.tph, npx = p.Wt / p.tpw;
+    const int64_t Np = (int64_t)(p.T / p.tt) * npy * npx;
+    const int F = 3 * p.tt * p.tph * p.tpw;
+    o = (b * Np + ((int64_t)(t / p.tt) * npy + y / p.tph) * npx + j / p.tpw) * F +
+        ((c * p.tt + t % p.tt) * p.tph + y % p.tph) * p.tpw + j % p.tpw;
+  }
+  if (p.out_dtype == AVB_DTYPE_BF16) {
+    uint4 lo, hi;
+    lo.x = pack_bf16x2(f[0], f[1]); lo.y = pack_bf16x2(f[2], f[3]); lo.z = pack_bf16x2(f[4], f[5]); lo.w = pack_bf16x2(f[6], f[7]);
+    hi.x = pack_bf16x2(f[8], f[9]); hi.y = pack_bf16x2(f[10], f[11]); hi.z = pack_bf16x2(f[12], f[13]); hi.w = pack_bf16x2(f[14], f[15]);
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.dst) + o);
+    d[0] = lo;
+    d[1] = hi;
+  } else {
+    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.dst) + o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+  }
+}
+
 // Host-side envelope for v4, in the exact-integer tap ranges of k1_taps: the most taps of any output
 // column (nt) and the most output rows whose vertical windows share one source row (nopen).
 static void k1_range(int crop, int tgt, int i, int& lo, int& hi) {
@@ -1133,6 +1192,21 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     cudaFuncSetAttribute(k1_rrc_normalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k1v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
+  }
+  // identity: full-frame boxes at the target size, planar rows (the fused-decode hand-off)
+  if (boxes_host && H == Ht && W == Wt && s_w == 1 && Wt % 16 == 0 && !getenv("AVB_K1_NO_IDENTITY") &&
+      (out_layout != AVB_LAYOUT_TUBELET || tpw % 16 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+      s_h % 16 == 0 && s_c % 16 == 0 && s_t % 16 == 0 && s_clip % 16 == 0 &&
+      ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    bool ident = true;
+    for (int64_t i = 0; i < B && ident; ++i)
+      ident = boxes_host[4 * i] == 0 && boxes_host[4 * i + 1] == 0 && boxes_host[4 * i + 2] == W &&
+              boxes_host[4 * i + 3] == H;
+    if (ident) {
+      const int64_t nchunks = B * (int64_t)T * 3 * Ht * (Wt / 16);
+      k1_identity_kernel<<<(unsigned)((nchunks + 255) / 256), 256, 0, avb::as_stream(stream)>>>(p, nchunks);
+      return avb::launch_status("avb_rrc_normalize (identity)");
+    }
   }
   // v4: streaming kernel for interleaved RGB downscales (every config-2 crop).  With host boxes
   //     the tap envelope is exact; with device-only boxes it is the worst case over every

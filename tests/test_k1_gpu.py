@@ -223,3 +223,29 @@ def test_v4_device_boxes_mixed_scales():
     fd = torch.from_numpy(flips.astype(np.uint8)).cuda()
     out = T.transform(fr.cuda(), bd, fd, out_dtype=torch.float32, validate=False)
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+
+
+@pytest.mark.parametrize("layout", ["cthw", "tchw", "tubelet"])
+def test_identity_planar_fused_decode_handoff(layout):
+    """CPU fused decode already cropped/scaled to 224^2 -> [B,T,3,224,224] uint8
+    (reference Batch.frames); K1's identity kernel only flips, normalizes, casts and re-lays out."""
+    B, Tn = 3, 4
+    fr = frames_u8(B, Tn, 224, 224, seed=13)                                 # [B,T,H,W,3]
+    planar = fr.permute(0, 1, 4, 2, 3).contiguous()                          # [B,T,3,H,W]
+    boxes = np.asarray([[0, 0, 224, 224]] * B, dtype=np.int32)
+    flips = np.asarray([0, 1, 1])
+    ref = O.transform_batch(fr.numpy(), boxes, flips)                        # [B,3,T,224,224]
+    kw = dict(layout=layout, channels_last=False)
+    if layout == "tubelet":
+        kw["tubelet"] = (2, 16, 16)
+        ref = ref.reshape(B, 3, Tn // 2, 2, 14, 16, 14, 16).transpose(0, 2, 4, 6, 1, 3, 5, 7).reshape(-1, 1536)
+    elif layout == "tchw":
+        ref = ref.transpose(0, 2, 1, 3, 4)
+    o32 = T.transform(planar.cuda(), boxes, flips, out_dtype=torch.float32, **kw).cpu().numpy()
+    assert np.abs(o32 - ref).max() <= 1e-3
+    o16 = T.transform(planar.cuda(), boxes, flips, **kw).float().cpu().numpy()
+    assert np.all(np.abs(o16 - ref) <= bf16_ulp(ref) + 1e-6)
+    # byte-exact gather through the identity path: recover the source bytes
+    back = T.transform(planar.cuda(), boxes, None, mean=(0, 0, 0), std=(1, 1, 1), out_dtype=torch.float32,
+                       channels_last=False)
+    assert np.array_equal(np.rint(back.cpu().numpy() * 255.0), fr.numpy().transpose(0, 4, 1, 2, 3))
