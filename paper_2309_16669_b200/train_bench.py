@@ -190,7 +190,8 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     else:
         ach = kern[dom]["tflops"]
     roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_tflops_sustained"],
-            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": traffic(dom),
+            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"],
+            "traffic": None if large else traffic(dom),   # the committed capture is of the config-4 shape
             "share_of_step": cands[dom] / args.steps / ms,
             "algorithmic_flops_per_launch": (att_b if dom == "attn_bwd" else att_f if dom == "attn_fwd" else None),
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
