@@ -426,7 +426,11 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   uint64_t* dq_free = s_full + 5;
   uint64_t* stage_free = s_full + 6;             // [2]
   uint64_t* fin_done = s_full + 8;               // every MMA of the CTA complete (dK / dV final)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
+  uint64_t* s_free = s_full + 9;                 // S_i^T read into registers by every compute warp
+  uint64_t* p_ready = s_full + 10;               // P_i^T stored in TMEM by every compute warp
+  uint64_t* dp_free = s_full + 11;               // dP_i^T read into registers by every compute warp
+  uint64_t* kv_tmem = s_full + 12;               // K and V copied into TMEM (A operands of S^T / dP^T)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -456,6 +460,10 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     tc::mbar_init(&stage_free[0], kBwdDrain);
     tc::mbar_init(&stage_free[1], kBwdDrain);
     tc::mbar_init(fin_done, 1);
+    tc::mbar_init(s_free, kBwdCompute);
+    tc::mbar_init(p_ready, kBwdCompute);
+    tc::mbar_init(dp_free, kBwdCompute);
+    tc::mbar_init(kv_tmem, 4);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -464,8 +472,9 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM: S^T | dP^T | dV | dK | dQ | P^T (bf16 pairs)
+  // TMEM: S^T (P^T packed over it) | dP^T (dS^T packed over it) | dV | dK | dQ | K | V (bf16 pairs)
   const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384,
-                 tPT = tmem + 448;
+                 tK = tmem + 448, tV = tmem + 480;
   const int64_t bh = (int64_t)b * a.H + h;
 
   if (warp == kTMA) {
@@ -497,26 +506,25 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV (A = P^T in TMEM), dK: B (dO / Q) MN-major
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto issue_s = [&](int ii) {      // S_ii^T = K Q_ii^T
+      auto issue_s = [&](int ii) {      // S_ii^T = K Q_ii^T, K (A) from TMEM
         const int st = ii % B_QD_STAGES;
         tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);
         tc::tc_fence_after();
         const uint32_t aQ = smem_u32(sQD + st * 32768);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tST, tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS,
-                          kk > 0);
+          tc::umma_f16_ts(tST, tK + 8 * kk, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
         tc::umma_commit(s_full);
       };
-      auto issue_dp = [&](int ii) {     // dP_ii^T = V dO_ii^T (qd_full(ii) already observed)
+      auto issue_dp = [&](int ii) {     // dP_ii^T = V dO_ii^T, V (A) from TMEM (qd_full(ii) already observed)
         const uint32_t aDO = smem_u32(sQD + (ii % B_QD_STAGES) * 32768) + 16384;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
-                          idSS, kk > 0);
+          tc::umma_f16_ts(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
         tc::umma_commit(dp_full);
       };
-      tc::mbar_wait(kv_full, 0);
+      tc::mbar_wait(kv_tmem, 0);          // K, V in TMEM (compute warps 0-3 copied them)
+      tc::tc_fence_after();
       issue_s(0);
       issue_dp(0);
       for (int ii = 0; ii < nq; ++ii) {
@@ -524,21 +532,24 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
         const uint32_t aDS = smem_u32(sDS + pb * 32768);
         const uint32_t acc = (ii > 0) ? 1u : 0u;
-        tc::mbar_wait(ds_ready, ii & 1);   // P_i^T in TMEM, dS_i^T in smem, S_i^T / dP_i^T consumed
+        // P_i^T lives over S_i^T and dS_i^T over dP_i^T (packed bf16, TMEM): dV_i / dK_i read them
+        // before S_{i+1} / dP_{i+1} overwrite those columns (tcgen05.mma executes in issue order)
+        tc::mbar_wait(p_ready, ii & 1);
         tc::tc_fence_after();
         BWD_TRACE(0, ii);
-        if (ii + 1 < nq) issue_s(ii + 1);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16)
-          tc::umma_f16_ts(tDV, tPT + 8 * kk, tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-        tc::umma_commit(pv_done);
-        if (ii + 1 < nq) issue_dp(ii + 1);
+        for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16) = chunk kk/2
+          tc::umma_f16_ts(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG,
+                          (acc | kk) ? 1u : 0u);
+        if (ii + 1 < nq) issue_s(ii + 1);
+        tc::mbar_wait(ds_ready, ii & 1);
+        tc::tc_fence_after();
         BWD_TRACE(1, ii);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t dS = tc::sdesc_sw128(aDS + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
-          tc::umma_f16_ss(tDK, dS, tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < 8; ++kk)     // dK += dS^T Q (A = dS^T from TMEM)
+          tc::umma_f16_ts(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG,
+                          (acc | kk) ? 1u : 0u);
+        if (ii + 1 < nq) issue_dp(ii + 1);
         if (ii >= 1) tc::mbar_wait(dq_free, (ii - 1) & 1);   // dQ_{i-1} read out of TMEM
         tc::tc_fence_after();
         BWD_TRACE(2, ii);
@@ -562,6 +573,14 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       const int pb = ii & 1;
       tc::mbar_wait(mma_done, ii & 1);   // dK_i / dQ_i complete: dQ_i final, dS^T_i buffer free
       tc::tc_fence_after();
+      if (a.dbg & 1) {
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(dq_free);
+          tc::mbar_arrive(&stage_free[pb]);
+        }
+        continue;
+      }
       uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -605,6 +624,26 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     const int kvi = kv0 + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
+    if (c == 0) {
+      // K and V rows of this quadrant -> TMEM (bf16 pairs, 32 columns each): the A operands of
+      // S^T = K Q^T and dP^T = V dO^T, so those MMAs read only Q / dO from shared memory
+      tc::mbar_wait(kv_full, 0);
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        const uint8_t* src = (which ? sV : sK) + row * 128;
+        uint32_t r[32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint4 q = *reinterpret_cast<const uint4*>(src + ((u ^ (row & 7)) << 4));
+          r[4 * u] = q.x; r[4 * u + 1] = q.y; r[4 * u + 2] = q.z; r[4 * u + 3] = q.w;
+        }
+        tc::tmem_st_32x32b_x32((which ? tV : tK) + lane_off, r);
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(kv_tmem);
+    }
     for (int ii = 0; ii < nq; ++ii) {
       const int i = i0 + ii, st = ii % B_QD_STAGES;
       const int q0 = i * BT;
@@ -622,8 +661,13 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       uint32_t pk[16];
       {
         uint32_t rs[32];
-        tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
-        tc::tmem_ld_wait();
+        if (a.dbg & 4) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) rs[e] = __float_as_uint((float)(lane + e) * -0.01f);
+        } else {
+          tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
+          tc::tmem_ld_wait();
+        }
         auto pbody = [&](auto edge_tag) {
           constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
@@ -653,17 +697,24 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         else
           pbody(std::false_type{});
       }
-      if (ii >= 1) tc::mbar_wait(pv_done, (ii - 1) & 1);   // dV_{i-1} has read the previous P^T
-      tc::tc_fence_after();
-      tc::tmem_st_32x32b_x16(tPT + lane_off + c * 16, pk);
+      if (!(a.dbg & 4)) tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over this warp's consumed S^T chunk
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_ready);
       tc::mbar_wait(dp_full, ii & 1);
       tc::tc_fence_after();
       if (warp == 0) BWD_TRACE(6, ii);
       if (ii >= 2) tc::mbar_wait(&stage_free[ii & 1], ((ii - 2) >> 1) & 1);  // dQ_{i-2} staging read out
       {
-        uint32_t rp[32];
-        tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-        tc::tmem_ld_wait();
+        uint32_t rp[32], dsk[16];
+        if (a.dbg & 4) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) rp[e] = __float_as_uint((float)(lane - e) * 0.01f);
+        } else {
+          tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+          tc::tmem_ld_wait();
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
@@ -677,9 +728,11 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
             const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
             const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
             wp[e] = pack_bf16x2(ds.x, ds.y);
+            dsk[u * 4 + e] = wp[e];
           }
-          st_sw128(ds_t, row, c * 4 + u, w);
+          if (!(a.dbg & 8)) st_sw128(ds_t, row, c * 4 + u, w);   // dQ's A operand (read MN-major from smem)
         }
+        if (!(a.dbg & 4)) tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
       }
       tc::tmem_st_wait();
       tc::fence_proxy_async();
