@@ -108,6 +108,10 @@ static_assert(F_SMEM <= 115712, "attn fwd: two CTAs per SM");
 //   S_g fp32 [64 key columns] at 64*g, overwritten in place by P_g (bf16 pairs, 32 columns) as the
 //   same thread consumes it; O_g fp32 at 128 + 64*g
 constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only when the running max grows by > 2^8
+#ifndef AVB_FWD_POLY_FROM
+#define AVB_FWD_POLY_FROM 6
+#endif
+constexpr int kFwdPolyFrom = AVB_FWD_POLY_FROM;  // exp2 pairs (e2 & 7) >= this go to the FMA pipe (2 of 8: measured best of 0-4)
 
 __global__ void __launch_bounds__(320, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(320, 2)
               const int col = c * 32 + 2 * e2;
               const float2 x = f2fma(make_float2(__uint_as_float(rb[0][2 * e2]), __uint_as_float(rb[0][2 * e2 + 1])),
                                      sl2, nm2);
-              float2 p = ((e2 & 7) >= 5) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+              float2 p = ((e2 & 7) >= kFwdPolyFrom) ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
               if (!FULL) {
                 p.x = (col < lim) ? p.x : 0.f;
                 p.y = (col + 1 < lim) ? p.y : 0.f;

@@ -4,7 +4,7 @@
 #include <cstdio>
 
 template <int VAR>
-__global__ void __launch_bounds__(128, 1) mix(int iters, long long* cyc) {
+__global__ void __launch_bounds__(128, 1) mix(int iters, long long* cyc, int random_data) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   __shared__ uint64_t bar;
@@ -15,6 +15,24 @@ __global__ void __launch_bounds__(128, 1) mix(int iters, long long* cyc) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = slot;
+  if (random_data) {
+    // bf16 values ~N(0,1)-ish in every operand (smem tiles and the TMEM A regions)
+    uint32_t st = 0x9E3779B9u * (threadIdx.x + 1) + blockIdx.x;
+    auto rnd = [&]() { st ^= st << 13; st ^= st >> 17; st ^= st << 5; return st; };
+    uint32_t* sm = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) sm[i] = (rnd() & 0x807F807Fu) | 0x3F003F00u;
+    tc::fence_proxy_async();
+    uint32_t r[32];
+    for (int col = 0; col < 512; col += 32) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) r[e] = (rnd() & 0x807F807Fu) | 0x3F003F00u;
+      tc::tmem_st_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + col, r);
+    }
+    tc::tmem_st_wait();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+  }
   if (threadIdx.x == 32) {
     const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384, tK = tmem + 448,
                    tV = tmem + 480;
@@ -52,10 +70,10 @@ __global__ void __launch_bounds__(128, 1) mix(int iters, long long* cyc) {
 }
 
 template <int VAR>
-void run(long long* cyc, const char* name) {
+void run(long long* cyc, const char* name, int rnd = 0) {
   const int iters = 1024;
   cudaFuncSetAttribute(mix<VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
-  mix<VAR><<<148, 128, 131072>>>(iters, cyc);
+  mix<VAR><<<148, 128, 131072>>>(iters, cyc, rnd);
   cudaDeviceSynchronize();
   long long h;
   cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
@@ -68,5 +86,7 @@ int main() {
   run<0>(cyc, "full mix (dV,S,dK,dP TS + dQ SS MN-major)");
   run<1>(cyc, "dV,S,dK,dP (TS) only");
   run<2>(cyc, "dQ (SS, A MN-major) only");
+  run<0>(cyc, "full mix, random bf16 operands", 1);
+  run<1>(cyc, "dV,S,dK,dP (TS), random operands", 1);
   return 0;
 }
