@@ -434,7 +434,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   uint64_t* p_ready = s_full + 10;               // P_i^T stored in TMEM by every compute warp
   uint64_t* dp_free = s_full + 11;               // dP_i^T read into registers by every compute warp
   uint64_t* kv_tmem = s_full + 12;               // K and V copied into TMEM (A operands of S^T / dP^T)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 13);
+  uint64_t* pt_read = s_full + 13;               // the dS group has read P_i^T (S^T columns reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -458,16 +459,17 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     tc::mbar_init(s_full, 1);
     tc::mbar_init(pv_done, 1);
     tc::mbar_init(dp_full, 1);
-    tc::mbar_init(ds_ready, kBwdCompute);
+    tc::mbar_init(ds_ready, kBwdCompute / 2);   // the dS group
     tc::mbar_init(mma_done, 1);
     tc::mbar_init(dq_free, kBwdDrain);
     tc::mbar_init(&stage_free[0], kBwdDrain);
     tc::mbar_init(&stage_free[1], kBwdDrain);
     tc::mbar_init(fin_done, 1);
     tc::mbar_init(s_free, kBwdCompute);
-    tc::mbar_init(p_ready, kBwdCompute);
+    tc::mbar_init(p_ready, kBwdCompute / 2);    // the exp group
     tc::mbar_init(dp_free, kBwdCompute);
     tc::mbar_init(kv_tmem, 4);
+    tc::mbar_init(pt_read, kBwdCompute / 2);    // the dS group
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -538,6 +540,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         const uint32_t acc = (ii > 0) ? 1u : 0u;
         // P_i^T lives over S_i^T and dS_i^T over dP_i^T (packed bf16, TMEM): dV_i / dK_i read them
         // before S_{i+1} / dP_{i+1} overwrite those columns (tcgen05.mma executes in issue order)
+        BWD_TRACE(8, ii);
         tc::mbar_wait(p_ready, ii & 1);
         tc::tc_fence_after();
         BWD_TRACE(0, ii);
@@ -545,7 +548,12 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16) = chunk kk/2
           tc::umma_f16_ts(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG,
                           (acc | kk) ? 1u : 0u);
+        BWD_TRACE(9, ii);
+        tc::mbar_wait(pt_read, ii & 1);    // the dS group holds P_i in registers: S^T columns are free
+        tc::tc_fence_after();
+        BWD_TRACE(10, ii);
         if (ii + 1 < nq) issue_s(ii + 1);
+        BWD_TRACE(11, ii);
         tc::mbar_wait(ds_ready, ii & 1);
         tc::tc_fence_after();
         BWD_TRACE(1, ii);
@@ -564,6 +572,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
           tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
         }
+        BWD_TRACE(12, ii);
         tc::umma_commit(mma_done);
         tc::umma_commit(&qd_empty[st]);
       }
@@ -621,14 +630,18 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ compute warps
-    // warp w: TMEM lane quadrant (w & 3) -> key rows; query chunk c = w >> 2 (32 of the 128 columns)
-    const int quad = warp & 3, c = warp >> 2;
+    // ------------------------------------------------------------ compute warps, two groups
+    // warps 0-7 "exp group": P^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 over S^T (TMEM);
+    // warps 8-15 "dS group": dS^T = P^T (dP^T - delta) -> bf16 over dP^T (TMEM) and into smem.
+    // The exp group runs one tile ahead: exp(i+1) overlaps dS(i) and the MMAs of tile i.
+    // warp w: TMEM lane quadrant (w & 3) -> key rows; query chunks {2h, 2h+1}, h = (w >> 2) & 1
+    const int quad = warp & 3, hh = (warp >> 2) & 1;
+    const bool exp_group = warp < 8;
     const int row = quad * 32 + lane;
     const int kvi = kv0 + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
-    if (c == 0) {
+    if (warp < 4) {
       // K and V rows of this quadrant -> TMEM (bf16 pairs, 32 columns each): the A operands of
       // S^T = K Q^T and dP^T = V dO^T, so those MMAs read only Q / dO from shared memory
       tc::mbar_wait(kv_full, 0);
@@ -651,115 +664,117 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     for (int ii = 0; ii < nq; ++ii) {
       const int i = i0 + ii, st = ii % B_QD_STAGES;
       const int q0 = i * BT;
-      uint8_t* ds_t = sDS + (ii & 1) * 32768;
       if (warp == 0) BWD_TRACE(4, ii);
-      tc::mbar_wait(s_full, ii & 1);
-      tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);  // -lse*log2e / -delta landed
-      tc::tc_fence_after();
-      if (warp == 0) BWD_TRACE(5, ii);
-      const float* sl = sLD + st * 256 + c * 32;
-      const float* sd = sLD + st * 256 + 128 + c * 32;
-      // warp-uniform: does any element of this 32 x 32 block need masking?
-      const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
-                        (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
-      uint32_t pk[16];
-      {
-        uint32_t rs[32];
-        if (a.dbg & 4) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) rs[e] = __float_as_uint((float)(lane + e) * -0.01f);
-        } else {
+      if (exp_group) {
+        tc::mbar_wait(s_full, ii & 1);
+        tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);  // -lse*log2e landed
+        tc::tc_fence_after();
+        if (warp == 0) BWD_TRACE(5, ii);
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hh + cc;
+          const float* sl = sLD + st * 256 + c * 32;
+          const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
+                            (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
+          uint32_t rs[32], pk[16];
           tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
           tc::tmem_ld_wait();
-        }
-        auto pbody = [&](auto edge_tag) {
-          constexpr bool EDGE = decltype(edge_tag)::value;
+          auto pbody = [&](auto edge_tag) {
+            constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
-            const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
-            const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                  make_float2(l1.z, l1.w)};
+            for (int u = 0; u < 4; ++u) {
+              const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
+              const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
+              const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                    make_float2(l1.z, l1.w)};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
-              const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
-              float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
-              if (EDGE) {
-                const int qi = q0 + c * 32 + u * 8 + 2 * e;
-                const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-                const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
-                p.x = ok0 ? p.x : 0.f;
-                p.y = ok1 ? p.y : 0.f;
+              for (int e = 0; e < 4; ++e) {
+                const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
+                const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
+                float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                if (EDGE) {
+                  const int qi = q0 + c * 32 + u * 8 + 2 * e;
+                  const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+                  const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
+                  p.x = ok0 ? p.x : 0.f;
+                  p.y = ok1 ? p.y : 0.f;
+                }
+                pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
               }
-              pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
             }
-          }
-        };
-        if (edge)
-          pbody(std::true_type{});
-        else
-          pbody(std::false_type{});
-      }
-      if (!(a.dbg & 4)) tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over this warp's consumed S^T chunk
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_ready);
-      tc::mbar_wait(dp_full, ii & 1);
-      tc::tc_fence_after();
-      if (warp == 0) BWD_TRACE(6, ii);
-      if (ii >= 2) tc::mbar_wait(&stage_free[ii & 1], ((ii - 2) >> 1) & 1);  // dQ_{i-2} staging read out
-      {
-        uint32_t rp[32], dsk[16];
-        if (a.dbg & 4) {
+          };
+          if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
+          tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
+        }
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_ready);
+      } else {
+        tc::mbar_wait(p_ready, ii & 1);
+        tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);  // -delta landed
+        tc::tc_fence_after();
+        uint32_t pk[2][16];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) rp[e] = __float_as_uint((float)(lane - e) * 0.01f);
-        } else {
+        for (int cc = 0; cc < 2; ++cc) tc::tmem_ld_32x32b_x16(tST + lane_off + (2 * hh + cc) * 32, pk[cc]);
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(pt_read);   // S(i+1) may now overwrite these columns
+        tc::mbar_wait(dp_full, ii & 1);
+        tc::tc_fence_after();
+        if (warp == 8) BWD_TRACE(6, ii);
+        if (ii >= 2) tc::mbar_wait(&stage_free[ii & 1], ((ii - 2) >> 1) & 1);  // dQ_{i-2} staging read out
+        uint8_t* ds_t = sDS + (ii & 1) * 32768;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hh + cc;
+          const float* sd = sLD + st * 256 + 128 + c * 32;
+          uint32_t rp[32], dsk[16];
           tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
           tc::tmem_ld_wait();
-        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
-          const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
-          const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
-                                make_float2(d1.z, d1.w)};
-          uint4 w;
-          uint32_t* wp = &w.x;
+          for (int u = 0; u < 4; ++u) {
+            const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
+            const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
+            const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
+                                  make_float2(d1.z, d1.w)};
+            uint4 w;
+            uint32_t* wp = &w.x;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
-            const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
-            wp[e] = pack_bf16x2(ds.x, ds.y);
-            dsk[u * 4 + e] = wp[e];
+            for (int e = 0; e < 4; ++e) {
+              const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
+              const float2 ds = f2mul(unpack_bf16x2(pk[cc][u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
+              wp[e] = pack_bf16x2(ds.x, ds.y);
+              dsk[u * 4 + e] = wp[e];
+            }
+            st_sw128(ds_t, row, c * 4 + u, w);   // dQ's A operand (read MN-major from smem)
           }
-          if (!(a.dbg & 8)) st_sw128(ds_t, row, c * 4 + u, w);   // dQ's A operand (read MN-major from smem)
+          tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
         }
-        if (!(a.dbg & 4)) tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
+        tc::tmem_st_wait();
+        tc::fence_proxy_async();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(ds_ready);
+        if (warp == 8) BWD_TRACE(7, ii);
       }
-      tc::tmem_st_wait();
-      tc::fence_proxy_async();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ds_ready);
-      if (warp == 0) BWD_TRACE(7, ii);
     }
     // dK / dV out (softmax scale folded into dK: dS was stored without it).  A dedicated barrier:
     // these warps skip mma_done phases, so a parity wait on it could be satisfied by an older phase.
+    // The exp group writes dV, the dS group dK; warp (quadrant, h) owns 32 of the 64 columns.
     tc::mbar_wait(fin_done, 0);
     tc::tc_fence_after();
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tsrc = which ? tDK : tDV;
-      const float osc = which ? a.scale : 1.f;
-      __nv_bfloat16* g = (which ? a.dk : a.dv) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + c * 16;
-      uint32_t r[16];
-      tc::tmem_ld_32x32b_x16(tsrc + lane_off + c * 16, r);
+    {
+      const uint32_t tsrc = exp_group ? tDV : tDK;
+      const float osc = exp_group ? 1.f : a.scale;
+      __nv_bfloat16* g = (exp_group ? a.dv : a.dk) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + hh * 32;
+      uint32_t r[32];
+      tc::tmem_ld_32x32b_x32(tsrc + lane_off + hh * 32, r);
       tc::tmem_ld_wait();
       if (kvi < a.N) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u) {
           uint4 v;
           v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
           v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);

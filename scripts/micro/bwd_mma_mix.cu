@@ -8,9 +8,10 @@ __global__ void __launch_bounds__(128, 1) mix(int iters, long long* cyc, int ran
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   __shared__ uint64_t bar;
+  __shared__ uint64_t bar2[5];
   const int warp = threadIdx.x >> 5;
   if (warp == 0) tc::tmem_alloc(&slot, 512);
-  if (threadIdx.x == 32) { tc::mbar_init(&bar, 1); tc::fence_barrier_init(); }
+  if (threadIdx.x == 32) { tc::mbar_init(&bar, 1); for (int i = 0; i < 5; ++i) tc::mbar_init(&bar2[i], 1); tc::fence_barrier_init(); }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -54,6 +55,30 @@ __global__ void __launch_bounds__(128, 1) mix(int iters, long long* cyc, int ran
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) tc::umma_f16_ts(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
       }
+      if (VAR == 3) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ts(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, 1u);
+        tc::umma_commit(&bar2[0]);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) tc::umma_f16_ts(tST, tK + 8 * kk, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_commit(&bar2[1]);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ts(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG, 1u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) tc::umma_f16_ts(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_commit(&bar2[2]);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::umma_f16_ss(tDQ, tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024), tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
+        tc::umma_commit(&bar2[3]);
+        tc::umma_commit(&bar2[4]);
+        tc::tc_fence_after();
+      }
       if (VAR == 0 || VAR == 2) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -87,6 +112,7 @@ int main() {
   run<1>(cyc, "dV,S,dK,dP (TS) only");
   run<2>(cyc, "dQ (SS, A MN-major) only");
   run<0>(cyc, "full mix, random bf16 operands", 1);
+  run<3>(cyc, "full mix + 5 commits + fences per step");
   run<1>(cyc, "dV,S,dK,dP (TS), random operands", 1);
   return 0;
 }
