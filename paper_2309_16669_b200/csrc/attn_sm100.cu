@@ -361,7 +361,8 @@ struct BwdArgs {
   __nv_bfloat16* dv;
   int64_t ld_g, sb_g;     // strides of dk/dv
   int causal;
-  long long* trace;       // debug: per-step clock64 events of CTA (0,0,0) (AVB_ATTN_TRACE), else null
+  int nkt, items;         // key tiles per (clip, head); work items = B * H * nkt (persistent grid)
+  long long* trace;       // debug: per-step clock64 events of CTA 0 (AVB_ATTN_TRACE), else null
   int dbg;                // debug experiment flags (AVB_ATTN_DBG): 1 = skip the dQ drain
 };
 
@@ -374,8 +375,10 @@ constexpr int B_SK = 0, B_SV = 16384;
 constexpr int B_SQD = 32768;                               // 3 stages x (Q 16K + dO 16K)
 constexpr int B_SDS = B_SQD + B_QD_STAGES * 32768;         // 2 buffers x dS^T 32K (then dQ staging)
 constexpr int B_SLD = B_SDS + 2 * 32768;                   // 3 stages x (lse 512 + delta 512)
-constexpr int B_BAR = B_SLD + B_QD_STAGES * 1024;
+constexpr int B_SK2 = B_SLD + B_QD_STAGES * 1024;           // second K buffer (next work item)
+constexpr int B_BAR = B_SK2 + 16384;
 constexpr int B_SMEM = B_BAR + 256;
+static_assert(B_SK2 % 1024 == 0, "attn bwd K2 alignment");
 static_assert(B_SMEM <= 232448, "attn bwd smem");
 constexpr int kBwdCompute = 16;              // compute warps: 4 per TMEM lane quadrant (one 32-query chunk each)
 constexpr int kBwdDrain = 4;                 // dQ drain warps: one per TMEM lane quadrant
@@ -387,7 +390,7 @@ constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
 
 #define BWD_TRACE(ev, ii)                                                                       \
   do {                                                                                          \
-    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && ii < 32) \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && (ii) < 32) \
       a.trace[(ii) * 16 + (ev)] = clock64();                                                      \
   } while (0)
 
@@ -397,55 +400,70 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
   return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
 }
 
-// One CTA per (128-key tile, head, clip), 1 CTA/SM, 22 warps.  Per query tile i (TMEM lanes = keys):
-//   MMA warp, after ds_ready(i):   S_{i+1}^T = K Q_{i+1}^T  -> s_full      (compute i+1 starts here)
-//                                  dV += P_i^T dO_i (A = P^T from TMEM) -> pv_done
-//                                  dP_{i+1}^T = V dO_{i+1}^T -> dp_full
-//                                  dK += dS_i^T Q_i;  dQ_i = dS_i K (dS^T smem tile, MN-major) -> mma_done
-//   compute warps 0-15 (quadrant w&3, query chunk w>>2):  P = exp2(S^T*scale*log2e - lse*log2e)
-//        -> bf16 P^T into its own TMEM region (after pv_done of i-1);  dS^T = P (dP^T - delta) -> smem
-//   drain warps 16-19: dQ_i TMEM -> 128B-swizzled fp32 staging (the dS^T_i buffer) -> TMA reduce-add
-//   warp 20 TMA (K, V once; Q/dO/-lse/-delta 3-stage ring), warp 21 MMA.
-// So the exp work of tile i+1 overlaps dV_i / dP_{i+1} / dK_i / dQ_i on the tensor core.
+// Persistent: gridDim.x CTAs (one per SM, 22 warps) walk work items w = blockIdx.x, +gridDim.x, ...;
+// item w = (128-key tile kt, head h, clip b).  One global step counter g runs over every (item,
+// query tile) pair of the CTA, so every per-step barrier keeps its phase across item boundaries
+// and the pipeline never drains between items: the next item's K/V are loaded (second K buffer)
+// and copied into TMEM while the current item's last tiles run, its first S^T / dP^T MMAs are
+// issued in the slot the current item's S_{i+1} would take, and the dK/dV epilogue is done by the
+// drain warps while the compute warps already work on the next item.  Per step g (TMEM lanes = keys):
+//   MMA warp:  dV += P_g^T dO_g (A = P^T from TMEM) | S_{g+1}^T = K Q_{g+1}^T (A = K from TMEM)
+//              dK += dS_g^T Q_g (A = dS^T from TMEM) | dP_{g+1}^T = V dO_{g+1}^T (A = V from TMEM)
+//              dQ_g = dS_g K (dS^T smem tile, MN-major; K from smem) -> mma_done
+//   exp group (warps 0-7): P^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 over S^T (TMEM)
+//   dS group (warps 8-15): dS^T = P^T (dP^T - delta) -> bf16 over dP^T (TMEM) and into smem
+//   drain warps 16-19: dQ_g TMEM -> 128B-swizzled fp32 staging (the dS^T_g buffer) -> TMA reduce-add;
+//                      after an item's last step, its dK / dV TMEM -> bf16 global
+//   warp 20 TMA (K, V per item; Q/dO/-lse/-delta 3-stage ring), warp 21 MMA.
+struct BwdItem {
+  int kt, h, b, i0, nq;
+};
+
+__device__ __forceinline__ BwdItem bwd_item(const BwdArgs& a, int w) {
+  BwdItem t;
+  t.kt = w % a.nkt;
+  const int r = w / a.nkt;
+  t.h = r % a.H;
+  t.b = r / a.H;
+  t.i0 = a.causal ? t.kt : 0;   // first query tile that sees this key tile
+  t.nq = a.nkt - t.i0;
+  return t;
+}
+
 __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                     const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
-  uint8_t* sK = smem + B_SK;
+  auto sKb = [&](int it) { return smem + ((it & 1) ? B_SK2 : B_SK); };   // K double buffer (per work item)
   uint8_t* sV = smem + B_SV;
   uint8_t* sQD = smem + B_SQD;
   uint8_t* sDS = smem + B_SDS;
   float* sLD = reinterpret_cast<float*>(smem + B_SLD);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
-  uint64_t* kv_full = bars + 0;
+  uint64_t* kv_full = bars + 0;                  // per item: K_it, V_it in smem
   uint64_t* qd_full = bars + 1;                  // [3]
   uint64_t* qd_empty = bars + 1 + B_QD_STAGES;   // [3]
   uint64_t* s_full = bars + 1 + 2 * B_QD_STAGES;
-  uint64_t* pv_done = s_full + 1;
-  uint64_t* dp_full = s_full + 2;
-  uint64_t* ds_ready = s_full + 3;
-  uint64_t* mma_done = s_full + 4;
-  uint64_t* dq_free = s_full + 5;
-  uint64_t* stage_free = s_full + 6;             // [2]
-  uint64_t* fin_done = s_full + 8;               // every MMA of the CTA complete (dK / dV final)
-  uint64_t* s_free = s_full + 9;                 // S_i^T read into registers by every compute warp
-  uint64_t* p_ready = s_full + 10;               // P_i^T stored in TMEM by every compute warp
-  uint64_t* dp_free = s_full + 11;               // dP_i^T read into registers by every compute warp
-  uint64_t* kv_tmem = s_full + 12;               // K and V copied into TMEM (A operands of S^T / dP^T)
-  uint64_t* pt_read = s_full + 13;               // the dS group has read P_i^T (S^T columns reusable)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 14);
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* ds_ready = s_full + 2;
+  uint64_t* mma_done = s_full + 3;
+  uint64_t* dq_free = s_full + 4;
+  uint64_t* stage_free = s_full + 5;             // [2]
+  uint64_t* acc_free = s_full + 7;               // per item: dK / dV read out of TMEM by the drain warps
+  uint64_t* p_ready = s_full + 8;                // P_g^T stored in TMEM by every exp-group warp
+  uint64_t* kv_tmem = s_full + 9;                // per item: K and V copied into TMEM (A operands of S^T / dP^T)
+  uint64_t* pt_read = s_full + 10;               // the dS group has read P_g^T (S^T columns reusable)
+  uint64_t* k_free = s_full + 11;                // [2] per item: its dQ MMAs are done with that K buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int kv0 = kt * BT;
-  const int nq_all = (a.N + BT - 1) / BT;
-  const int i0 = a.causal ? kt : 0;  // first query tile that sees this key tile
-  const int nq = nq_all - i0;
+  const int stride = gridDim.x;
   constexpr int kDrain0 = kBwdCompute, kTMA = kBwdCompute + kBwdDrain, kMMA = kTMA + 1;
 
   if (warp == kTMA && lane == 0) {
+    BWD_TRACE(13, 0);
     tc::tma_prefetch(&tmQ);
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
@@ -457,19 +475,18 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       tc::mbar_init(&qd_empty[s], 1);
     }
     tc::mbar_init(s_full, 1);
-    tc::mbar_init(pv_done, 1);
     tc::mbar_init(dp_full, 1);
     tc::mbar_init(ds_ready, kBwdCompute / 2);   // the dS group
     tc::mbar_init(mma_done, 1);
     tc::mbar_init(dq_free, kBwdDrain);
     tc::mbar_init(&stage_free[0], kBwdDrain);
     tc::mbar_init(&stage_free[1], kBwdDrain);
-    tc::mbar_init(fin_done, 1);
-    tc::mbar_init(s_free, kBwdCompute);
+    tc::mbar_init(acc_free, kBwdDrain);
     tc::mbar_init(p_ready, kBwdCompute / 2);    // the exp group
-    tc::mbar_init(dp_free, kBwdCompute);
-    tc::mbar_init(kv_tmem, 4);
+    tc::mbar_init(kv_tmem, kBwdCompute / 2);    // the exp group
     tc::mbar_init(pt_read, kBwdCompute / 2);    // the dS group
+    tc::mbar_init(&k_free[0], 1);
+    tc::mbar_init(&k_free[1], 1);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -477,33 +494,38 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T | dP^T | dV | dK | dQ | P^T (bf16 pairs)
   // TMEM: S^T (P^T packed over it) | dP^T (dS^T packed over it) | dV | dK | dQ | K | V (bf16 pairs)
   const uint32_t tST = tmem, tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tDQ = tmem + 384,
                  tK = tmem + 448, tV = tmem + 480;
-  const int64_t bh = (int64_t)b * a.H + h;
 
   if (warp == kTMA) {
     if (lane == 0) {
-      tc::mbar_arrive_expect_tx(kv_full, 32768);
-      tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
-      tc::tma_load_3d(sV, &tmV, kv_full, h * HD, kv0, b);
-      for (int ii = 0; ii < nq; ++ii) {
-        const int i = i0 + ii, st = ii % B_QD_STAGES;
-        if (ii >= B_QD_STAGES) tc::mbar_wait(&qd_empty[st], ((ii / B_QD_STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
-        tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
-        tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
-        const float* gl = a.nlse2 + bh * a.Npad + i * BT;
-        const float* gd = a.ndelta + bh * a.Npad + i * BT;
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                         smem_u32(sLD + st * 256)),
-                     "l"(gl), "r"(smem_u32(&qd_full[st]))
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                         smem_u32(sLD + st * 256 + 128)),
-                     "l"(gd), "r"(smem_u32(&qd_full[st]))
-                     : "memory");
+      int g = 0, it = 0;
+      for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
+        const BwdItem t = bwd_item(a, w);
+        const int64_t bh = (int64_t)t.b * a.H + t.h;
+        if (it >= 1) tc::mbar_wait(kv_tmem, (it - 1) & 1);                  // V_{it-1} copied out of sV
+        if (it >= 2) tc::mbar_wait(&k_free[it & 1], ((it >> 1) - 1) & 1);  // item it-2 done with this K buffer
+        tc::mbar_arrive_expect_tx(kv_full, 32768);
+        tc::tma_load_3d(sKb(it), &tmK, kv_full, t.h * HD, t.kt * BT, t.b);
+        tc::tma_load_3d(sV, &tmV, kv_full, t.h * HD, t.kt * BT, t.b);
+        for (int ii = 0; ii < t.nq; ++ii, ++g) {
+          const int i = t.i0 + ii, st = g % B_QD_STAGES;
+          if (g >= B_QD_STAGES) tc::mbar_wait(&qd_empty[st], ((g / B_QD_STAGES) - 1) & 1);
+          tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
+          tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], t.h * HD, i * BT, t.b);
+          tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], t.h * HD, i * BT, t.b);
+          const float* gl = a.nlse2 + bh * a.Npad + i * BT;
+          const float* gd = a.ndelta + bh * a.Npad + i * BT;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                           smem_u32(sLD + st * 256)),
+                       "l"(gl), "r"(smem_u32(&qd_full[st]))
+                       : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                           smem_u32(sLD + st * 256 + 128)),
+                       "l"(gd), "r"(smem_u32(&qd_full[st]))
+                       : "memory");
+        }
       }
     }
   } else if (warp == kMMA) {
@@ -511,10 +533,9 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
       constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV (A = P^T in TMEM), dK: B (dO / Q) MN-major
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto issue_s = [&](int ii) {      // S_ii^T = K Q_ii^T, K (A) from TMEM
-        const int st = ii % B_QD_STAGES;
-        tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);
+      auto issue_s = [&](int gg) {      // S_gg^T = K Q_gg^T, K (A) from TMEM
+        const int st = gg % B_QD_STAGES;
+        tc::mbar_wait(&qd_full[st], (gg / B_QD_STAGES) & 1);
         tc::tc_fence_after();
         const uint32_t aQ = smem_u32(sQD + st * 32768);
 #pragma unroll
@@ -522,110 +543,156 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           tc::umma_f16_ts(tST, tK + 8 * kk, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
         tc::umma_commit(s_full);
       };
-      auto issue_dp = [&](int ii) {     // dP_ii^T = V dO_ii^T, V (A) from TMEM (qd_full(ii) already observed)
-        const uint32_t aDO = smem_u32(sQD + (ii % B_QD_STAGES) * 32768) + 16384;
+      auto issue_dp = [&](int gg) {     // dP_gg^T = V dO_gg^T, V (A) from TMEM (qd_full(gg) already observed)
+        const uint32_t aDO = smem_u32(sQD + (gg % B_QD_STAGES) * 32768) + 16384;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           tc::umma_f16_ts(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
         tc::umma_commit(dp_full);
       };
-      tc::mbar_wait(kv_tmem, 0);          // K, V in TMEM (compute warps 0-3 copied them)
-      tc::tc_fence_after();
-      issue_s(0);
-      issue_dp(0);
-      for (int ii = 0; ii < nq; ++ii) {
-        const int st = ii % B_QD_STAGES, pb = ii & 1;
-        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
-        const uint32_t aDS = smem_u32(sDS + pb * 32768);
-        const uint32_t acc = (ii > 0) ? 1u : 0u;
-        // P_i^T lives over S_i^T and dS_i^T over dP_i^T (packed bf16, TMEM): dV_i / dK_i read them
-        // before S_{i+1} / dP_{i+1} overwrite those columns (tcgen05.mma executes in issue order)
-        BWD_TRACE(8, ii);
-        tc::mbar_wait(p_ready, ii & 1);
-        tc::tc_fence_after();
-        BWD_TRACE(0, ii);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16) = chunk kk/2
-          tc::umma_f16_ts(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG,
-                          (acc | kk) ? 1u : 0u);
-        BWD_TRACE(9, ii);
-        tc::mbar_wait(pt_read, ii & 1);    // the dS group holds P_i in registers: S^T columns are free
-        tc::tc_fence_after();
-        BWD_TRACE(10, ii);
-        if (ii + 1 < nq) issue_s(ii + 1);
-        BWD_TRACE(11, ii);
-        tc::mbar_wait(ds_ready, ii & 1);
-        tc::tc_fence_after();
-        BWD_TRACE(1, ii);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)     // dK += dS^T Q (A = dS^T from TMEM)
-          tc::umma_f16_ts(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG,
-                          (acc | kk) ? 1u : 0u);
-        if (ii + 1 < nq) issue_dp(ii + 1);
-        if (ii >= 1) tc::mbar_wait(dq_free, (ii - 1) & 1);   // dQ_{i-1} read out of TMEM
-        tc::tc_fence_after();
-        BWD_TRACE(2, ii);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
-          // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
-          const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
-          tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
+      int g = 0, it = 0;
+      for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
+        const BwdItem t = bwd_item(a, w);
+        const bool has_next = w + stride < a.items;
+        const uint32_t aK = smem_u32(sKb(it));
+        if (it == 0) {
+          tc::mbar_wait(kv_tmem, 0);      // K, V of the first item in TMEM (exp-group warps copied them)
+          tc::tc_fence_after();
+          issue_s(0);
+          issue_dp(0);
         }
-        BWD_TRACE(12, ii);
-        tc::umma_commit(mma_done);
-        tc::umma_commit(&qd_empty[st]);
+        for (int ii = 0; ii < t.nq; ++ii, ++g) {
+          const int st = g % B_QD_STAGES, pb = g & 1;
+          const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
+          const uint32_t aDS = smem_u32(sDS + pb * 32768);
+          const uint32_t acc = (ii > 0) ? 1u : 0u;
+          const bool last = ii + 1 == t.nq, nxt = !last || has_next;
+          // P_g^T lives over S_g^T and dS_g^T over dP_g^T (packed bf16, TMEM): dV_g / dK_g read them
+          // before S_{g+1} / dP_{g+1} overwrite those columns (tcgen05.mma executes in issue order)
+          BWD_TRACE(8, g);
+          tc::mbar_wait(p_ready, g & 1);
+          if (ii == 0 && it > 0) tc::mbar_wait(acc_free, (it - 1) & 1);   // previous item's dK / dV read out
+          tc::tc_fence_after();
+          BWD_TRACE(0, g);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16) = chunk kk/2
+            tc::umma_f16_ts(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024),
+                            idG, (acc | kk) ? 1u : 0u);
+          BWD_TRACE(9, g);
+          tc::mbar_wait(pt_read, g & 1);     // the dS group holds P_g in registers: S^T columns are free
+          if (last && has_next) tc::mbar_wait(kv_tmem, (it + 1) & 1);   // next item's K / V in TMEM
+          tc::tc_fence_after();
+          BWD_TRACE(10, g);
+          if (nxt) issue_s(g + 1);
+          BWD_TRACE(11, g);
+          tc::mbar_wait(ds_ready, g & 1);
+          tc::tc_fence_after();
+          BWD_TRACE(1, g);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)     // dK += dS^T Q (A = dS^T from TMEM)
+            tc::umma_f16_ts(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024),
+                            idG, (acc | kk) ? 1u : 0u);
+          if (nxt) issue_dp(g + 1);
+          if (g >= 1) tc::mbar_wait(dq_free, (g - 1) & 1);   // dQ_{g-1} read out of TMEM
+          tc::tc_fence_after();
+          BWD_TRACE(2, g);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
+            // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
+            const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
+            tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
+          }
+          BWD_TRACE(12, g);
+          tc::umma_commit(mma_done);
+          tc::umma_commit(&qd_empty[st]);
+          if (last) tc::umma_commit(&k_free[it & 1]);
+        }
       }
-      tc::umma_commit(fin_done);
     }
   } else if (warp >= kDrain0) {
-    // ------------------------------------------------------------ dQ drain warps (one per TMEM lane quadrant)
+    // ------------------------------------------------------------ drain warps (one per TMEM lane quadrant)
     const int quad = warp & 3;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    for (int ii = 0; ii < nq; ++ii) {
-      const int pb = ii & 1;
-      tc::mbar_wait(mma_done, ii & 1);   // dK_i / dQ_i complete: dQ_i final, dS^T_i buffer free
-      tc::tc_fence_after();
-      if (a.dbg & 1) {
-        __syncwarp();
-        if (lane == 0) {
-          tc::mbar_arrive(dq_free);
-          tc::mbar_arrive(&stage_free[pb]);
-        }
-        continue;
-      }
-      uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
+    int g = 0;
+    for (int w = blockIdx.x; w < a.items; w += stride) {
+      const BwdItem t = bwd_item(a, w);
+      for (int ii = 0; ii < t.nq; ++ii, ++g) {
+        const int pb = g & 1;
+        tc::mbar_wait(mma_done, g & 1);   // dK_g / dQ_g complete: dQ_g final, dS^T_g buffer free
+        tc::tc_fence_after();
+        if (ii + 1 == t.nq) {
+          // the item's dK / dV are final: out as bf16 (softmax scale folded into dK: dS was stored
+          // without it), then hand the accumulators to the next item
+          const int kvi = t.kt * BT + quad * 32 + lane;
+#pragma unroll 1
+          for (int which = 0; which < 2; ++which) {
+            const uint32_t tsrc = which ? tDK : tDV;
+            const float osc = which ? a.scale : 1.f;
+            __nv_bfloat16* gp = (which ? a.dk : a.dv) + (int64_t)t.b * a.sb_g + (int64_t)kvi * a.ld_g + t.h * HD;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tDQ + lane_off + hh * 32, r);
-        tc::tmem_ld_wait();
-        if (hh == 1) {
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t r[32];
+              tc::tmem_ld_32x32b_x32(tsrc + lane_off + hh * 32, r);
+              tc::tmem_ld_wait();
+              if (kvi < a.N) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  uint4 v;
+                  v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
+                  v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
+                  v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * osc, __uint_as_float(r[u * 8 + 5]) * osc);
+                  v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * osc, __uint_as_float(r[u * 8 + 7]) * osc);
+                  reinterpret_cast<uint4*>(gp + hh * 32)[u] = v;
+                }
+              }
+            }
+          }
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(dq_free);
+          if (lane == 0) tc::mbar_arrive(acc_free);
         }
+        if (a.dbg & 1) {
+          __syncwarp();
+          if (lane == 0) {
+            tc::mbar_arrive(dq_free);
+            tc::mbar_arrive(&stage_free[pb]);
+          }
+          continue;
+        }
+        uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<uint4*>(stage + hh * 4096 + lane * 128 + ((u ^ (lane & 7)) << 4)) =
-              make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
-      }
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        const int q0 = (i0 + ii) * BT + quad * 32;
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(tDQ + lane_off + hh * 32, r);
+          tc::tmem_ld_wait();
+          if (hh == 1) {
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(dq_free);
+          }
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-          asm volatile(
-              "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                  reinterpret_cast<uint64_t>(&tmDQ)),
-              "r"(smem_u32(stage + hh * 4096)), "r"(h * HD + hh * 32), "r"(q0), "r"(b)
-              : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        tc::mbar_arrive(&stage_free[pb]);   // the buffer may take dS^T_{i+2}
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(stage + hh * 4096 + lane * 128 + ((u ^ (lane & 7)) << 4)) =
+                make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
+        }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int q0 = (t.i0 + ii) * BT + quad * 32;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmDQ)),
+                "r"(smem_u32(stage + hh * 4096)), "r"(t.h * HD + hh * 32), "r"(q0), "r"(t.b)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          tc::mbar_arrive(&stage_free[pb]);   // the buffer may take dS^T_{g+2}
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
@@ -633,160 +700,143 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     // ------------------------------------------------------------ compute warps, two groups
     // warps 0-7 "exp group": P^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 over S^T (TMEM);
     // warps 8-15 "dS group": dS^T = P^T (dP^T - delta) -> bf16 over dP^T (TMEM) and into smem.
-    // The exp group runs one tile ahead: exp(i+1) overlaps dS(i) and the MMAs of tile i.
+    // The exp group runs one tile ahead: exp(g+1) overlaps dS(g) and the MMAs of tile g.
     // warp w: TMEM lane quadrant (w & 3) -> key rows; query chunks {2h, 2h+1}, h = (w >> 2) & 1
     const int quad = warp & 3, hh = (warp >> 2) & 1;
     const bool exp_group = warp < 8;
     const int row = quad * 32 + lane;
-    const int kvi = kv0 + row;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
-    if (warp < 4) {
-      // K and V rows of this quadrant -> TMEM (bf16 pairs, 32 columns each): the A operands of
-      // S^T = K Q^T and dP^T = V dO^T, so those MMAs read only Q / dO from shared memory
-      tc::mbar_wait(kv_full, 0);
-#pragma unroll
-      for (int which = 0; which < 2; ++which) {
-        const uint8_t* src = (which ? sV : sK) + row * 128;
+    int g = 0, it = 0;
+    for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
+      const BwdItem t = bwd_item(a, w);
+      const int kv0 = t.kt * BT, kvi = kv0 + row;
+      if (exp_group) {
+        // this item's K (warps 0-3) / V (warps 4-7) rows -> TMEM (bf16 pairs, 32 columns): the A
+        // operands of S^T = K Q^T and dP^T = V dO^T, once the previous item's last S^T / dP^T
+        // MMAs are done reading them (dp_full of its last step: dP was issued after S)
+        tc::mbar_wait(kv_full, it & 1);
+        if (g > 0) tc::mbar_wait(dp_full, (g - 1) & 1);
+        tc::tc_fence_after();
+        const uint8_t* src = (hh ? sV : sKb(it)) + row * 128;
         uint32_t r[32];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint4 q = *reinterpret_cast<const uint4*>(src + ((u ^ (row & 7)) << 4));
           r[4 * u] = q.x; r[4 * u + 1] = q.y; r[4 * u + 2] = q.z; r[4 * u + 3] = q.w;
         }
-        tc::tmem_st_32x32b_x32((which ? tV : tK) + lane_off, r);
+        tc::tmem_st_32x32b_x32((hh ? tV : tK) + lane_off, r);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(kv_tmem);
       }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(kv_tmem);
-    }
-    for (int ii = 0; ii < nq; ++ii) {
-      const int i = i0 + ii, st = ii % B_QD_STAGES;
-      const int q0 = i * BT;
-      if (warp == 0) BWD_TRACE(4, ii);
-      if (exp_group) {
-        tc::mbar_wait(s_full, ii & 1);
-        tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);  // -lse*log2e landed
-        tc::tc_fence_after();
-        if (warp == 0) BWD_TRACE(5, ii);
+      for (int ii = 0; ii < t.nq; ++ii, ++g) {
+        const int i = t.i0 + ii, st = g % B_QD_STAGES;
+        const int q0 = i * BT;
+        if (warp == 0) BWD_TRACE(4, g);
+        if (exp_group) {
+          tc::mbar_wait(s_full, g & 1);
+          tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -lse*log2e landed
+          tc::tc_fence_after();
+          if (warp == 0) BWD_TRACE(5, g);
 #pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * hh + cc;
-          const float* sl = sLD + st * 256 + c * 32;
-          const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
-                            (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
-          uint32_t rs[32], pk[16];
-          tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hh + cc;
+            const float* sl = sLD + st * 256 + c * 32;
+            const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
+                              (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
+            uint32_t rs[32], pk[16];
+            tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
+            tc::tmem_ld_wait();
+            auto pbody = [&](auto edge_tag) {
+              constexpr bool EDGE = decltype(edge_tag)::value;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
+                const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
+                const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                      make_float2(l1.z, l1.w)};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 sv =
+                      make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
+                  const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
+                  float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                  if (EDGE) {
+                    const int qi = q0 + c * 32 + u * 8 + 2 * e;
+                    const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+                    const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
+                    p.x = ok0 ? p.x : 0.f;
+                    p.y = ok1 ? p.y : 0.f;
+                  }
+                  pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
+                }
+              }
+            };
+            if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
+            tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
+          }
+          tc::tmem_st_wait();
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(p_ready);
+        } else {
+          tc::mbar_wait(p_ready, g & 1);
+          tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -delta landed
+          tc::tc_fence_after();
+          uint32_t pk[2][16];
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) tc::tmem_ld_32x32b_x16(tST + lane_off + (2 * hh + cc) * 32, pk[cc]);
           tc::tmem_ld_wait();
-          auto pbody = [&](auto edge_tag) {
-            constexpr bool EDGE = decltype(edge_tag)::value;
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(pt_read);   // S_{g+1} may now overwrite these columns
+          tc::mbar_wait(dp_full, g & 1);
+          tc::tc_fence_after();
+          if (warp == 8) BWD_TRACE(6, g);
+          if (g >= 2) tc::mbar_wait(&stage_free[g & 1], ((g - 2) >> 1) & 1);  // dQ_{g-2} staging read out
+          uint8_t* ds_t = sDS + (g & 1) * 32768;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hh + cc;
+            const float* sd = sLD + st * 256 + 128 + c * 32;
+            uint32_t rp[32], dsk[16];
+            tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+            tc::tmem_ld_wait();
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
-              const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
-              const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                    make_float2(l1.z, l1.w)};
+              const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
+              const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
+              const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
+                                    make_float2(d1.z, d1.w)};
+              uint4 wv;
+              uint32_t* wp = &wv.x;
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
-                const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
-                float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
-                if (EDGE) {
-                  const int qi = q0 + c * 32 + u * 8 + 2 * e;
-                  const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-                  const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
-                  p.x = ok0 ? p.x : 0.f;
-                  p.y = ok1 ? p.y : 0.f;
-                }
-                pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
+                const float2 dp =
+                    make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
+                const float2 ds = f2mul(unpack_bf16x2(pk[cc][u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
+                wp[e] = pack_bf16x2(ds.x, ds.y);
+                dsk[u * 4 + e] = wp[e];
               }
+              st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
             }
-          };
-          if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
-          tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
-        }
-        tc::tmem_st_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_ready);
-      } else {
-        tc::mbar_wait(p_ready, ii & 1);
-        tc::mbar_wait(&qd_full[st], (ii / B_QD_STAGES) & 1);  // -delta landed
-        tc::tc_fence_after();
-        uint32_t pk[2][16];
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) tc::tmem_ld_32x32b_x16(tST + lane_off + (2 * hh + cc) * 32, pk[cc]);
-        tc::tmem_ld_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(pt_read);   // S(i+1) may now overwrite these columns
-        tc::mbar_wait(dp_full, ii & 1);
-        tc::tc_fence_after();
-        if (warp == 8) BWD_TRACE(6, ii);
-        if (ii >= 2) tc::mbar_wait(&stage_free[ii & 1], ((ii - 2) >> 1) & 1);  // dQ_{i-2} staging read out
-        uint8_t* ds_t = sDS + (ii & 1) * 32768;
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * hh + cc;
-          const float* sd = sLD + st * 256 + 128 + c * 32;
-          uint32_t rp[32], dsk[16];
-          tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
-            const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
-            const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
-                                  make_float2(d1.z, d1.w)};
-            uint4 w;
-            uint32_t* wp = &w.x;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
-              const float2 ds = f2mul(unpack_bf16x2(pk[cc][u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
-              wp[e] = pack_bf16x2(ds.x, ds.y);
-              dsk[u * 4 + e] = wp[e];
-            }
-            st_sw128(ds_t, row, c * 4 + u, w);   // dQ's A operand (read MN-major from smem)
+            tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
           }
-          tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
-        }
-        tc::tmem_st_wait();
-        tc::fence_proxy_async();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(ds_ready);
-        if (warp == 8) BWD_TRACE(7, ii);
-      }
-    }
-    // dK / dV out (softmax scale folded into dK: dS was stored without it).  A dedicated barrier:
-    // these warps skip mma_done phases, so a parity wait on it could be satisfied by an older phase.
-    // The exp group writes dV, the dS group dK; warp (quadrant, h) owns 32 of the 64 columns.
-    tc::mbar_wait(fin_done, 0);
-    tc::tc_fence_after();
-    {
-      const uint32_t tsrc = exp_group ? tDV : tDK;
-      const float osc = exp_group ? 1.f : a.scale;
-      __nv_bfloat16* g = (exp_group ? a.dv : a.dk) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + hh * 32;
-      uint32_t r[32];
-      tc::tmem_ld_32x32b_x32(tsrc + lane_off + hh * 32, r);
-      tc::tmem_ld_wait();
-      if (kvi < a.N) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
-          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
-          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * osc, __uint_as_float(r[u * 8 + 5]) * osc);
-          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * osc, __uint_as_float(r[u * 8 + 7]) * osc);
-          reinterpret_cast<uint4*>(g)[u] = v;
+          tc::tmem_st_wait();
+          tc::fence_proxy_async();
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(ds_ready);
+          if (warp == 8) BWD_TRACE(7, g);
         }
       }
     }
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (warp == kTMA) BWD_TRACE(14, 0);
   if (warp == kMMA) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 512);
@@ -1477,6 +1527,8 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.ld_g = ld_g;
   a.sb_g = sb_g;
   a.causal = causal;
+  a.nkt = (N + BT - 1) / BT;
+  a.items = B * H * a.nkt;
   a.trace = nullptr;
   if (const char* tr = getenv("AVB_ATTN_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
   a.dbg = getenv("AVB_ATTN_DBG") ? atoi(getenv("AVB_ATTN_DBG")) : 0;
@@ -1486,7 +1538,8 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     if (e != cudaSuccess) return avb::cuda_status(e, "attn_bwd smem attr");
     attr = true;
   }
-  dim3 grid((N + BT - 1) / BT, H, B);
+  // persistent: one CTA per SM walks work items blockIdx.x, +gridDim.x, ... (1 CTA/SM: TMEM 512 cols)
+  const int grid = std::min(a.items, avb::sm_count());
   attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, a);
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
   const int64_t threads = (int64_t)B * N * H * 8;

@@ -22,10 +22,14 @@ e1.record(); torch.cuda.synchronize()
 print("bwd ms", e0.elapsed_time(e1) / 3)
 t = tr.view(32, 16).cpu()
 split = bool(os.environ.get("AVB_ATTN_BWD_SPLIT"))
-t0 = int(t[0, 9 if split else 4])
+t0 = int(t[0, 9 if split else 13])
 names = ({0: "m:p_rdy", 1: "m:dV_iss", 2: "m:ds_rdy", 3: "m:dK_iss", 4: "m:dPS_iss", 9: "c:top", 5: "c:s_full",
           6: "c:p_arr", 7: "c:dp_full", 8: "c:ds_arr"} if split else
          {8: "m:wait_p", 0: "m:p_rdy", 9: "m:dV_iss", 10: "m:pt_rd", 11: "m:S_iss", 1: "m:ds_rdy",
           2: "m:dK,dP_iss", 12: "m:dQ_iss", 4: "e:top", 5: "e:s_full", 6: "d:dp_full", 7: "d:ds_arr"})
-for ii in range(13):
+for ii in list(range(3)) + [12]:
     print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in ((9, 5, 6, 0, 1, 7, 8, 2, 3, 4) if split else (4, 5, 6, 7, 8, 0, 9, 10, 11, 1, 2, 12)) if int(t[ii, e]) != 0))
+if not split:
+    print("kernel start->first step top", int(t[0, 4]) - t0, " last ds_arr -> kernel end", int(t[0, 14]) - int(t[12, 7]),
+          " total", int(t[0, 14]) - t0)
+
