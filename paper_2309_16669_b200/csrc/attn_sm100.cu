@@ -390,8 +390,16 @@ constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
 
 #define BWD_TRACE(ev, ii)                                                                       \
   do {                                                                                          \
-    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && (ii) < 32) \
-      a.trace[(ii) * 16 + (ev)] = clock64();                                                      \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && (ii) < 1024) \
+      a.trace[(ii) * 32 + (ev)] = clock64();                                                        \
+  } while (0)
+#define BWD_TRACE_NS(ev, ii)                                                                    \
+  do {                                                                                          \
+    if (a.trace && blockIdx.x == 0 && lane == 0 && (ii) < 1024) {                               \
+      uint64_t ns;                                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));                                    \
+      a.trace[(ii) * 32 + (ev)] = (long long)ns;                                                \
+    }                                                                                           \
   } while (0)
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -433,7 +441,8 @@ __device__ __forceinline__ BwdItem bwd_item(const BwdArgs& a, int w) {
 __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const __grid_constant__ CUtensorMap tmDQ, const BwdArgs a) {
+                    const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
+                    const __grid_constant__ CUtensorMap tmDV, const BwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
   auto sKb = [&](int it) { return smem + ((it & 1) ? B_SK2 : B_SK); };   // K double buffer (per work item)
@@ -455,7 +464,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   uint64_t* p_ready = s_full + 8;                // P_g^T stored in TMEM by every exp-group warp
   uint64_t* kv_tmem = s_full + 9;                // per item: K and V copied into TMEM (A operands of S^T / dP^T)
   uint64_t* pt_read = s_full + 10;               // the dS group has read P_g^T (S^T columns reusable)
-  uint64_t* k_free = s_full + 11;                // [2] per item: its dQ MMAs are done with that K buffer
+  uint64_t* kst_free = s_full + 11;              // [2] per item: its K buffer is free (dQ MMAs done, dK/dV staged out)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,6 +478,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     tc::tma_prefetch(&tmV);
     tc::tma_prefetch(&tmdO);
     tc::tma_prefetch(&tmDQ);
+    tc::tma_prefetch(&tmDK);
+    tc::tma_prefetch(&tmDV);
     tc::mbar_init(kv_full, 1);
     for (int s = 0; s < B_QD_STAGES; ++s) {
       tc::mbar_init(&qd_full[s], 1);
@@ -485,8 +496,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     tc::mbar_init(p_ready, kBwdCompute / 2);    // the exp group
     tc::mbar_init(kv_tmem, kBwdCompute / 2);    // the exp group
     tc::mbar_init(pt_read, kBwdCompute / 2);    // the dS group
-    tc::mbar_init(&k_free[0], 1);
-    tc::mbar_init(&k_free[1], 1);
+    tc::mbar_init(&kst_free[0], kBwdDrain);
+    tc::mbar_init(&kst_free[1], kBwdDrain);
     tc::fence_barrier_init();
   }
   if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         const BwdItem t = bwd_item(a, w);
         const int64_t bh = (int64_t)t.b * a.H + t.h;
         if (it >= 1) tc::mbar_wait(kv_tmem, (it - 1) & 1);                  // V_{it-1} copied out of sV
-        if (it >= 2) tc::mbar_wait(&k_free[it & 1], ((it >> 1) - 1) & 1);  // item it-2 done with this K buffer
+        if (it >= 2) tc::mbar_wait(&kst_free[it & 1], ((it >> 1) - 1) & 1);  // item it-2 done with this K buffer
         tc::mbar_arrive_expect_tx(kv_full, 32768);
         tc::tma_load_3d(sKb(it), &tmK, kv_full, t.h * HD, t.kt * BT, t.b);
         tc::tma_load_3d(sV, &tmV, kv_full, t.h * HD, t.kt * BT, t.b);
@@ -606,7 +617,6 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           BWD_TRACE(12, g);
           tc::umma_commit(mma_done);
           tc::umma_commit(&qd_empty[st]);
-          if (last) tc::umma_commit(&k_free[it & 1]);
         }
       }
     }
@@ -614,43 +624,68 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     // ------------------------------------------------------------ drain warps (one per TMEM lane quadrant)
     const int quad = warp & 3;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    int g = 0;
-    for (int w = blockIdx.x; w < a.items; w += stride) {
+    int g = 0, it = 0;
+    for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
       const BwdItem t = bwd_item(a, w);
       for (int ii = 0; ii < t.nq; ++ii, ++g) {
         const int pb = g & 1;
         tc::mbar_wait(mma_done, g & 1);   // dK_g / dQ_g complete: dQ_g final, dS^T_g buffer free
         tc::tc_fence_after();
         if (ii + 1 == t.nq) {
-          // the item's dK / dV are final: out as bf16 (softmax scale folded into dK: dS was stored
-          // without it), then hand the accumulators to the next item
-          const int kvi = t.kt * BT + quad * 32 + lane;
-#pragma unroll 1
-          for (int which = 0; which < 2; ++which) {
-            const uint32_t tsrc = which ? tDK : tDV;
-            const float osc = which ? a.scale : 1.f;
-            __nv_bfloat16* gp = (which ? a.dk : a.dv) + (int64_t)t.b * a.sb_g + (int64_t)kvi * a.ld_g + t.h * HD;
+          // the item's dK / dV are final and its K buffer is free (last dQ MMA done): bf16 tiles
+          // staged there (this warp's 32 rows = 4 KB, 128B-swizzled) and written by TMA stores,
+          // so no warp waits on scattered global stores.  dK (softmax scale folded in: dS was
+          // stored without it) is held as bf16 pairs while dV's staging is read out.
+          uint8_t* stg = sKb(it) + quad * 4096;
+          uint32_t kb[32];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              uint32_t r[32];
-              tc::tmem_ld_32x32b_x32(tsrc + lane_off + hh * 32, r);
-              tc::tmem_ld_wait();
-              if (kvi < a.N) {
+          for (int hh = 0; hh < 4; ++hh) {   // dV cols [0,32) [32,64), then dK
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32((hh < 2 ? tDV : tDK) + lane_off + (hh & 1) * 32, r);
+            tc::tmem_ld_wait();
+            const float osc = hh < 2 ? 1.f : a.scale;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  uint4 v;
-                  v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
-                  v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
-                  v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * osc, __uint_as_float(r[u * 8 + 5]) * osc);
-                  v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * osc, __uint_as_float(r[u * 8 + 7]) * osc);
-                  reinterpret_cast<uint4*>(gp + hh * 32)[u] = v;
-                }
-              }
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t p = pack_bf16x2(__uint_as_float(r[2 * e]) * osc, __uint_as_float(r[2 * e + 1]) * osc);
+              if (hh < 2) r[e] = p; else kb[(hh & 1) * 16 + e] = p;
+            }
+            if (hh < 2) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<uint4*>(stg + lane * 128 + ((((hh & 1) * 4 + u) ^ (lane & 7)) << 4)) =
+                    make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
             }
           }
           tc::tc_fence_before();
+          tc::fence_proxy_async();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(acc_free);
+          if (lane == 0) {
+            tc::mbar_arrive(acc_free);   // the next item's first dV / dK MMA may overwrite them
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tmDV)),
+                         "r"(smem_u32(stg)), "r"(t.h * HD), "r"(t.kt * BT + quad * 32), "r"(t.b)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((u ^ (lane & 7)) << 4)) =
+                make_uint4(kb[4 * u], kb[4 * u + 1], kb[4 * u + 2], kb[4 * u + 3]);
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tmDK)),
+                         "r"(smem_u32(stg)), "r"(t.h * HD), "r"(t.kt * BT + quad * 32), "r"(t.b)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            tc::mbar_arrive(&kst_free[it & 1]);   // the TMA may load K of item it+2 here
+          }
+          __syncwarp();
+          if (warp == kDrain0) BWD_TRACE(23, g);
         }
         if (a.dbg & 1) {
           __syncwarp();
@@ -730,16 +765,22 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(kv_tmem);
+        if (warp == 0) BWD_TRACE(16, g);
+        if (warp == 4) BWD_TRACE(17, g);
       }
       for (int ii = 0; ii < t.nq; ++ii, ++g) {
         const int i = t.i0 + ii, st = g % B_QD_STAGES;
         const int q0 = i * BT;
-        if (warp == 0) BWD_TRACE(4, g);
+        if (warp == 0) {
+          BWD_TRACE(4, g);
+          BWD_TRACE_NS(15, g);
+        }
         if (exp_group) {
           tc::mbar_wait(s_full, g & 1);
           tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -lse*log2e landed
           tc::tc_fence_after();
           if (warp == 0) BWD_TRACE(5, g);
+          if (warp == 4) BWD_TRACE(19, g);
 #pragma unroll 1
           for (int cc = 0; cc < 2; ++cc) {
             const int c = 2 * hh + cc;
@@ -781,6 +822,9 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(p_ready);
+          if (warp == 0) BWD_TRACE(18, g);
+          if (warp == 4) BWD_TRACE(20, g);
+          if (warp == 7) BWD_TRACE(21, g);
         } else {
           tc::mbar_wait(p_ready, g & 1);
           tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -delta landed
@@ -1509,7 +1553,9 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     attn_bwd_dq_kernel<<<grid, 32 * kSplitWarps, SB_SMEM, st>>>(mq, mk, mv, mdo, sa);
     return avb::launch_status("avb_attn_bwd (dq)");
   }
-  CUtensorMap mdq;
+  CUtensorMap mdq, mdk, mdv;
+  if ((s = make_maps(&mdk, dk, B, H, N, ld_g, sb_g, 32))) return s;   // dK / dV TMA stores: 32-row boxes
+  if ((s = make_maps(&mdv, dv, B, H, N, ld_g, sb_g, 32))) return s;
   if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
                                  (uint64_t)N * H * HD, 32, 32, 1, 128)))
     return s;
@@ -1540,7 +1586,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   }
   // persistent: one CTA per SM walks work items blockIdx.x, +gridDim.x, ... (1 CTA/SM: TMEM 512 cols)
   const int grid = std::min(a.items, avb::sm_count());
-  attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, a);
+  attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
