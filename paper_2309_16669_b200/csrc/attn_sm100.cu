@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       }
     }
   } else if (warp == kMMA) {
-    if (lane == 0) {
+    {   // all 32 lanes run the issue loop (warp-uniform values); one elected lane issues
       constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
       constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV (A = P^T in TMEM), dK: B (dO / Q) MN-major
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
@@ -551,15 +551,15 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         const uint32_t aQ = smem_u32(sQD + st * 32768);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ts(tST, tK + 8 * kk, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
-        tc::umma_commit(s_full);
+          tc::umma_f16_ts_w(tST, tK + 8 * kk, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_commit_w(s_full);
       };
       auto issue_dp = [&](int gg) {     // dP_gg^T = V dO_gg^T, V (A) from TMEM (qd_full(gg) already observed)
         const uint32_t aDO = smem_u32(sQD + (gg % B_QD_STAGES) * 32768) + 16384;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ts(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
-        tc::umma_commit(dp_full);
+          tc::umma_f16_ts_w(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_commit_w(dp_full);
       };
       int g = 0, it = 0;
       for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           BWD_TRACE(0, g);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)     // dV += P^T dO: K step kk = queries [16kk, 16kk+16) = chunk kk/2
-            tc::umma_f16_ts(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024),
+            tc::umma_f16_ts_w(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024),
                             idG, (acc | kk) ? 1u : 0u);
           BWD_TRACE(9, g);
           tc::mbar_wait(pt_read, g & 1);     // the dS group holds P_g in registers: S^T columns are free
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           BWD_TRACE(1, g);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)     // dK += dS^T Q (A = dS^T from TMEM)
-            tc::umma_f16_ts(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024),
+            tc::umma_f16_ts_w(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024),
                             idG, (acc | kk) ? 1u : 0u);
           if (nxt) issue_dp(g + 1);
           if (g >= 1) tc::mbar_wait(dq_free, (g - 1) & 1);   // dQ_{g-1} read out of TMEM
@@ -612,11 +612,11 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
             // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
             // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
             const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
-            tc::umma_f16_ss(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
+            tc::umma_f16_ss_w(tDQ, dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
           }
           BWD_TRACE(12, g);
-          tc::umma_commit(mma_done);
-          tc::umma_commit(&qd_empty[st]);
+          tc::umma_commit_w(mma_done);
+          tc::umma_commit_w(&qd_empty[st]);
         }
       }
     }

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
 }
 
 template <int NC, bool SUM>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
+__global__ void __launch_bounds__(256, (NC <= 3 ? 2 : 1)) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
                                                      const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, __nv_bfloat16* dx, int64_t lddx,
@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
   const int64_t nwarps = (int64_t)gridDim.x * 8;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < M; row += nwarps) {
     const float mu = mean[row], rs = rstd[row];
-    uint4 rx[NC], rd[NC];
+    // every load of the row (x, dy and the residual-stream gradient dx) issued up front: one
+    // memory round trip per row instead of two (the dx read does not depend on the row sums)
+    uint4 rx[NC], rd[NC], rp[NC];
     bool ok[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
       ok[k] = c < D;
       rx[k] = ok[k] ? *reinterpret_cast<const uint4*>(x + row * ldx + c) : make_uint4(0, 0, 0, 0);
       rd[k] = ok[k] ? *reinterpret_cast<const uint4*>(dy + row * lddy + c) : make_uint4(0, 0, 0, 0);
+      rp[k] = (ok[k] && accumulate) ? *reinterpret_cast<const uint4*>(dx + row * lddx + c) : make_uint4(0, 0, 0, 0);
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const __nv_bfloat16* __rest
       float xv[8], dv[8], pv[8], o[8];
       unpack8(rx[k], xv);
       unpack8(rd[k], dv);
-      unpack8(accumulate ? *reinterpret_cast<const uint4*>(dx + row * lddx + c) : make_uint4(0, 0, 0, 0), pv);
+      unpack8(rp[k], pv);
       const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
       const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
       const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
