@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(320, 2)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
+    {   // all 32 lanes run the issue loop (warp-uniform values); one elected lane issues
       constexpr uint32_t idS = tc::idesc_bf16_f32(128, FKB, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16_f32(128, 64, 0, 1);   // A = P from TMEM, B = V MN-major
       const uint32_t aQ = smem_u32(sQ);
@@ -181,17 +181,17 @@ __global__ void __launch_bounds__(320, 2)
         const uint32_t aK = smem_u32(sKV + (j % F_STAGES) * 16384);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tmem + 64 * g, tc::sdesc_sw128(aQ + g * 16384 + kk * 32, 16, 1024),
+          tc::umma_f16_ss_w(tmem + 64 * g, tc::sdesc_sw128(aQ + g * 16384 + kk * 32, 16, 1024),
                           tc::sdesc_sw128(aK + kk * 32, 16, 1024), idS, kk > 0);
-        tc::umma_commit(gb + 4 * g + 0);
+        tc::umma_commit_w(gb + 4 * g + 0);
       };
       auto issue_pv = [&](int g, int j) {
         const uint32_t aV = smem_u32(sKV + (j % F_STAGES) * 16384 + 8192);
 #pragma unroll
         for (int kk = 0; kk < FKB / 16; ++kk)
-          tc::umma_f16_ts(tmem + 128 + 64 * g, tmem + 64 * g + kk * 8,
+          tc::umma_f16_ts_w(tmem + 128 + 64 * g, tmem + 64 * g + kk * 8,
                           tc::sdesc_sw128(aV + kk * 2048, 8192, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
-        tc::umma_commit(gb + 4 * g + 3);
+        tc::umma_commit_w(gb + 4 * g + 3);
       };
       tc::mbar_wait(q_full, 0);
       tc::mbar_wait(&kv_full[0], 0);
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(320, 2)
           issue_pv(g, j);
           if (more) issue_s(g, j + 1);
         }
-        tc::umma_commit(&kv_empty[j % F_STAGES]);
+        tc::umma_commit_w(&kv_empty[j % F_STAGES]);
       }
     }
   } else {
