@@ -201,6 +201,26 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "h"((uint16_t)0x3)
       : "memory");
 }
+// warp-collective forms (all lanes call with uniform operands; one elected lane issues)
+__device__ __forceinline__ void umma_f16_ss_cg2_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
 
 // Stage 32 rows x 32 bf16 (thread = row) into a 64B-swizzled 2 KB block and TMA-store it.
 template <int PENDING>
@@ -356,8 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kWMma) {
-    if (lane == 0 && leader) {
-      // ------------------------------------------------ MMA issuer (pair mode: the leader CTA only)
+    if (leader) {
+      // ------------------------------------------------ MMA issuer (pair mode: the leader CTA only);
+      // the whole warp runs the loop with uniform values, one elected lane issues each tcgen05 op
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -385,24 +406,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t da = da0 + soff + (uint64_t)((A_MN ? k * 2048 : k * 32) >> 4);
             const uint64_t db = db0 + soff + (uint64_t)((B_MN ? k * 2048 : k * 32) >> 4);
             if constexpr (PAIR) {
-              umma_f16_ss_cg2(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+              umma_f16_ss_cg2_w(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
               if (do_rs)   // ones tile: each CTA supplies 8 of the 16 B rows (all ones)
-                umma_f16_ss_cg2(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
+                umma_f16_ss_cg2_w(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
                                 (kb > kb0 || k > 0) ? 1u : 0u);
               continue;
             }
-            tc::umma_f16_ss(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            tc::umma_f16_ss_w(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
             if (do_rs)
-              tc::umma_f16_ss(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
+              tc::umma_f16_ss_w(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
                               (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          if (PAIR) umma_commit_pair(&empty[stage]); else tc::umma_commit(&empty[stage]);
+          if (PAIR) umma_commit_pair_w(&empty[stage]); else tc::umma_commit_w(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (PAIR) umma_commit_pair(&tfull[acc]); else tc::umma_commit(&tfull[acc]);
+        if (PAIR) umma_commit_pair_w(&tfull[acc]); else tc::umma_commit_w(&tfull[acc]);
       }
     }
   } else if (warp < kEpiWarps) {
