@@ -798,7 +798,9 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   // aux / store rings so TMA latency is covered while the epilogue streams 32-column chunks
   const bool heavy = BN == 256 && a_major == 0 && (g.tma_aux || (g.tma_out && epilogue == AVB_EPI_BIAS_GELU)) &&
                      !getenv("AVB_GEMM_NO_HEAVY");
-  if (pair && (!(heavy && g.tma_aux) || getenv("AVB_GEMM_PAIR_AUX"))) {   // aux-reading epilogues: single-CTA by default
+  // aux-reading epilogues: CTA pairs only when the mainloop is long enough to hide the aux stream
+  // (same-box: fc2 fwd + residual, K = 3072: 1208 -> 1355 TFLOP/s; K = 768 shapes 2-4 % slower)
+  if (pair && (!(heavy && g.tma_aux) || K >= 1536 || getenv("AVB_GEMM_PAIR_AUX"))) {
     g.num_m = (M + 2 * BM - 1) / (2 * BM);
     if (heavy && g.tma_aux) {
       if (b_major == 0) return launch<256, false, false, 1, true>(ta, tb, tcm, tx, g, st);

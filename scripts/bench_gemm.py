@@ -13,6 +13,8 @@ shapes = [  # name, M, N, K, a_mn, b_mn, epi
     ("fc1_fwd_gelu", M, 4 * D, D, False, False, ops.EPI_BIAS_GELU),
     ("fc2_dgrad_dgelu", M, 4 * D, D, False, True, ops.EPI_DGELU),
     ("fc2_fwd", M, D, 4 * D, False, False, ops.EPI_BF16),
+    ("fc2_fwd_res", M, D, 4 * D, False, False, ops.EPI_BF16),
+    ("proj_fwd_res", M, D, D, False, False, ops.EPI_BF16),
     ("fc1_dgrad", M, D, 4 * D, False, True, ops.EPI_BF16),
     ("fc2_dgrad", M, 4 * D, D, False, True, ops.EPI_BF16),
     ("fc1_wgrad", 4 * D, D, M, True, True, ops.EPI_F32_ACCUM),
@@ -34,6 +36,8 @@ for name, m, n, k, amn, bmn, epi in shapes:
         kw = dict(bias=torch.randn(n, device="cuda"), aux_out=torch.empty((m, n), device="cuda", dtype=torch.bfloat16))
     if epi == ops.EPI_DGELU:
         kw = dict(aux=torch.randn((m, n), device="cuda").to(torch.bfloat16))
+    if name.endswith("_res"):   # bias + residual add (the training step's proj / fc2 forward)
+        kw = dict(bias=torch.randn(n, device="cuda"), aux=torch.randn((m, n), device="cuda").to(torch.bfloat16))
     f = lambda: ops.gemm(A, B, a_mn=amn, b_mn=bmn, out=out, epilogue=epi, split_k=split, **kw)
     for _ in range(3): f()
     torch.cuda.synchronize()
