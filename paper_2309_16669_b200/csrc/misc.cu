@@ -167,6 +167,35 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
   }
 }
 
+// Same update, four parameters per thread (16-byte p/g/m/v, 4-byte mask, 8-byte bf16 shadow):
+// the optimizer step is a pure HBM stream (31 B/param), so every access is vectorised.
+__global__ void adamw_vec4_kernel(float4* __restrict__ p, const float4* __restrict__ g, float4* __restrict__ m,
+                                  float4* __restrict__ v, uint2* __restrict__ pb, const uchar4* __restrict__ mask,
+                                  int64_t n4, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                                  float gscale) {
+  const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 g4 = g[i], m4 = m[i], v4 = v[i], p4 = p[i];
+    const uchar4 k4 = mask ? mask[i] : make_uchar4(1, 1, 1, 1);
+    const float gi[4] = {g4.x, g4.y, g4.z, g4.w}, mi0[4] = {m4.x, m4.y, m4.z, m4.w};
+    const float vi0[4] = {v4.x, v4.y, v4.z, v4.w}, pi0[4] = {p4.x, p4.y, p4.z, p4.w};
+    const uint8_t ki[4] = {k4.x, k4.y, k4.z, k4.w};
+    float mo[4], vo[4], po[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gg = gi[e] * gscale;
+      mo[e] = b1 * mi0[e] + (1.f - b1) * gg;
+      vo[e] = b2 * vi0[e] + (1.f - b2) * gg * gg;
+      const float wdi = ki[e] ? wd : 0.f;
+      po[e] = pi0[e] * (1.f - lr * wdi) - lr * (mo[e] * ib1) / (sqrtf(vo[e] * ib2) + eps);
+    }
+    m[i] = make_float4(mo[0], mo[1], mo[2], mo[3]);
+    v[i] = make_float4(vo[0], vo[1], vo[2], vo[3]);
+    p[i] = make_float4(po[0], po[1], po[2], po[3]);
+    if (pb) pb[i] = make_uint2(pack_bf16x2(po[0], po[1]), pack_bf16x2(po[2], po[3]));
+  }
+}
+
 __global__ void cast_bf16_kernel(const float* __restrict__ s, __nv_bfloat16* __restrict__ d, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = __float2bfloat16_rn(s[i]);
@@ -316,9 +345,27 @@ extern "C" int avb_adamw(float* p, const float* g, float* m, float* v, void* p_b
   if (n == 0) return AVB_OK;
   AVB_CHECK_ARG(p && g && m && v, "null pointer");
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
-  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)avb::sm_count() * 8);
-  adamw_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(p, g, m, v, reinterpret_cast<__nv_bfloat16*>(p_bf16), decay_mask, n, lr,
-                                                           beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
+  auto al = [](const void* q, uintptr_t b) { return (reinterpret_cast<uintptr_t>(q) & (b - 1)) == 0; };
+  const bool vec = al(p, 16) && al(g, 16) && al(m, 16) && al(v, 16) && (!p_bf16 || al(p_bf16, 8)) &&
+                   (!decay_mask || al(decay_mask, 4));
+  int64_t done = 0;
+  if (vec && n >= 4) {
+    const int64_t n4 = n / 4;
+    const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)avb::sm_count() * 8);
+    adamw_vec4_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(
+        reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g), reinterpret_cast<float4*>(m),
+        reinterpret_cast<float4*>(v), reinterpret_cast<uint2*>(p_bf16), reinterpret_cast<const uchar4*>(decay_mask),
+        n4, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
+    int s = avb::launch_status("avb_adamw");
+    if (s) return s;
+    done = n4 * 4;
+  }
+  if (done == n) return AVB_OK;
+  const int64_t r = n - done;   // unaligned buffers, or the < 4 element tail
+  const int blocks = (int)std::min<int64_t>((r + 255) / 256, (int64_t)avb::sm_count() * 8);
+  adamw_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(
+      p + done, g + done, m + done, v + done, p_bf16 ? reinterpret_cast<__nv_bfloat16*>(p_bf16) + done : nullptr,
+      decay_mask ? decay_mask + done : nullptr, r, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
   return avb::launch_status("avb_adamw");
 }
 

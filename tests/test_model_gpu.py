@@ -54,13 +54,15 @@ def test_finetune_step_matches_oracle(cfg, B, C):
     assert not bad, bad
 
 
-def test_adamw_kernel_matches_torch():
-    n = 10_000
+@pytest.mark.parametrize("n,off", [(10_000, 0), (10_003, 0), (10_003, 1)])
+def test_adamw_kernel_matches_torch(n, off):
+    # off = 1: every buffer is a view one element in (not 16-byte aligned) -> scalar kernel;
+    # n = 10_003: vectorised body + scalar tail
     g0 = torch.Generator(device="cuda").manual_seed(3)
-    p = torch.randn(n, device="cuda", generator=g0)
+    p = torch.randn(n + off, device="cuda", generator=g0)[off:]
     grads = [torch.randn(n, device="cuda", generator=g0) for _ in range(3)]
-    m, v = torch.zeros_like(p), torch.zeros_like(p)
-    sh = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    m, v = torch.zeros(n + off, device="cuda")[off:], torch.zeros(n + off, device="cuda")[off:]
+    sh = torch.empty(n + off, dtype=torch.bfloat16, device="cuda")[off:]
     mask = (torch.arange(n, device="cuda") % 3 != 0).to(torch.uint8)
     tp_d = p.clone().requires_grad_(True)
     tp_n = p.clone().requires_grad_(True)
@@ -75,8 +77,10 @@ def test_adamw_kernel_matches_torch():
     assert torch.equal(sh, p.to(torch.bfloat16))
 
 
-def test_layernorm_and_colsum():
-    M, D = 1000, 768
+@pytest.mark.parametrize("M,D,acc", [(1000, 768, True), (1, 768, True), (1003, 256, False), (20011, 1024, True),
+                                     (4099, 512, False)])
+def test_layernorm_and_colsum(M, D, acc):
+    # ragged row counts (M % 8 != 0) exercise the partial last row block of the TMA-staged kernels
     g0 = torch.Generator(device="cuda").manual_seed(4)
     x = torch.randn(M, D, device="cuda", generator=g0).to(torch.bfloat16)
     gam = torch.randn(D, device="cuda", generator=g0)
@@ -89,11 +93,13 @@ def test_layernorm_and_colsum():
     dy = torch.randn(M, D, device="cuda", generator=g0).to(torch.bfloat16)
     ref.backward(dy.float())
     dx = torch.randn(M, D, device="cuda", generator=g0).to(torch.bfloat16)
+    if not acc:
+        dx.zero_()
     dx0 = dx.float().clone()
     dg = torch.zeros(D, device="cuda")
     db = torch.zeros(D, device="cuda")
     csum = torch.zeros(D, device="cuda")
-    ops.layernorm_bwd(dy, x, gam, mu, rs, dx, dg, db, accumulate=True, dx_colsum=csum)
+    ops.layernorm_bwd(dy, x, gam, mu, rs, dx, dg, db, accumulate=acc, dx_colsum=csum)
     assert rel(dx.float() - dx0, xf.grad) < 2e-2
     assert rel(csum, dx.float().sum(0)) < 1e-4
     assert rel(dg, gf.grad) < 1e-3 and rel(db, bf.grad) < 1e-3
