@@ -402,7 +402,6 @@ constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
     }                                                                                           \
   } while (0)
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
   return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
