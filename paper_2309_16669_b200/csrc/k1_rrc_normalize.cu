@@ -800,15 +800,37 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   uint8_t* ring = reinterpret_cast<uint8_t*>(rowtab + p.H);
   const size_t stage_stride = (size_t)p.fpc * p.slot_bytes;
 
-  // ---- per-source-row push table: weights of the NOPEN open output rows, rows completed after it
+  // ---- per-source-row push table: weights of the NOPEN open output rows, rows completed after it.
+  // Built per output row (one fp64 normalisation per row, the same math and summation order as
+  // k1_row_weight, so the weights are bit-identical) and scattered into the source rows it spans.
+  float* rowtab_f = reinterpret_cast<float*>(rowtab);
   for (int y = tid; y < ch; y += blockDim.x) {
     const int base = k1_rows_done(ch, p.Ht, y);
     const int next = (y + 1 < ch) ? k1_rows_done(ch, p.Ht, y + 1) : p.Ht;
-    float w[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-    for (int q = 0; q < NOPEN; ++q)
-      if (base + q < p.Ht) w[q] = k1_row_weight(ch, p.Ht, base + q, y);
-    rowtab[y] = make_float4(w[0], w[1], w[2], __int_as_float(next - base));
+    rowtab[y] = make_float4(0.f, 0.f, 0.f, __int_as_float(next - base));
+  }
+  __syncthreads();
+  for (int i = tid; i < p.Ht; i += blockDim.x) {
+    const long long c2 = 2LL * p.Ht;
+    long long lo = floordiv_i64((long long)ch * (2 * i - 1) + p.Ht, c2);
+    long long hi = floordiv_i64((long long)ch * (2 * i + 3) + p.Ht, c2);
+    if (lo < 0) lo = 0;
+    if (hi > ch) hi = ch;
+    const double sc = static_cast<double>(ch) / p.Ht;
+    const double inv = 1.0 / sc;
+    const double cc = sc * (i + 0.5);
+    double tot = 0.0;
+    for (long long k = 0; k < hi - lo; ++k) {
+      const double d = fabs((lo + k + 0.5 - cc) * inv);
+      tot += d < 1.0 ? 1.0 - d : 0.0;
+    }
+    const double r = tot > 0.0 ? 1.0 / tot : 0.0;
+    for (long long k = 0; k < hi - lo; ++k) {
+      const int y = (int)(lo + k);
+      const int q = i - k1_rows_done(ch, p.Ht, y);   // slot of row i among the rows open at y
+      const double d = fabs((lo + k + 0.5 - cc) * inv);
+      if (q >= 0 && q < NOPEN) rowtab_f[4 * y + q] = static_cast<float>((d < 1.0 ? 1.0 - d : 0.0) * r);
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < V4_RS; ++s) {
@@ -927,6 +949,13 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   const uint8_t* slot0 = slot;
   const int lane = tid & 31;
 
+  const float2 sc2[3] = {make_float2(p.scale[0], p.scale[0]), make_float2(p.scale[1], p.scale[1]),
+                         make_float2(p.scale[2], p.scale[2])};
+  const float2 bi2[3] = {make_float2(p.bias[0], p.bias[0]), make_float2(p.bias[1], p.bias[1]),
+                         make_float2(p.bias[2], p.bias[2])};
+  // the row loop, instantiated per (output dtype, paired store): no per-emission dtype branches
+  auto rows_loop = [&](auto bf16_tag, auto pair_tag) {
+  constexpr bool BF16 = decltype(bf16_tag)::value, PAIR = decltype(pair_tag)::value;
   float2 acc[NOPEN][3];
 #pragma unroll
   for (int q = 0; q < NOPEN; ++q)
@@ -963,11 +992,11 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
       if (active) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const float2 v = ffma2(acc[0][c], make_float2(p.scale[c], p.scale[c]), make_float2(p.bias[c], p.bias[c]));
+          const float2 v = ffma2(acc[0][c], sc2[c], bi2[c]);
           const int oc = rowoff + c * cstride;
-          if (bf16) {
+          if constexpr (BF16) {
             __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dbase) + oc;
-            if (pair_store) {
+            if constexpr (PAIR) {
               *reinterpret_cast<uint32_t*>(d) = pack_bf16x2(v.x, v.y);
             } else {
               d[0] = __float2bfloat16_rn(v.x);
@@ -975,7 +1004,7 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
             }
           } else {
             float* d = reinterpret_cast<float*>(dbase) + oc;
-            if (pair_store) {
+            if constexpr (PAIR) {
               *reinterpret_cast<float2*>(d) = v;
             } else {
               d[0] = v.x;
@@ -992,6 +1021,14 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
       for (int c = 0; c < 3; ++c) acc[NOPEN - 1][c] = make_float2(0.f, 0.f);
       if (++rph == ph_rows) { rph = 0; rowoff += big_step; } else { rowoff += small_step; }
     }
+  }
+  };
+  if (bf16) {
+    if (pair_store) rows_loop(std::true_type{}, std::true_type{});
+    else rows_loop(std::true_type{}, std::false_type{});
+  } else {
+    if (pair_store) rows_loop(std::false_type{}, std::true_type{});
+    else rows_loop(std::false_type{}, std::false_type{});
   }
 }
 
