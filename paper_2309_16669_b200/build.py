@@ -27,7 +27,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-Xptxas", "-v" if os.environ.get("AVB_PTXAS_VERBOSE") else "-O3",
-          "-I" + os.path.join(ROOT, "include")]
+          "-I" + os.path.join(ROOT, "include")] + os.environ.get("AVB_NVCC_DEFS", "").split()
+# AVB_NVCC_DEFS: extra defines for debug builds, e.g. "-DAVB_ATTN_TRACE_HOOKS" (build with clean=True)
 
 
 def _deps(src: str) -> list[str]:

@@ -94,9 +94,23 @@ struct FwdArgs {
   int64_t ld_o, sb_o;
   float* lse;
   int causal;
+  long long* trace;   // debug: per-tile clock64 events of CTA (0,0,0) (AVB_ATTN_FTRACE), else null
 };
 
-constexpr int FKB = 64;                               // key tile
+constexpr int FKB = 64;
+// Debug timelines (scripts/trace_attn_{fwd,bwd}.py) are compiled in only with
+// -DAVB_ATTN_TRACE_HOOKS (AVB_NVCC_DEFS at build time): the checks cost ~6 % in the forward.
+#ifdef AVB_ATTN_TRACE_HOOKS
+#define FWD_TRACE(ev, j)                                                                              \
+  do {                                                                                                \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && (j) < 64)    \
+      a.trace[(j) * 16 + (ev)] = clock64();                                                           \
+  } while (0)
+#else
+#define FWD_TRACE(ev, j) \
+  do {                   \
+  } while (0)
+#endif                               // key tile
 constexpr int F_STAGES = 4;
 constexpr int F_SQ = 0;                               // 2 Q tiles (A, B) x 16 KB
 constexpr int F_SKV = 32768;                          // F_STAGES x (K 8 KB + V 8 KB)
@@ -167,6 +181,7 @@ __global__ void __launch_bounds__(320, 2)
       for (int j = 0; j < nkv; ++j) {
         const int st = j % F_STAGES;
         tc::mbar_wait(&kv_empty[st], ((j / F_STAGES) & 1) ^ 1);
+        FWD_TRACE(9, j);
         tc::mbar_arrive_expect_tx(&kv_full[st], 16384);
         tc::tma_load_3d(sKV + st * 16384, &tmK, &kv_full[st], h * HD, j * FKB, b);
         tc::tma_load_3d(sKV + st * 16384 + 8192, &tmV, &kv_full[st], h * HD, j * FKB, b);
@@ -201,10 +216,12 @@ __global__ void __launch_bounds__(320, 2)
         const bool more = j + 1 < nkv;
         if (more) tc::mbar_wait(&kv_full[(j + 1) % F_STAGES], ((j + 1) / F_STAGES) & 1);
         for (int g = 0; g < ng; ++g) {
+          FWD_TRACE(g == 0 ? 0 : 10, j);
           tc::mbar_wait(gb + 4 * g + 2, j & 1);    // P_g(j) in TMEM, S_g(j) consumed
           tc::tc_fence_after();
           issue_pv(g, j);
           if (more) issue_s(g, j + 1);
+          FWD_TRACE(g == 0 ? 1 : 2, j);
         }
         tc::umma_commit_w(&kv_empty[j % F_STAGES]);
       }
@@ -223,6 +240,7 @@ __global__ void __launch_bounds__(320, 2)
       float m_run = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         tc::mbar_wait(s_full, j & 1);
+        if (quad == 0) FWD_TRACE(g == 0 ? 3 : 7, j);
         tc::tc_fence_after();
         const int kv0 = j * FKB;
         int lim = a.N - kv0;
@@ -254,8 +272,10 @@ __global__ void __launch_bounds__(320, 2)
         const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
                                fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
         const float m_new = fmaxf(m_run, mx * a.scale_log2);
+        if (quad == 0 && g == 0) FWD_TRACE(4, j);
         if (j > 0) {
           tc::mbar_wait(o_full, (j - 1) & 1);  // PV(j-1) done: O stable, P buffer free
+          if (quad == 0 && g == 0) FWD_TRACE(5, j);
           tc::tc_fence_after();
         }
         // warp-uniform lazy rescale of the TMEM accumulator (tcgen05.ld/st are warp-collective)
@@ -317,6 +337,7 @@ __global__ void __launch_bounds__(320, 2)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);   // also frees S_g for S_g(j+1)
+        if (quad == 0) FWD_TRACE(g == 0 ? 6 : 8, j);
       }
       tc::mbar_wait(o_full, (nkv - 1) & 1);
       tc::tc_fence_after();
@@ -388,6 +409,7 @@ constexpr int kBwdDrain = 4;                 // dQ drain warps: one per TMEM lan
 constexpr int kBwdPolyFrom = AVB_BWD_POLY_FROM; // pairs e >= this (of 4) take the FMA-pipe exp2 (4: none -- measured best)
 constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
 
+#ifdef AVB_ATTN_TRACE_HOOKS
 #define BWD_TRACE(ev, ii)                                                                       \
   do {                                                                                          \
     if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && (ii) < 1024) \
@@ -401,6 +423,14 @@ constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
       a.trace[(ii) * 32 + (ev)] = (long long)ns;                                                \
     }                                                                                           \
   } while (0)
+#else
+#define BWD_TRACE(ev, ii) \
+  do {                    \
+  } while (0)
+#define BWD_TRACE_NS(ev, ii) \
+  do {                       \
+  } while (0)
+#endif
 
 
 __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
@@ -1479,6 +1509,8 @@ extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t
   a.sb_o = sb_o;
   a.lse = lse;
   a.causal = causal;
+  a.trace = nullptr;
+  if (const char* tr = getenv("AVB_ATTN_FTRACE")) a.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);

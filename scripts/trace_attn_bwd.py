@@ -1,4 +1,7 @@
-"""Per-step event timeline of K5 for CTA (0,0,0) on the config-4 shape (AVB_ATTN_TRACE debug hook)."""
+"""Per-step event timeline of K5 for CTA (0,0,0) on the config-4 shape (AVB_ATTN_TRACE debug hook).
+Needs a build with the hooks compiled in:
+  AVB_NVCC_DEFS=-DAVB_ATTN_TRACE_HOOKS python -c "from paper_2309_16669_b200 import build as B; B.build(clean=True)"
+"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
