@@ -716,6 +716,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           __syncwarp();
           if (warp == kDrain0) BWD_TRACE(23, g);
         }
+#ifdef AVB_ATTN_TRACE_HOOKS
         if (a.dbg & 1) {
           __syncwarp();
           if (lane == 0) {
@@ -724,6 +725,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           }
           continue;
         }
+#endif
         uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
