@@ -404,9 +404,10 @@ static_assert(B_SMEM <= 232448, "attn bwd smem");
 constexpr int kBwdCompute = 16;              // compute warps: 4 per TMEM lane quadrant (one 32-query chunk each)
 constexpr int kBwdDrain = 4;                 // dQ drain warps: one per TMEM lane quadrant
 #ifndef AVB_BWD_POLY_FROM
-#define AVB_BWD_POLY_FROM 4
+#define AVB_BWD_POLY_FROM 3
 #endif
-constexpr int kBwdPolyFrom = AVB_BWD_POLY_FROM; // pairs e >= this (of 4) take the FMA-pipe exp2 (4: none -- measured best)
+constexpr int kBwdPolyFrom = AVB_BWD_POLY_FROM; // pairs e >= this (of 4) take the FMA-pipe exp2: 1 of 4
+                                                // (same-box sweep 1/2/3/4: 1.94 / 1.80 / 1.75 / 1.79 ms)
 constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
 
 #ifdef AVB_ATTN_TRACE_HOOKS
