@@ -57,9 +57,19 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;               // 16 KB
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;   // 32 KB (BN=256), 16 KB per CTA of a pair
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = PAIR ? (EK == 0 ? 5 : (EK == 1 ? 4 : 5)) : ((BN == 256) ? (EK ? 3 : 4) : 6);
+// pair-mode plain-epilogue pipeline depth / store slots (compile-time tuning hooks; same-box sweep
+// after the issue fix: 6/2 = 5/4 within noise on the step's shapes, 4/4 2-6 % slower)
+#ifndef AVB_GEMM_PAIR_STAGES0
+#define AVB_GEMM_PAIR_STAGES0 5
+#endif
+#ifndef AVB_GEMM_PAIR_SSLOTS0
+#define AVB_GEMM_PAIR_SSLOTS0 4
+#endif
+  static constexpr int STAGES =
+      PAIR ? (EK == 0 ? AVB_GEMM_PAIR_STAGES0 : (EK == 1 ? 4 : 5)) : ((BN == 256) ? (EK ? 3 : 4) : 6);
   // EK 0: plain; 1: bf16 aux read (residual / GELU pre-activation); 2: second bf16 output (BIAS_GELU)
-  static constexpr int SSLOTS = EK == 0 ? (PAIR ? 4 : 2) : (EK == 1 ? 2 : 4);  // TMA-store staging slots per epilogue warp
+  static constexpr int SSLOTS =
+      EK == 0 ? (PAIR ? AVB_GEMM_PAIR_SSLOTS0 : 2) : (EK == 1 ? 2 : 4);  // TMA-store staging slots per epilogue warp
   static constexpr int XSLOTS = EK == 1 ? 3 : 1;                   // TMA-load aux ring slots per epilogue warp
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_BYTES = (SSLOTS + (EK == 1 ? XSLOTS : 0)) * kEpiWarps * 2048;  // 2 KB slots per epilogue warp
