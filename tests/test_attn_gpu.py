@@ -60,7 +60,11 @@ def test_fwd_packed_qkv_view():
     assert rel(o.view(B, N, H, 64), ro) < 2e-2
 
 
-@pytest.mark.parametrize("B,N,H", [(1, 128, 1), (2, 197, 3), (1, 785, 2), (1, 1569, 2), (2, 300, 1)])
+# (12, 785, 12) and (4, 1569, 6): more (key tile, head, clip) work items than SMs, so every CTA of
+# the persistent backward walks several items (cross-item pipelining, K double buffer, dK/dV
+# staged through the freed K buffer); (1, 2049, 1): the ViT-L/14 sequence length
+@pytest.mark.parametrize("B,N,H", [(1, 128, 1), (2, 197, 3), (1, 785, 2), (1, 1569, 2), (2, 300, 1), (1, 2049, 1),
+                                   (12, 785, 12), (4, 1569, 6)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_bwd(B, N, H, causal):
     qkv = packed(B, N, H, seed=7 + N)
