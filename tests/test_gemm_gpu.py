@@ -44,24 +44,30 @@ def test_gemm_layouts(a_mn, b_mn, M, N, K):
     assert rel(out16, ref) < 1e-2
 
 
-def test_epilogues():
-    M, N, K = 777, 768, 3072
-    A, B = mk(M, K, seed=3), mk(N, K, seed=4)
+# K = 768: aux-reading epilogues on single CTAs; K = 3072: on CTA pairs (the K >= 1536 rule);
+# b_mn: the dgrad form (B = W read MN-major), which is how the training step runs dGELU
+@pytest.mark.parametrize("K", [768, 3072])
+@pytest.mark.parametrize("b_mn", [False, True])
+def test_epilogues(K, b_mn):
+    M, N = 777, 768
+    A = mk(M, K, seed=3)
+    Bw = mk(K, N, seed=4) if b_mn else mk(N, K, seed=4)
+    Bt = Bw.float() if b_mn else Bw.float().t()   # [K, N]
     bias = torch.randn(N, device="cuda")
     res = mk(M, N, seed=5)
-    ref = A.float() @ B.float().t() + bias
-    out = ops.gemm(A, B, bias=bias, aux=res)
+    ref = A.float() @ Bt + bias
+    out = ops.gemm(A, Bw, b_mn=b_mn, bias=bias, aux=res)
     assert rel(out, ref + res.float()) < 1e-2
     pre = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    act = ops.gemm(A, B, bias=bias, epilogue=ops.EPI_BIAS_GELU, aux_out=pre)
+    act = ops.gemm(A, Bw, b_mn=b_mn, bias=bias, epilogue=ops.EPI_BIAS_GELU, aux_out=pre)
     assert rel(pre, ref) < 1e-2
     assert rel(act, ref * torch.sigmoid(1.702 * ref)) < 1e-2
-    dg = ops.gemm(A, B, epilogue=ops.EPI_DGELU, aux=pre)
+    dg = ops.gemm(A, Bw, b_mn=b_mn, epilogue=ops.EPI_DGELU, aux=pre)
     h = pre.float()
     s = torch.sigmoid(1.702 * h)
-    assert rel(dg, (A.float() @ B.float().t()) * (s + 1.702 * h * s * (1 - s))) < 1e-2
-    half = ops.gemm(A, B, epilogue=ops.EPI_F32, alpha=0.5)
-    assert rel(half, 0.5 * (A.float() @ B.float().t())) < 1e-4
+    assert rel(dg, (A.float() @ Bt) * (s + 1.702 * h * s * (1 - s))) < 1e-2
+    half = ops.gemm(A, Bw, b_mn=b_mn, epilogue=ops.EPI_F32, alpha=0.5)
+    assert rel(half, 0.5 * (A.float() @ Bt)) < 1e-4
 
 
 @pytest.mark.parametrize("splits", [1, 4, 13])
