@@ -96,6 +96,14 @@ int avb_rrc_normalize_tubelet(const uint8_t* src, int64_t B, int T, int H, int W
                               const float* mean3, const float* inv_std3, int out_dtype,
                               int tub_t, int tub_h, int tub_w, void* dst, void* stream);
 
+/* Test hook: pin K1's kernel choice for the calling process (path comparisons in the parity tests).
+ * AVB_K1_PATH_AUTO (default) picks identity / streaming / strip / generic by shape; GENERIC forces the
+ * any-stride kernel, STRIP the strip/band kernel.  Returns the previous setting. */
+#define AVB_K1_PATH_AUTO    0
+#define AVB_K1_PATH_GENERIC 1
+#define AVB_K1_PATH_STRIP   2
+int avb_k1_force_path(int path);
+
 /* Test hook: the device-computed tap table for one (crop, target) pair:
  * lo[tgt], hi[tgt] int32 device, weights[tgt*max_taps] float device. */
 int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_dev,
@@ -152,13 +160,25 @@ int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, int64_t ldx, 
 /* out[n] += sum_m X[m,n] (bias gradients); X bf16 [M, ldx]. */
 int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void* stream);
 
-/* tokens: x[b,0] = cls + pos[0]; x[b,1+n] = pe[b*Np+n] + pos[1+n]   (bf16 x, fp32 cls/pos) */
-int avb_tokens_fwd(const void* pe, const float* cls, const float* pos, void* x, int B, int Np, int D,
-                   void* stream);
-/* dpe = dx[:,1:] (nullable); dpos += sum_b dx; dcls += sum_b dx[:,0] */
-int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos, int B, int Np, int D, void* stream);
+/* Token assembly with the separable space-time position embedding of PAPER.md:727-729
+ * (PE[i] = PE_t[i] + PE_s):  patch n = t*S + s (t < Np/S temporal index, s < S spatial index),
+ *   x[b,0]   = cls + pos_s[0]
+ *   x[b,1+n] = pe[b*Np+n] + pos_s[1+s] + pos_t[t]
+ * pos_s fp32 [1+S, D] (CLIP's spatial table incl. the cls slot), pos_t fp32 [Np/S, D]; bf16 x. */
+int avb_tokens_fwd(const void* pe, const float* cls, const float* pos_s, const float* pos_t, void* x, int B,
+                   int Np, int S, int D, void* stream);
+/* dpe = dx[:,1:] (nullable); dcls += sum_b dx[:,0]; dpos_s[0] += sum_b dx[:,0];
+ * dpos_s[1+s] += sum_{b,t} dx[b,1+t*S+s]; dpos_t[t] += sum_{b,s} dx[b,1+t*S+s]  (each nullable) */
+int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos_s, float* dpos_t, int B, int Np, int S,
+                   int D, void* stream);
 
-/* softmax cross-entropy: loss += scale*sum_i (lse_i - z_i[y_i]); dlogits bf16 = scale*(softmax - onehot) */
+/* Tubelet patchify of normalised clips (the nn.Module path that takes [B,3,T,H,W] input; the training
+ * step gets the same rows straight from K1's tubelet layout): x bf16 contiguous [B,3,T,H,W] ->
+ * dst [B*Np, 3*tt*th*tw], Conv3d-weight feature order; tw even. */
+int avb_patchify(const void* x, int B, int T, int H, int W, int tt, int th, int tw, void* dst, void* stream);
+
+/* softmax cross-entropy: loss += scale*sum_i (lse_i - z_i[y_i]); dlogits bf16 = scale*(softmax - onehot).
+ * labels int32; a row whose label is outside [0, C) is ignored (no loss term, zero gradient row). */
 int avb_xent(const float* logits, int64_t ld, const int32_t* labels, int B, int C, float scale, float* loss,
              void* dlogits, int64_t ldd, void* stream);
 

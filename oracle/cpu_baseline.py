@@ -1,10 +1,12 @@
 """CPU baseline timings for bench.py (TEST/BASELINE INFRASTRUCTURE ONLY).
 
 The reference has no GPU path: its CPU implementation of K1's step is
-libswscale inside `convert_to_rgb` (codec.cpp:226-246), which needs FFmpeg
-headers to build (absent here).  The timed CPU baseline is
-therefore the torch fp32 restatement of the same algorithm (crop -> hflip ->
-antialiased bilinear -> normalize -> bf16), using every host thread.
+libswscale inside `convert_to_rgb` (codec.cpp:226-246).  Its own extension
+needs FFmpeg headers to build (absent here); the scaler itself
+is timed through ctypes in `oracle/swscale_ref.py`.  This module times the
+torch fp32 restatement of the same algorithm (crop -> hflip -> antialiased
+bilinear -> normalize -> bf16), using every host thread -- the `port` baseline
+carried beside every augment line.
 """
 
 from __future__ import annotations
@@ -51,9 +53,3 @@ def time_augment(boxes, flips, T: int, hw, budget_s: float, threads: int) -> tup
         if time.perf_counter() - t0 >= budget_s:
             break
     return n / (time.perf_counter() - t0), n
-
-
-def reference_train_line(args, world, cores):  # filled in with the encoder oracle
-    from oracle import vit_oracle
-
-    return vit_oracle.reference_train_line(args, world, cores)

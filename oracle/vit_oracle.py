@@ -2,8 +2,9 @@
 
 PARITY UNPINNED: the reference package has no encoder, attention or loss code and
 no tests for them; this restates PAPER.md directly:
-  * tubelet patch-embed: non-overlapping t x h x w cubes -> Linear(3*t*h*w, D), plus a
-    learned position table and a cls token (PAPER.md:258-259, :727-729, :1028);
+  * tubelet patch-embed: non-overlapping t x h x w cubes -> Linear(3*t*h*w, D), plus the
+    separable position embedding PE[t*S + s] = PE_t[t] + PE_s[1 + s] (cls: PE_s[0]) and a cls
+    token (PAPER.md:258-259, :727-729, :1028);
   * pre-LN ViT block: x += Proj(MHA(LN x)); x += FC2(QuickGELU(FC1(LN x)))
     (PAPER.md:259-260, :727; QuickGELU = CLIP's activation, an assumption);
   * attention softmax(QK^T/sqrt(d)) V computed densely here (the kernels are blockwise;
@@ -64,7 +65,10 @@ def encoder_forward(P: dict, patches, cfg, B, prefix="enc"):
     pe = patches @ P[f"{prefix}.pe.w"].t() + P[f"{prefix}.pe.b"]
     pe = pe.view(B, N - 1, D)
     cls = P[f"{prefix}.cls"].view(1, 1, D).expand(B, 1, D)
-    x = (torch.cat([cls, pe], 1) + P[f"{prefix}.pos"].view(1, N, D)).reshape(B * N, D)
+    ps, pt = P[f"{prefix}.pos_s"], P[f"{prefix}.pos_t"]                       # [1+S, D], [T', D]
+    S = ps.shape[0] - 1
+    pos = torch.cat([ps[:1], (pt.view(-1, 1, D) + ps[1:].view(1, S, D)).reshape(-1, D)], 0)
+    x = (torch.cat([cls, pe], 1) + pos.view(1, N, D)).reshape(B * N, D)
     return blocks(P, x, B, N, D, cfg.heads, cfg.depth, prefix)
 
 
@@ -105,50 +109,76 @@ def clip_loss(v, t, logit_scale):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_train_step_time(cfg, num_classes: int, clips: int, threads: int, steps: int = 1):
-    """Seconds per fp32 training step (fwd+bwd+AdamW) of the restatement on `clips` clips."""
-    torch.set_num_threads(threads)
-    gen = torch.Generator().manual_seed(0)
-    D, Fd, Hd, N = cfg.dim, cfg.patch_dim, cfg.hidden, cfg.tokens
-    P = {"enc.pe.w": (D, Fd), "enc.pe.b": (D,), "enc.cls": (D,), "enc.pos": (N, D)}
-    for l in range(cfg.depth):
-        g = f"enc.blk{l}"
+def _encoder_param_shapes(cfg, prefix="enc"):
+    D, Fd, Hd = cfg.dim, cfg.patch_dim, cfg.hidden
+    P = {f"{prefix}.pe.w": (D, Fd), f"{prefix}.pe.b": (D,), f"{prefix}.cls": (D,),
+         f"{prefix}.pos_s": (1 + cfg.spatial_tokens, D), f"{prefix}.pos_t": (cfg.temporal_tokens, D)}
+    P.update(_block_param_shapes(D, Hd, cfg.depth, prefix))
+    return P
+
+
+def _block_param_shapes(D, Hd, depth, prefix):
+    P = {}
+    for l in range(depth):
+        g = f"{prefix}.blk{l}"
         P.update({f"{g}.ln1.g": (D,), f"{g}.ln1.b": (D,), f"{g}.qkv.w": (3 * D, D), f"{g}.qkv.b": (3 * D,),
                   f"{g}.proj.w": (D, D), f"{g}.proj.b": (D,), f"{g}.ln2.g": (D,), f"{g}.ln2.b": (D,),
                   f"{g}.fc1.w": (Hd, D), f"{g}.fc1.b": (Hd,), f"{g}.fc2.w": (D, Hd), f"{g}.fc2.b": (D,)})
-    P.update({"head.ln.g": (D,), "head.ln.b": (D,), "head.w": (num_classes, D), "head.b": (num_classes,)})
-    params = {k: (torch.randn(*s, generator=gen) * 0.02).requires_grad_(True) for k, s in P.items()}
-    opt = torch.optim.AdamW(params.values(), lr=3e-5, weight_decay=0.01)
-    clips_t = torch.randn(clips, 3, cfg.frames, cfg.height, cfg.width, generator=gen)
-    labels = torch.randint(0, num_classes, (clips,), generator=gen)
-    times = []
-    for _ in range(steps + 1):
-        t0 = time.perf_counter()
-        x = encoder_forward(params, patchify(clips_t, cfg), cfg, clips)
-        loss, _ = head_loss(params, x, clips, N, labels, num_classes)
-        opt.zero_grad()
+    return P
+
+
+class CpuTrainStep:
+    """One fp32 training step (fwd + bwd + AdamW) of the restatement on the host cores.
+
+    kind "finetune": config-4/5 encoder + cls head CE over `num_classes`;
+    kind "clip":     config-3 video + text towers + InfoNCE.
+    Built once (weights, optimizer, synthetic inputs); `step()` runs exactly one step.
+    """
+
+    def __init__(self, cfg, clips: int, threads: int, kind: str = "finetune", num_classes: int = 3806,
+                 tcfg=None, embed_dim: int = 256):
+        torch.set_num_threads(threads)
+        gen = torch.Generator().manual_seed(0)
+        self.cfg, self.clips, self.kind, self.C = cfg, clips, kind, num_classes
+        D = cfg.dim
+        P = _encoder_param_shapes(cfg)
+        if kind == "finetune":
+            P.update({"head.ln.g": (D,), "head.ln.b": (D,), "head.w": (num_classes, D), "head.b": (num_classes,)})
+        else:
+            self.tcfg = tcfg
+            P.update({"txt.tok": (tcfg.vocab, tcfg.dim), "txt.pos": (tcfg.context, tcfg.dim)})
+            P.update(_block_param_shapes(tcfg.dim, tcfg.hidden, tcfg.depth, "txt"))
+            P.update({"clip.vln.g": (D,), "clip.vln.b": (D,), "clip.vproj": (embed_dim, D),
+                      "clip.tln.g": (tcfg.dim,), "clip.tln.b": (tcfg.dim,), "clip.tproj": (embed_dim, tcfg.dim),
+                      "clip.logit_scale": (1,)})
+        self.params = {k: (torch.randn(*s, generator=gen) * 0.02).requires_grad_(True) for k, s in P.items()}
+        self.opt = torch.optim.AdamW(self.params.values(), lr=3e-5, weight_decay=0.01)
+        self.clips_t = torch.randn(clips, 3, cfg.frames, cfg.height, cfg.width, generator=gen)
+        self.labels = torch.randint(0, num_classes, (clips,), generator=gen)
+        if kind == "clip":
+            self.tokens = torch.randint(0, tcfg.vocab, (clips, tcfg.context), generator=gen)
+            self.eot = torch.arange(clips) * tcfg.context + tcfg.context - 1
+
+    def step(self) -> float:
+        P, cfg = self.params, self.cfg
+        if self.kind == "finetune":
+            x = encoder_forward(P, patchify(self.clips_t, cfg), cfg, self.clips)
+            loss, _ = head_loss(P, x, self.clips, cfg.tokens, self.labels, self.C)
+        else:
+            loss = clip_forward_loss(P, patchify(self.clips_t, cfg), self.tokens, self.eot, cfg, self.tcfg)
+        self.opt.zero_grad()
         loss.backward()
-        opt.step()
+        self.opt.step()
+        return float(loss)
+
+
+def cpu_train_step_time(cfg, num_classes: int, clips: int, threads: int, steps: int = 1):
+    """Seconds per fp32 fine-tune step (min over `steps` after one untimed step)."""
+    st = CpuTrainStep(cfg, clips, threads, "finetune", num_classes)
+    st.step()
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        st.step()
         times.append(time.perf_counter() - t0)
-    return min(times[1:]) if steps else times[0]
-
-
-def reference_train_line(args, world, cores):
-    """`bench.py --impl reference --workload train`: CPU fp32 restatement of the config-4 step."""
-    from paper_2309_16669_b200.vit import CONFIG4_VIT_B_16F as cfg  # shapes only
-
-    clips = 1
-    for _ in range(max(0, args.warmup - 2)):
-        pass
-    sec = cpu_train_step_time(cfg, 3806, clips, cores, steps=max(1, min(args.steps, 2)))
-    v = clips / sec
-    return {"impl": "reference", "metric": "train clips/sec ViT-B/16 16x224^2 (fine-tune step)", "value": v,
-            "unit": "clips/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic clips, random-init weights",
-            "config": {"workload": "configs[3] ViT-B/16 fine-tune 16x224^2, tubelet 2x16x16 (N=1569)",
-                       "clips_per_step": clips},
-            "cpu_baseline": {"value": v, "unit": "clips/s", "cores": cores, "kind": "port",
-                             "sample": f"{clips} clip per step, torch fp32 restatement fwd+bwd+AdamW, "
-                                       f"{cores} threads"},
-            "e2e": {"value": v, "unit": "clips/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return min(times)

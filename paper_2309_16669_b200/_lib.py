@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("AVB_LIB", os.path.join(_HERE, "libavion_b200.so"))
 AVB_OK, AVB_E_ARG, AVB_E_BOX, AVB_E_UNSUPPORTED, AVB_E_CUDA = 0, 1, 2, 3, 4
 AVB_DTYPE_BF16, AVB_DTYPE_F32 = 0, 1
 AVB_LAYOUT_CTHW, AVB_LAYOUT_TCHW, AVB_LAYOUT_TUBELET = 0, 1, 2
+AVB_K1_PATH_AUTO, AVB_K1_PATH_GENERIC, AVB_K1_PATH_STRIP = 0, 1, 2
 
 _vp, _i32, _i64, _f32p = C.c_void_p, C.c_int, C.c_int64, C.POINTER(C.c_float)
 
@@ -31,14 +32,16 @@ EXPORTS: dict[str, tuple] = {
     "avb_rrc_normalize": (_i32, [_vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64,
                                  _vp, _vp, _vp, _i32, _i32, _f32p, _f32p, _i32, _i32, _vp, _vp]),
     "avb_rrc_taps": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32, _vp]),
+    "avb_k1_force_path": (_i32, [_i32]),
     "avb_rrc_normalize_tubelet": (_i32, [_vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                          _i32, _i32, _f32p, _f32p, _i32, _i32, _i32, _i32, _vp, _vp]),
     "avb_layernorm_fwd": (_i32, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, C.c_float, _vp]),
     "avb_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _i32,
                                  _vp]),
     "avb_colsum_accum": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
-    "avb_tokens_fwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp]),
-    "avb_tokens_bwd": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp]),
+    "avb_tokens_fwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "avb_tokens_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "avb_patchify": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "avb_xent": (_i32, [_vp, _i64, _vp, _i32, _i32, C.c_float, _vp, _vp, _i64, _vp]),
     "avb_adamw": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, _i32,
                          C.c_float, _vp]),

@@ -12,6 +12,7 @@ from __future__ import annotations
 import argparse
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -20,7 +21,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "avion")
+BUILD_ROOT = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libavion_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -28,7 +29,12 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-Xptxas", "-v" if os.environ.get("AVB_PTXAS_VERBOSE") else "-O3",
           "-I" + os.path.join(ROOT, "include")] + os.environ.get("AVB_NVCC_DEFS", "").split()
-# AVB_NVCC_DEFS: extra defines for debug builds, e.g. "-DAVB_ATTN_TRACE_HOOKS" (build with clean=True)
+# AVB_NVCC_DEFS: extra defines for debug builds, e.g. "-DAVB_ATTN_TRACE_HOOKS" or "-DAVB_DEBUG_KNOBS".
+# Objects live in a directory keyed by a hash of every flag, so a debug build never leaks into a
+# product build (the library itself is always relinked when the flag set changes).
+_FLAG_KEY = hashlib.sha1(" ".join([NVCC, *ARCH, *CFLAGS]).encode()).hexdigest()[:12]
+BUILD = os.path.join(BUILD_ROOT, "avion-" + _FLAG_KEY)
+STAMP = LIB + ".flags"
 
 
 def _deps(src: str) -> list[str]:
@@ -65,12 +71,15 @@ def build(clean: bool = False, verbose: bool = False) -> str:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
-    if _stale(LIB, objs):
+    stamp_ok = os.path.exists(STAMP) and open(STAMP).read().strip() == _FLAG_KEY
+    if _stale(LIB, objs) or not stamp_ok:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcuda"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         os.replace(LIB + ".tmp", LIB)
+        with open(STAMP, "w") as fh:
+            fh.write(_FLAG_KEY + "\n")
     return LIB
 
 

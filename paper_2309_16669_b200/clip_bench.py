@@ -89,7 +89,35 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     flops = B * world * 3.0 * (vc.forward_flops_per_clip() + 2.0 * tcfg.context * tcfg.dim * tcfg.dim * 12 *
                                 tcfg.depth + 4.0 * tcfg.context ** 2 * tcfg.dim * tcfg.depth)
     pk, src = peaks()
-    return {
+    # breakdown pass after the timed region: the dominant kernel's achieved rate = the roofline
+    from .train_bench import instrumented_pass
+
+    nb = 0 if args.no_breakdown else 2
+    fam, lps = instrumented_pass(step, nb)
+    roof = None
+    if fam:
+        N, Hh = vc.tokens, vc.heads
+        att_f = 4.0 * B * Hh * N * N * 64
+        cands = {}
+        for k, v in fam.items():
+            if k.startswith("gemm:"):
+                dims = k.split(":")[1].split("/")[0].split("x")
+                cands[k] = (v["total_ms"] / nb, 2.0 * int(dims[0]) * int(dims[1]) * int(dims[2]) / (v["avg_ms"] / 1e3))
+        # video-tower attention launches: the fwd/bwd families mix video (N=785) and text (L=77) layers,
+        # the video ones dominate (12 x 785^2 vs 12 x 77^2 per clip)
+        if "attn_bwd" in fam:
+            cands["attn_bwd"] = (fam["attn_bwd"]["total_ms"] / nb,
+                                 2 * att_f * vc.depth / (fam["attn_bwd"]["total_ms"] / nb / 1e3))
+        if "attn_fwd" in fam:
+            cands["attn_fwd"] = (fam["attn_fwd"]["total_ms"] / nb,
+                                 att_f * vc.depth / (fam["attn_fwd"]["total_ms"] / nb / 1e3))
+        dom = max(cands, key=lambda k: cands[k][0])
+        ach = cands[dom][1] / 1e12
+        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": None,
+                "share_of_step": cands[dom][0] / ms,
+                "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
+    line = {
         "metric": "train pairs/sec ViT-B/16 CLIP dual encoder 4x224^2, InfoNCE over the global batch",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -100,4 +128,24 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "pairs/s",
                 "h2d_bytes_per_step": int(host.numel() + tok_h.numel() * 4), "d2h_bytes_per_step": 4},
         "clocks": clocks, "loss": float(loss_h.item()),
+        "roofline": roof,
+        "kernels": {k: v for k, v in fam.items() if ":" not in k},
+        "gpu_launches": (lps * args.steps) if lps else None,
     }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import os
+
+        from oracle import vit_oracle as VO
+
+        cores = os.cpu_count() or 1
+        st = VO.CpuTrainStep(vc, 2, cores, kind="clip", tcfg=tcfg)
+        st.step()
+        import time
+
+        t0 = time.perf_counter()
+        st.step()
+        sec = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": 2.0 / sec, "unit": "pairs/s", "cores": cores, "kind": "port",
+                                "sample": "2 pairs, one fp32 CLIP dual-encoder fwd+bwd+AdamW step of the torch "
+                                          "restatement (oracle/vit_oracle.py), all host threads"}
+    return line

@@ -992,490 +992,6 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
   *reinterpret_cast<uint4*>(dq + b * sb + (int64_t)n * ld + h * HD + sub * 8) = v;
 }
 
-// ---------------------------------------------------------------------------------- backward, split (default)
-// Two kernels, each with every MMA operand it produces kept in TMEM (A-from-TMEM "TS" MMAs), so
-// shared memory only feeds the TMA-loaded tiles and nothing is reduced through L2:
-//
-//   K5a  dK/dV, one CTA per (128-key tile, head, clip), loop over query tiles i (TMEM lanes = keys):
-//        S_i^T = K Q_i^T into one of two TMEM buffers (issued two tiles ahead),
-//        compute: P_i^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 over the consumed S^T columns
-//                 -> p_ready;  dS_i^T = P^T (dP^T - delta) -> bf16 over the consumed dP^T columns
-//        MMA:     dV += P_i^T dO_i (TS), dK += dS_i^T Q_i (TS), then dP_{i+1}^T = V dO_{i+1}^T and
-//                 S_{i+2}^T, so the exp work of tile i+1 overlaps dV_i / dK_i / dP_{i+1}.
-//   K5b  dQ, one CTA per (128-query tile, head, clip), loop over key tiles j (TMEM lanes = queries):
-//        S_j = Q K_j^T (double-buffered), dP_j = dO V_j^T; compute: dS_j = P (dP - delta) -> bf16 over
-//        the consumed dP columns (lse / delta are per lane: no broadcasts); dQ += dS_j K_j (TS);
-//        dQ is written once, in bf16 (no fp32 accumulator, no atomics).
-constexpr int S_STAGES = 4;                              // Q/dO (K5a) or K/V (K5b) ring depth
-constexpr int SA_KV = 0;                                 // K5a: K 16K | V 16K
-constexpr int SA_QD = 32768;                             // 4 x (Q 16K + dO 16K)
-constexpr int SA_LD = SA_QD + S_STAGES * 32768;          // 4 x (-lse*log2e 512 | -delta 512)
-constexpr int SA_BAR = SA_LD + S_STAGES * 1024;
-constexpr int SA_SMEM = SA_BAR + 256;
-static_assert(SA_SMEM <= 232448, "attn bwd dkdv smem");
-constexpr int SB_QD = 0;                                 // K5b: Q 16K | dO 16K
-constexpr int SB_KV = 32768;                             // 4 x (K 16K + V 16K)
-constexpr int SB_BAR = SB_KV + S_STAGES * 32768;
-constexpr int SB_SMEM = SB_BAR + 256;
-static_assert(SB_SMEM <= 232448, "attn bwd dq smem");
-constexpr int kSplitCompute = 16;                        // compute warps: quadrant (w&3) x 32-column chunk (w>>2)
-constexpr int kSplitWarps = kSplitCompute + 2;
-
-struct BwdSplitArgs {
-  int B, H, N, Npad;
-  float scale, scale_log2;
-  const float* nlse2;     // -lse * log2(e)   [B*H, Npad]
-  const float* ndelta;    // -rowsum(dO * O)  [B*H, Npad]
-  __nv_bfloat16* g0;      // K5a: dk   K5b: dq
-  __nv_bfloat16* g1;      // K5a: dv
-  int64_t ld_g, sb_g;
-  int causal;
-  long long* trace;       // debug (AVB_ATTN_TRACE): per-step clock64 events of CTA (0,0,0)
-  int dbg;                // debug (AVB_ATTN_DBG): 2 = compute warps skip TMEM traffic and math
-};
-
-__global__ void __launch_bounds__(32 * kSplitWarps, 1)
-    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                         const BwdSplitArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
-  uint8_t* sK = smem + SA_KV;
-  uint8_t* sV = smem + SA_KV + 16384;
-  uint8_t* sQD = smem + SA_QD;
-  float* sLD = reinterpret_cast<float*>(smem + SA_LD);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SA_BAR);
-  uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;                  // [4]
-  uint64_t* qd_empty = bars + 1 + S_STAGES;      // [4]
-  uint64_t* s_full = bars + 1 + 2 * S_STAGES;    // [2]
-  uint64_t* p_ready = s_full + 2;
-  uint64_t* dp_full = s_full + 3;
-  uint64_t* ds_ready = s_full + 4;
-  uint64_t* fin_done = s_full + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int kv0 = kt * BT;
-  const int nq_all = (a.N + BT - 1) / BT;
-  const int i0 = a.causal ? kt : 0;
-  const int nq = nq_all - i0;
-  constexpr int kTMA = kSplitCompute, kMMA = kSplitCompute + 1;
-
-  if (warp == kTMA && lane == 0) {
-    tc::tma_prefetch(&tmQ);
-    tc::tma_prefetch(&tmK);
-    tc::tma_prefetch(&tmV);
-    tc::tma_prefetch(&tmdO);
-    tc::mbar_init(kv_full, 1);
-    for (int s = 0; s < S_STAGES; ++s) {
-      tc::mbar_init(&qd_full[s], 1);
-      tc::mbar_init(&qd_empty[s], 1);
-    }
-    tc::mbar_init(&s_full[0], 1);
-    tc::mbar_init(&s_full[1], 1);
-    tc::mbar_init(p_ready, kSplitCompute);
-    tc::mbar_init(dp_full, 1);
-    tc::mbar_init(ds_ready, kSplitCompute);
-    tc::mbar_init(fin_done, 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T buffer 0 | dP^T (dS^T packed over it) | dV | dK | S^T buffer 1; P^T packed over its S^T buffer
-  const uint32_t tDPT = tmem + 128, tDV = tmem + 256, tDK = tmem + 320;
-  auto tS = [&](int buf) { return tmem + (buf ? 384u : 0u); };
-  const int64_t bh = (int64_t)b * a.H + h;
-
-  if (warp == kTMA) {
-    if (lane == 0) {
-      tc::mbar_arrive_expect_tx(kv_full, 32768);
-      tc::tma_load_3d(sK, &tmK, kv_full, h * HD, kv0, b);
-      tc::tma_load_3d(sV, &tmV, kv_full, h * HD, kv0, b);
-      for (int ii = 0; ii < nq; ++ii) {
-        const int i = i0 + ii, st = ii % S_STAGES;
-        if (ii >= S_STAGES) tc::mbar_wait(&qd_empty[st], ((ii / S_STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
-        tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], h * HD, i * BT, b);
-        tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], h * HD, i * BT, b);
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                         smem_u32(sLD + st * 256)),
-                     "l"(a.nlse2 + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                         smem_u32(sLD + st * 256 + 128)),
-                     "l"(a.ndelta + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
-                     : "memory");
-      }
-    }
-  } else if (warp == kMMA) {
-    if (lane == 0) {
-      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T
-      constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV / dK: A in TMEM, B (dO / Q) MN-major
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto issue_s = [&](int ii) {
-        const int st = ii % S_STAGES;
-        tc::mbar_wait(&qd_full[st], (ii / S_STAGES) & 1);
-        tc::tc_fence_after();
-        const uint32_t aQ = smem_u32(sQD + st * 32768);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tS(ii & 1), tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
-                          idSS, kk > 0);
-        tc::umma_commit(&s_full[ii & 1]);
-      };
-      auto issue_dp = [&](int ii) {      // qd_full(ii) already observed by issue_s(ii)
-        const uint32_t aDO = smem_u32(sQD + (ii % S_STAGES) * 32768) + 16384;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
-                          idSS, kk > 0);
-        tc::umma_commit(dp_full);
-      };
-      tc::mbar_wait(kv_full, 0);
-      issue_s(0);
-      issue_dp(0);
-      if (nq > 1) issue_s(1);
-      for (int ii = 0; ii < nq; ++ii) {
-        const int st = ii % S_STAGES;
-        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
-        const uint32_t acc = ii > 0 ? 1u : 0u;
-        tc::mbar_wait(p_ready, ii & 1);
-        tc::tc_fence_after();
-        BWD_TRACE(0, ii);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)   // K step kk = queries [16kk, 16kk+16): chunk kk/2, packed column 8(kk&1)
-          tc::umma_f16_ts(tDV, tS(ii & 1) + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024),
-                          idG, (acc | kk) ? 1u : 0u);
-        BWD_TRACE(1, ii);
-        tc::mbar_wait(ds_ready, ii & 1);
-        tc::tc_fence_after();
-        BWD_TRACE(2, ii);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024), idG,
-                          (acc | kk) ? 1u : 0u);
-        tc::umma_commit(&qd_empty[st]);
-        BWD_TRACE(3, ii);
-        if (ii + 1 < nq) issue_dp(ii + 1);   // overwrites dS_i^T only after dK_i read it (in order)
-        if (ii + 2 < nq) issue_s(ii + 2);    // overwrites P_i^T only after dV_i read it
-        BWD_TRACE(4, ii);
-      }
-      tc::umma_commit(fin_done);
-    }
-  } else {
-    const int quad = warp & 3, c = warp >> 2;
-    const int row = quad * 32 + lane;
-    const int kvi = kv0 + row;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
-    for (int ii = 0; ii < nq; ++ii) {
-      const int st = ii % S_STAGES;
-      const int q0 = (i0 + ii) * BT;
-      const uint32_t tSb = tS(ii & 1) + lane_off + c * 32;
-      if (warp == 0) BWD_TRACE(9, ii);
-      tc::mbar_wait(&s_full[ii & 1], (ii >> 1) & 1);
-      tc::mbar_wait(&qd_full[st], (ii / S_STAGES) & 1);
-      tc::tc_fence_after();
-      if (warp == 0) BWD_TRACE(5, ii);
-      const float* sl = sLD + st * 256 + c * 32;
-      const float* sd = sl + 128;
-      const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
-                        (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
-      uint32_t pk[16];
-      if (a.dbg & 2) {
-        if (lane == 0) tc::mbar_arrive(p_ready);
-        tc::mbar_wait(dp_full, ii & 1);
-        if (lane == 0) tc::mbar_arrive(ds_ready);
-        continue;
-      }
-      {
-        uint32_t rs[32];
-        tc::tmem_ld_32x32b_x32(tSb, rs);
-        tc::tmem_ld_wait();
-        auto pbody = [&](auto edge_tag) {
-          constexpr bool EDGE = decltype(edge_tag)::value;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
-            const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
-            const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                  make_float2(l1.z, l1.w)};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 arg = f2fma(make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1])),
-                                       sl2, nl[e]);
-              float2 p = (e >= 2) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
-              if (EDGE) {
-                const int qi = q0 + c * 32 + u * 8 + 2 * e;
-                p.x = (qi < a.N && kvi < a.N && (!a.causal || qi >= kvi)) ? p.x : 0.f;
-                p.y = (qi + 1 < a.N && kvi < a.N && (!a.causal || qi + 1 >= kvi)) ? p.y : 0.f;
-              }
-              pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
-            }
-          }
-        };
-        if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
-      }
-      tc::tmem_st_32x32b_x16(tSb, pk);          // P^T over the consumed S^T chunk
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_ready);
-      if (warp == 0) BWD_TRACE(6, ii);
-      tc::mbar_wait(dp_full, ii & 1);
-      tc::tc_fence_after();
-      if (warp == 0) BWD_TRACE(7, ii);
-      {
-        uint32_t rp[32], dk[16];
-        tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
-          const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
-          const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
-                                make_float2(d1.z, d1.w)};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]),
-                                    f2add(make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1])),
-                                          nd[e]));
-            dk[u * 4 + e] = pack_bf16x2(ds.x, ds.y);
-          }
-        }
-        tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dk);   // dS^T over the consumed dP^T chunk
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ds_ready);
-      if (warp == 0) BWD_TRACE(8, ii);
-    }
-    tc::mbar_wait(fin_done, 0);
-    tc::tc_fence_after();
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tsrc = which ? tDK : tDV;
-      const float osc = which ? a.scale : 1.f;   // dS carries no softmax scale
-      __nv_bfloat16* g = (which ? a.g0 : a.g1) + (int64_t)b * a.sb_g + (int64_t)kvi * a.ld_g + h * HD + c * 16;
-      uint32_t r[16];
-      tc::tmem_ld_32x32b_x16(tsrc + lane_off + c * 16, r);
-      tc::tmem_ld_wait();
-      if (kvi < a.N) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
-          v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
-          v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * osc, __uint_as_float(r[u * 8 + 5]) * osc);
-          v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * osc, __uint_as_float(r[u * 8 + 7]) * osc);
-          reinterpret_cast<uint4*>(g)[u] = v;
-        }
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == kMMA) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
-  }
-}
-
-__global__ void __launch_bounds__(32 * kSplitWarps, 1)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                       const BwdSplitArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
-  uint8_t* sQ = smem + SB_QD;
-  uint8_t* sDO = smem + SB_QD + 16384;
-  uint8_t* sKV = smem + SB_KV;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SB_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;                  // [4]
-  uint64_t* kv_empty = bars + 1 + S_STAGES;      // [4]
-  uint64_t* s_full = bars + 1 + 2 * S_STAGES;    // [2]
-  uint64_t* dp_full = s_full + 2;
-  uint64_t* ds_ready = s_full + 3;
-  uint64_t* fin_done = s_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qt * BT;
-  const int nk_all = (a.N + BT - 1) / BT;
-  const int nk = a.causal ? min(nk_all, qt + 1) : nk_all;
-  constexpr int kTMA = kSplitCompute, kMMA = kSplitCompute + 1;
-
-  if (warp == kTMA && lane == 0) {
-    tc::tma_prefetch(&tmQ);
-    tc::tma_prefetch(&tmK);
-    tc::tma_prefetch(&tmV);
-    tc::tma_prefetch(&tmdO);
-    tc::mbar_init(q_full, 1);
-    for (int s = 0; s < S_STAGES; ++s) {
-      tc::mbar_init(&kv_full[s], 1);
-      tc::mbar_init(&kv_empty[s], 1);
-    }
-    tc::mbar_init(&s_full[0], 1);
-    tc::mbar_init(&s_full[1], 1);
-    tc::mbar_init(dp_full, 1);
-    tc::mbar_init(ds_ready, kSplitCompute);
-    tc::mbar_init(fin_done, 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S buffer 0 | S buffer 1 | dP (dS packed over it) | dQ
-  const uint32_t tDP = tmem + 256, tDQ = tmem + 384;
-  auto tS = [&](int buf) { return tmem + (buf ? 128u : 0u); };
-  const int64_t bh = (int64_t)b * a.H + h;
-
-  if (warp == kTMA) {
-    if (lane == 0) {
-      tc::mbar_arrive_expect_tx(q_full, 32768);
-      tc::tma_load_3d(sQ, &tmQ, q_full, h * HD, q0, b);
-      tc::tma_load_3d(sDO, &tmdO, q_full, h * HD, q0, b);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j % S_STAGES;
-        if (j >= S_STAGES) tc::mbar_wait(&kv_empty[st], ((j / S_STAGES) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&kv_full[st], 32768);
-        tc::tma_load_3d(sKV + st * 32768, &tmK, &kv_full[st], h * HD, j * BT, b);
-        tc::tma_load_3d(sKV + st * 32768 + 16384, &tmV, &kv_full[st], h * HD, j * BT, b);
-      }
-    }
-  } else if (warp == kMMA) {
-    if (lane == 0) {
-      constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S = Q K^T, dP = dO V^T
-      constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 0, 1);    // dQ: A = dS in TMEM, B = K MN-major
-      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO);
-      auto issue_s = [&](int j) {
-        const int st = j % S_STAGES;
-        tc::mbar_wait(&kv_full[st], (j / S_STAGES) & 1);
-        tc::tc_fence_after();
-        const uint32_t aK = smem_u32(sKV + st * 32768);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tS(j & 1), tc::sdesc_sw128(aQ + kk * 32, 16, 1024), tc::sdesc_sw128(aK + kk * 32, 16, 1024),
-                          idSS, kk > 0);
-        tc::umma_commit(&s_full[j & 1]);
-      };
-      auto issue_dp = [&](int j) {       // kv_full(j) already observed
-        const uint32_t aV = smem_u32(sKV + (j % S_STAGES) * 32768) + 16384;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::umma_f16_ss(tDP, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), tc::sdesc_sw128(aV + kk * 32, 16, 1024), idSS,
-                          kk > 0);
-        tc::umma_commit(dp_full);
-      };
-      tc::mbar_wait(q_full, 0);
-      issue_s(0);
-      issue_dp(0);
-      if (nk > 1) issue_s(1);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j % S_STAGES;
-        const uint32_t aK = smem_u32(sKV + st * 32768);
-        tc::mbar_wait(ds_ready, j & 1);
-        tc::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)   // K step kk = keys [16kk, 16kk+16): chunk kk/2, packed column 8(kk&1)
-          tc::umma_f16_ts(tDQ, tDP + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ,
-                          (j > 0 || kk > 0) ? 1u : 0u);
-        tc::umma_commit(&kv_empty[st]);
-        if (j + 1 < nk) issue_dp(j + 1);   // overwrites dS_j only after dQ_j read it (in order)
-        if (j + 2 < nk) issue_s(j + 2);
-      }
-      tc::umma_commit(fin_done);
-    }
-  } else {
-    const int quad = warp & 3, c = warp >> 2;
-    const int row = quad * 32 + lane;
-    const int qi = q0 + row;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const float nl = qi < a.N ? a.nlse2[bh * a.Npad + qi] : 0.f;    // per lane: this query row
-    const float ndl = qi < a.N ? a.ndelta[bh * a.Npad + qi] : 0.f;
-    const float2 sl2 = make_float2(a.scale_log2, a.scale_log2), nl2 = make_float2(nl, nl), nd2 = make_float2(ndl, ndl);
-    for (int j = 0; j < nk; ++j) {
-      const int k0 = j * BT;
-      tc::mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-      tc::tc_fence_after();
-      const bool edge = (k0 + c * 32 + 32 > a.N) || (a.causal && k0 + c * 32 + 31 > q0 + quad * 32);
-      uint32_t pk[16];
-      {
-        uint32_t rs[32];
-        tc::tmem_ld_32x32b_x32(tS(j & 1) + lane_off + c * 32, rs);
-        tc::tmem_ld_wait();
-        auto pbody = [&](auto edge_tag) {
-          constexpr bool EDGE = decltype(edge_tag)::value;
-#pragma unroll
-          for (int e2 = 0; e2 < 16; ++e2) {
-            const float2 arg = f2fma(make_float2(__uint_as_float(rs[2 * e2]), __uint_as_float(rs[2 * e2 + 1])), sl2, nl2);
-            float2 p = ((e2 & 3) >= 2) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
-            if (EDGE) {
-              const int kj = k0 + c * 32 + 2 * e2;
-              p.x = (kj < a.N && (!a.causal || kj <= qi)) ? p.x : 0.f;
-              p.y = (kj + 1 < a.N && (!a.causal || kj + 1 <= qi)) ? p.y : 0.f;
-            }
-            pk[e2] = pack_bf16x2(p.x, p.y);
-          }
-        };
-        if (__all_sync(0xffffffffu, !edge)) pbody(std::false_type{}); else pbody(std::true_type{});
-      }
-      tc::mbar_wait(dp_full, j & 1);
-      tc::tc_fence_after();
-      {
-        uint32_t rp[32], ds[16];
-        tc::tmem_ld_32x32b_x32(tDP + lane_off + c * 32, rp);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e2 = 0; e2 < 16; ++e2) {
-          const float2 d = f2mul(unpack_bf16x2(pk[e2]),
-                                 f2add(make_float2(__uint_as_float(rp[2 * e2]), __uint_as_float(rp[2 * e2 + 1])), nd2));
-          ds[e2] = pack_bf16x2(d.x, d.y);
-        }
-        tc::tmem_st_32x32b_x16(tDP + lane_off + c * 32, ds);   // dS over the consumed dP chunk
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ds_ready);
-    }
-    tc::mbar_wait(fin_done, 0);
-    tc::tc_fence_after();
-    uint32_t r[16];
-    tc::tmem_ld_32x32b_x16(tDQ + lane_off + c * 16, r);
-    tc::tmem_ld_wait();
-    if (qi < a.N) {
-      __nv_bfloat16* g = a.g0 + (int64_t)b * a.sb_g + (int64_t)qi * a.ld_g + h * HD + c * 16;
-      const float osc = a.scale;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        uint4 v;
-        v.x = pack_bf16x2(__uint_as_float(r[u * 8 + 0]) * osc, __uint_as_float(r[u * 8 + 1]) * osc);
-        v.y = pack_bf16x2(__uint_as_float(r[u * 8 + 2]) * osc, __uint_as_float(r[u * 8 + 3]) * osc);
-        v.z = pack_bf16x2(__uint_as_float(r[u * 8 + 4]) * osc, __uint_as_float(r[u * 8 + 5]) * osc);
-        v.w = pack_bf16x2(__uint_as_float(r[u * 8 + 6]) * osc, __uint_as_float(r[u * 8 + 7]) * osc);
-        reinterpret_cast<uint4*>(g)[u] = v;
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == kMMA) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
-  }
-}
-
 int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, int64_t sb, uint32_t rows = 128) {
   return avb::make_tmap_3d_bf16(m, p, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)ld, (uint64_t)sb, 64, rows,
                                 1);
@@ -1513,13 +1029,11 @@ extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t
   a.lse = lse;
   a.causal = causal;
   a.trace = nullptr;
+#ifdef AVB_ATTN_TRACE_HOOKS   // trace build only: a device buffer address handed over by scripts/trace_attn_fwd.py
   if (const char* tr = getenv("AVB_ATTN_FTRACE")) a.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
-    if (e != cudaSuccess) return avb::cuda_status(e, "attn_fwd smem attr");
-    attr = true;
-  }
+#endif
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(attn_fwd_kernel), F_SMEM, "attn_fwd smem attr"))
+    return e;
   dim3 grid((N + 2 * BT - 1) / (2 * BT), H, B);
   attn_fwd_kernel<<<grid, 320, F_SMEM, avb::as_stream(stream)>>>(mq, mk, mv, a);
   return avb::launch_status("avb_attn_fwd");
@@ -1540,9 +1054,6 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
                 "strides must be multiples of 8 elements");
   cudaStream_t st = avb::as_stream(stream);
   const int Npad = (N + BT - 1) / BT * BT;
-  // default: the fused single kernel (K5); AVB_ATTN_BWD_SPLIT=1 selects the two-kernel K5a/K5b variant
-  const bool fused = getenv("AVB_ATTN_BWD_SPLIT") == nullptr;
-  if (!fused) dq_acc = nullptr;                                  // the split kernels need no fp32 accumulator
   {
     const int64_t threads = (int64_t)B * N * H * 8 + (int64_t)B * H * (Npad - N);
     attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
@@ -1557,36 +1068,6 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   if ((s = make_maps(&mk, k, B, H, N, ld, sb))) return s;
   if ((s = make_maps(&mv, v, B, H, N, ld, sb))) return s;
   if ((s = make_maps(&mdo, dout, B, H, N, ld_o, sb_o))) return s;
-  if (!fused) {
-    BwdSplitArgs sa;
-    sa.B = B; sa.H = H; sa.N = N; sa.Npad = Npad;
-    sa.scale = softmax_scale;
-    sa.scale_log2 = softmax_scale * kLog2e;
-    sa.ndelta = delta;
-    sa.nlse2 = delta + (int64_t)B * H * Npad;
-    sa.ld_g = ld_g; sa.sb_g = sb_g;
-    sa.causal = causal;
-    sa.trace = nullptr;
-    sa.dbg = getenv("AVB_ATTN_DBG") ? atoi(getenv("AVB_ATTN_DBG")) : 0;
-    if (const char* tr = getenv("AVB_ATTN_TRACE")) sa.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SA_SMEM);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SB_SMEM);
-      if (e != cudaSuccess) return avb::cuda_status(e, "attn_bwd split smem attr");
-      attr2 = true;
-    }
-    dim3 grid((N + BT - 1) / BT, H, B);
-    sa.g0 = reinterpret_cast<__nv_bfloat16*>(dk);
-    sa.g1 = reinterpret_cast<__nv_bfloat16*>(dv);
-    attn_bwd_dkdv_kernel<<<grid, 32 * kSplitWarps, SA_SMEM, st>>>(mq, mk, mv, mdo, sa);
-    if ((s = avb::launch_status("avb_attn_bwd (dk/dv)"))) return s;
-    sa.g0 = reinterpret_cast<__nv_bfloat16*>(dq);
-    sa.g1 = nullptr;
-    attn_bwd_dq_kernel<<<grid, 32 * kSplitWarps, SB_SMEM, st>>>(mq, mk, mv, mdo, sa);
-    return avb::launch_status("avb_attn_bwd (dq)");
-  }
   CUtensorMap mdq, mdk, mdv;
   if ((s = make_maps(&mdk, dk, B, H, N, ld_g, sb_g, 32))) return s;   // dK / dV TMA stores: 32-row boxes
   if ((s = make_maps(&mdv, dv, B, H, N, ld_g, sb_g, 32))) return s;
@@ -1610,14 +1091,13 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.nkt = (N + BT - 1) / BT;
   a.items = B * H * a.nkt;
   a.trace = nullptr;
+  a.dbg = 0;
+#ifdef AVB_ATTN_TRACE_HOOKS   // trace build only (scripts/trace_attn_bwd.py)
   if (const char* tr = getenv("AVB_ATTN_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(tr, nullptr, 0));
   a.dbg = getenv("AVB_ATTN_DBG") ? atoi(getenv("AVB_ATTN_DBG")) : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
-    if (e != cudaSuccess) return avb::cuda_status(e, "attn_bwd smem attr");
-    attr = true;
-  }
+#endif
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(attn_bwd_kernel), B_SMEM, "attn_bwd smem attr"))
+    return e;
   // persistent: one CTA per SM walks work items blockIdx.x, +gridDim.x, ... (1 CTA/SM: TMEM 512 cols)
   const int grid = std::min(a.items, avb::sm_count());
   attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);

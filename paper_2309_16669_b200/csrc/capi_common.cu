@@ -2,6 +2,8 @@
 #include "common.cuh"
 
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 
 namespace avb {
@@ -26,6 +28,22 @@ int sm_count() {
     cached[dev] = n;
   }
   return cached[dev];
+}
+
+int ensure_kernel_attrs(const void* func, int smem_bytes, const char* what, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({func, dev})) return AVB_OK;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (e == cudaSuccess && nonportable_cluster)
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  done.insert({func, dev});
+  return AVB_OK;
 }
 
 }  // namespace avb

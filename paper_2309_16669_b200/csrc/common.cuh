@@ -33,6 +33,11 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 
+// Raise a kernel's dynamic shared-memory limit (and optionally allow non-portable cluster sizes) on
+// the CURRENT device, once per (kernel, device).  Kernel attributes are per device, so a process
+// that launches on several GPUs needs the call on each; the cache is mutex-protected.
+int ensure_kernel_attrs(const void* func, int smem_bytes, const char* what, bool nonportable_cluster = false);
+
 }  // namespace avb
 
 #define AVB_CHECK_ARG(cond, ...)            \

@@ -560,21 +560,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// A/B experiment switches (same-box comparisons of the pair / TMA-store / heavy-epilogue paths):
+// read from the environment only in a -DAVB_DEBUG_KNOBS build; the product build has none.
+inline bool knob(const char* name) {
+#ifdef AVB_DEBUG_KNOBS
+  return getenv(name) != nullptr;
+#else
+  (void)name;
+  return false;
+#endif
+}
+
 template <int BN, bool A_MN, bool B_MN, int EK, bool PAIR = false>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm, const CUtensorMap& tx,
            const GemmArgs& a, cudaStream_t st) {
   using C = Cfg<BN, A_MN, B_MN, EK, PAIR>;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EK, PAIR>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return avb::cuda_status(e, "gemm: set smem attribute");
-    if (PAIR) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-      (void)e;
-    }
-    attr = true;
-  }
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(kern), C::SMEM, "gemm: set smem attribute"))
+    return e;
   const int total = a.num_m * a.num_n * a.splits;
   if (!PAIR) {
     const int grid = total < avb::sm_count() ? total : avb::sm_count();
@@ -731,7 +734,7 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
 
   const int BN = (N <= 128) ? 128 : 256;
   // CTA pairs (cta_group::2, 256 x 256 tiles) for the large-M forward / dgrad shapes
-  const bool pair = BN == 256 && M > 128 && !getenv("AVB_GEMM_NO_PAIR");
+  const bool pair = BN == 256 && M > 128 && !knob("AVB_GEMM_NO_PAIR");
   CUtensorMap ta, tb;
   int s;
   if (a_major == 0)
@@ -775,14 +778,14 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   memset(&tx, 0, sizeof(tx));
   g.tma_out = 0;
   if (g.vec_ok && (epilogue == AVB_EPI_BF16 || epilogue == AVB_EPI_BIAS_GELU || epilogue == AVB_EPI_DGELU) &&
-      !getenv("AVB_GEMM_NO_TMA_STORE")) {
+      !knob("AVB_GEMM_NO_TMA_STORE")) {
     int s1 = avb::make_tmap_2d_bf16_sw(&tcm, C, N, M, ldc, 32, 32, 64);
     int s2 = (epilogue == AVB_EPI_BIAS_GELU) ? avb::make_tmap_2d_bf16_sw(&tx, aux_out, N, M, ldaux, 32, 32, 64) : 0;
     if (s1 == AVB_OK && s2 == AVB_OK) g.tma_out = 1;
   }
   g.tma_aux = 0;
   if (g.vec_ok && aux && (epilogue == AVB_EPI_BF16 || epilogue == AVB_EPI_DGELU) && a_major == 0 && N > 128 &&
-      !getenv("AVB_GEMM_NO_TMA_AUX")) {
+      !knob("AVB_GEMM_NO_TMA_AUX")) {
     if (avb::make_tmap_2d_bf16_sw(&tx, aux, N, M, ldaux, 32, 32, 64) == AVB_OK) g.tma_aux = 1;
   }
   cudaStream_t st = avb::as_stream(stream);
@@ -790,10 +793,10 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   // heavy epilogues (bf16 aux read or a second bf16 output) get 3 mainloop stages and 6-deep
   // aux / store rings so TMA latency is covered while the epilogue streams 32-column chunks
   const bool heavy = BN == 256 && a_major == 0 && (g.tma_aux || (g.tma_out && epilogue == AVB_EPI_BIAS_GELU)) &&
-                     !getenv("AVB_GEMM_NO_HEAVY");
+                     !knob("AVB_GEMM_NO_HEAVY");
   // aux-reading epilogues: CTA pairs only when the mainloop is long enough to hide the aux stream
   // (same-box: fc2 fwd + residual, K = 3072: 1208 -> 1355 TFLOP/s; K = 768 shapes 2-4 % slower)
-  if (pair && (!(heavy && g.tma_aux) || K >= 1536 || getenv("AVB_GEMM_PAIR_AUX"))) {
+  if (pair && (!(heavy && g.tma_aux) || K >= 1536 || knob("AVB_GEMM_PAIR_AUX"))) {
     g.num_m = (M + 2 * BM - 1) / (2 * BM);
     if (heavy && g.tma_aux) {
       if (b_major == 0) return launch<256, false, false, 1, true>(ta, tb, tcm, tx, g, st);

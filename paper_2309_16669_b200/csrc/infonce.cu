@@ -203,12 +203,8 @@ extern "C" int avb_infonce_fwd(const float* v, const float* t, int Bg, int E, co
   rownorm_kernel<<<(Bg + 7) / 8, 256, 0, st>>>(t, Bg, E, norms_t);
   const size_t smem = sizeof(float) * (2 * RB * E + 2 * (size_t)RB * Bg);
   AVB_CHECK_ARG(smem <= 200 * 1024, "global batch too large for one InfoNCE pass (Bg=%d)", Bg);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(infonce_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(infonce_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(infonce_stats_kernel), 200 * 1024, "infonce attr"))
+    return e;
   infonce_stats_kernel<<<(Bg + RB - 1) / RB, kThr, smem, st>>>(v, t, norms_v, norms_t, Bg, E, log_scale, lse_r,
                                                                lse_c, loss, dlog_scale);
   return avb::launch_status("avb_infonce_fwd");
@@ -223,11 +219,8 @@ extern "C" int avb_infonce_bwd(const float* v, const float* t, int Bg, int E, co
   AVB_CHECK_ARG(v && t && log_scale && norms_v && norms_t && lse_r && lse_c && dv && dt, "null pointer");
   const size_t smem = sizeof(float) * (2 * RB * E + (size_t)RB * Bg + RB);
   AVB_CHECK_ARG(smem <= 200 * 1024, "global batch too large for one InfoNCE pass (Bg=%d)", Bg);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(infonce_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(infonce_grad_kernel), 200 * 1024, "infonce attr"))
+    return e;
   dim3 grid((n + RB - 1) / RB, 2);
   infonce_grad_kernel<<<grid, kThr, smem, avb::as_stream(stream)>>>(v, t, norms_v, norms_t, Bg, E, log_scale, lse_r,
                                                                     lse_c, r0, n, grad_scale, dv, dt);

@@ -21,6 +21,7 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <math.h>
 #include <stdlib.h>
 
@@ -468,174 +469,6 @@ __global__ void __launch_bounds__(kThreads) k1v2_kernel(const K1v2Params p) {
   }
 }
 
-
-// ------------------------------------------------------------------------------------------------
-// K1 v3 (streaming).  A CTA owns one column strip of one frame and walks the crop's source rows
-// once, top to bottom, in chunks of SCH rows staged by cp.async (double buffered).  Thread q owns
-// word column q of the strip and adds every source row y into the output rows i whose vertical
-// window [ylo_i, ylo_i + yn_i) contains y (a contiguous range [ra(y), rb(y)]); those accumulate
-// in a ring of VR fp32 rows in shared memory.  After each chunk, the output rows that can no
-// longer receive contributions get the horizontal pass (all three channels per strip column),
-// normalization and the store.  No source row is read or converted twice.
-constexpr int SCH = 8;    // source rows per chunk
-constexpr int VR = 24;    // output-row ring: rows started per chunk (<= SCH) + rows in flight (<= 2/s + 2)
-
-__global__ void __launch_bounds__(kThreads) k1v3_kernel(const K1v2Params p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int strip = blockIdx.x, t = blockIdx.y;
-  const int64_t b = blockIdx.z;
-  const int tid = threadIdx.x;
-  const int4 box = *reinterpret_cast<const int4*>(p.boxes + 4 * b);
-  const int x0 = box.x, y0 = box.y, cw = box.z, ch = box.w;
-  if (x0 < 0 || y0 < 0 || cw < 1 || ch < 1 || x0 + cw > p.W || y0 + ch > p.H) return;
-  const bool flip = p.flips ? (p.flips[b] != 0) : false;
-  const int jj0 = strip * p.cps;
-  const int jj1 = min(p.Wt, jj0 + p.cps);
-  const int nj = jj1 - jj0;
-  if (nj <= 0) return;
-
-  float* wx = reinterpret_cast<float*>(smem);                 // [cps][tx_cap]
-  int* xlo = reinterpret_cast<int*>(wx + p.cps * p.tx_cap);   // [cps]
-  int* xn = xlo + p.cps;                                      // [cps]
-  float* wy = reinterpret_cast<float*>(xn + p.cps);           // [Ht][ty_cap]
-  int* ylo = reinterpret_cast<int*>(wy + p.Ht * p.ty_cap);    // [Ht]
-  int* yn = ylo + p.Ht;                                       // [Ht]
-  int* rmis = yn + p.Ht;                                      // [2][SCH]
-  size_t off = (reinterpret_cast<uint8_t*>(rmis + 2 * SCH) - smem + 15) & ~size_t(15);
-  uint8_t* stage = smem + off;                                // [2][SCH][rowb_cap]
-  float* vring = reinterpret_cast<float*>(stage + 2 * (size_t)SCH * p.rowb_cap);  // [VR][rowb_cap]
-
-  for (int k = tid; k < nj; k += kThreads) {
-    int lo;
-    const int n = k1_taps(cw, p.Wt, jj0 + k, wx + k * p.tx_cap, lo);
-    for (int e = n; e < p.tx_cap; ++e) wx[k * p.tx_cap + e] = 0.f;
-    xlo[k] = lo;
-    xn[k] = n;
-  }
-  for (int r = tid; r < p.Ht; r += kThreads) {
-    int lo;
-    const int n = k1_taps(ch, p.Ht, r, wy + r * p.ty_cap, lo);
-    ylo[r] = lo;
-    yn[r] = n;
-  }
-  __syncthreads();
-  const int sx0 = xlo[0];
-  const int sx1 = min(cw, xlo[nj - 1] + xn[nj - 1]);
-  const int nbytes = (sx1 - sx0) * 3;
-  const uint8_t* frame = p.src + b * p.s_clip + (int64_t)t * p.s_t;
-  const uintptr_t first = reinterpret_cast<uintptr_t>(frame + (int64_t)y0 * p.s_h + (int64_t)(x0 + sx0) * 3);
-  const int m4 = (int)(first & 3);
-  const int nwords = (nbytes + m4 + 3) >> 2;
-  const uint8_t* src_end = p.src + p.total_bytes;
-  const int ybeg = ylo[0];
-  const int yend = ylo[p.Ht - 1] + yn[p.Ht - 1];
-  // chunk height scaled with the vertical scale so each chunk starts <= SCH output rows (upscales)
-  const int sch = max(1, min(SCH, (SCH * ch) / p.Ht));
-  const int nchunks = (yend - ybeg + sch - 1) / sch;
-  const int chunks16 = (nbytes + m4 + 27) >> 4;
-
-  auto issue_chunk = [&](int cidx, int buf) {
-    const int ya = ybeg + cidx * sch;
-    const int nr = min(sch, yend - ya);
-    uint8_t* sb = stage + (size_t)buf * SCH * p.rowb_cap;
-    for (int idx = tid; idx < nr * chunks16; idx += kThreads) {
-      const int rr = idx / chunks16, k = idx - rr * chunks16;
-      const uint8_t* a = frame + (int64_t)(y0 + ya + rr) * p.s_h + (int64_t)(x0 + sx0) * 3;
-      const uintptr_t al = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
-      const int mis = (int)(reinterpret_cast<uintptr_t>(a) - al);
-      const uint8_t* g = reinterpret_cast<const uint8_t*>(al) + 16 * k;
-      const int64_t left = src_end - g;
-      const int nb = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
-      if (16 * k < mis + nbytes) cp_async16(sb + (size_t)rr * p.rowb_cap + 16 * k, nb ? g : p.src, nb);
-      if (k == 0) rmis[buf * SCH + rr] = mis - m4;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  // output rows are produced in order; `ia` = first output row not yet started, `idone` = rows stored
-  int ia = 0, idone = 0;
-  issue_chunk(0, 0);
-  for (int cidx = 0; cidx < nchunks; ++cidx) {
-    const int buf = cidx & 1;
-    if (cidx + 1 < nchunks) {
-      issue_chunk(cidx + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const int ya = ybeg + cidx * sch;
-    const int nr = min(sch, yend - ya);
-    const uint8_t* sb = stage + (size_t)buf * SCH * p.rowb_cap;
-    // ---- vertical: rows ya..ya+nr-1 into their output rows (same decisions in every thread)
-    for (int rr = 0; rr < nr; ++rr) {
-      const int y = ya + rr;
-      // start output rows whose window begins here (ring slot zeroed by its owner thread)
-      while (ia < p.Ht && ylo[ia] <= y) {
-        float* vr = vring + (size_t)(ia % VR) * p.rowb_cap;
-        for (int q = tid; q < nwords; q += kThreads) *reinterpret_cast<float4*>(vr + 4 * q) = make_float4(0, 0, 0, 0);
-        ++ia;
-      }
-      // contributing rows: i in [first i with ylo_i + yn_i > y, ia)
-      int i0 = idone;
-      while (i0 < ia && ylo[i0] + yn[i0] <= y) ++i0;
-      const int mis = rmis[buf * SCH + rr];
-      for (int q = tid; q < nwords; q += kThreads) {
-        const uint32_t u = *reinterpret_cast<const uint32_t*>(sb + (size_t)rr * p.rowb_cap + mis + 4 * q);
-        float2 f01 = make_float2(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7440)),
-                                 __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7441)));
-        float2 f23 = make_float2(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7442)),
-                                 __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7443)));
-        f01.x -= 8388608.f; f01.y -= 8388608.f;
-        f23.x -= 8388608.f; f23.y -= 8388608.f;
-        for (int i = i0; i < ia; ++i) {
-          const int k = y - ylo[i];
-          if (k >= yn[i]) continue;
-          const float w = wy[i * p.ty_cap + k];
-          float4* vp = reinterpret_cast<float4*>(vring + (size_t)(i % VR) * p.rowb_cap + 4 * q);
-          float4 v = *vp;
-          float2 a01 = ffma2(make_float2(w, w), f01, make_float2(v.x, v.y));
-          float2 a23 = ffma2(make_float2(w, w), f23, make_float2(v.z, v.w));
-          *vp = make_float4(a01.x, a01.y, a23.x, a23.y);
-        }
-      }
-    }
-    __syncthreads();
-    // ---- completed output rows: windows end before the next chunk's first row
-    const int ynext = ya + nr;
-    int icomp = idone;
-    while (icomp < ia && ylo[icomp] + yn[icomp] <= ynext) ++icomp;
-    const int nrow = icomp - idone;
-    for (int idx = tid; idx < nrow * nj; idx += kThreads) {
-      const int r = idx / nj, k = idx - r * nj;
-      const int i = idone + r;
-      const int jj = jj0 + k;
-      const int j = flip ? (p.Wt - 1 - jj) : jj;
-      const float* w = wx + k * p.tx_cap;
-      const int lim = xn[k];
-      const float* v = vring + (size_t)(i % VR) * p.rowb_cap + (xlo[k] - sx0) * 3 + m4;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-      for (int e = 0; e < lim; ++e) {
-        const float we = w[e];
-        a0 = fmaf(we, v[3 * e], a0);
-        a1 = fmaf(we, v[3 * e + 1], a1);
-        a2 = fmaf(we, v[3 * e + 2], a2);
-      }
-      const float ys[3] = {fmaf(a0, p.scale[0], p.bias[0]), fmaf(a1, p.scale[1], p.bias[1]),
-                           fmaf(a2, p.scale[2], p.bias[2])};
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t o = k1_out_index(p, b, c, t, i, j);
-        if (p.out_dtype == AVB_DTYPE_BF16)
-          reinterpret_cast<__nv_bfloat16*>(p.dst)[o] = __float2bfloat16_rn(ys[c]);
-        else
-          reinterpret_cast<float*>(p.dst)[o] = ys[c];
-      }
-    }
-    idone = icomp;
-    __syncthreads();
-  }
-}
 
 // ------------------------------------------------------------------------------------------------
 // K1 v4 (default for downscales of interleaved RGB): horizontal-first streaming.
@@ -1146,7 +979,15 @@ static void k1v4_envelope_all(int H, int W, int Ht, int Wt, int& nt, int& nopen)
   cache.push_back({H, W, Ht, Wt, nt, nopen});
 }
 
+std::atomic<int> g_force_path{AVB_K1_PATH_AUTO};
+
 }  // namespace
+
+extern "C" int avb_k1_force_path(int path) {
+  AVB_CHECK_ARG(path == AVB_K1_PATH_AUTO || path == AVB_K1_PATH_GENERIC || path == AVB_K1_PATH_STRIP,
+                "bad K1 path %d", path);
+  return g_force_path.exchange(path);
+}
 
 extern "C" int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_dev,
                             int max_taps, void* stream) {
@@ -1224,14 +1065,12 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     avb::set_error("frame too wide for the shared-memory staging (W=%d)", W);
     return AVB_E_UNSUPPORTED;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k1_rrc_normalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k1v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(k1_rrc_normalize_kernel), 200 * 1024, "k1 attr"))
+    return e;
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(k1v2_kernel), 200 * 1024, "k1 attr")) return e;
+  const int force = g_force_path.load();
   // identity: full-frame boxes at the target size, planar rows (the fused-decode hand-off)
-  if (boxes_host && H == Ht && W == Wt && s_w == 1 && Wt % 16 == 0 && !getenv("AVB_K1_NO_IDENTITY") &&
+  if (boxes_host && H == Ht && W == Wt && s_w == 1 && Wt % 16 == 0 && force == AVB_K1_PATH_AUTO &&
       (out_layout != AVB_LAYOUT_TUBELET || tpw % 16 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
       s_h % 16 == 0 && s_c % 16 == 0 && s_t % 16 == 0 && s_clip % 16 == 0 &&
       ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -1249,8 +1088,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
   //     the tap envelope is exact; with device-only boxes it is the worst case over every
   //     downscale crop and a complement launch of v2 covers any upscale clip.
   bool v4_done = false, v4_partial = false;
-  if (p.fast && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && !getenv("AVB_K1_V1") &&
-      !getenv("AVB_K1_V2") && !getenv("AVB_K1_V3") && Ht <= H && Wt <= W && Wt <= 448 && T <= 65535 &&
+  if (p.fast && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && force == AVB_K1_PATH_AUTO && Ht <= H && Wt <= W && Wt <= 448 && T <= 65535 &&
       B <= 65535 && 3LL * T * Ht * Wt < (1LL << 31)) {
     int nt = 0, nopen = 0, cw_max = W;
     bool ok = true;
@@ -1282,9 +1120,10 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
                            (size_t)V4_RS * q.fpc * q.slot_bytes;
       if (smem4 <= 200 * 1024) {
         dim3 g4((T + q.fpc - 1) / q.fpc, (unsigned)B);
+        int ast = AVB_OK;
         auto launch = [&](auto kern) {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
-          kern<<<g4, q.ncomp + 32, smem4, avb::as_stream(stream)>>>(q);
+          ast = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(kern), 200 * 1024, "k1 v4 attr");
+          if (ast == AVB_OK) kern<<<g4, q.ncomp + 32, smem4, avb::as_stream(stream)>>>(q);
         };
         auto by_nt = [&](auto nopen_c) {
           constexpr int NO = decltype(nopen_c)::value;
@@ -1295,6 +1134,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
         };
         if (NOPEN == 2) by_nt(std::integral_constant<int, 2>{});
         else by_nt(std::integral_constant<int, 3>{});
+        if (ast != AVB_OK) return ast;
         const int st = avb::launch_status("avb_rrc_normalize");
         if (st != AVB_OK || !v4_partial) return st;
         v4_done = true;
@@ -1302,7 +1142,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     }
   }
   const bool v2ok = p.fast && (s_h % 4 == 0) && (s_t % 4 == 0) && (s_clip % 4 == 0) &&
-                    ((reinterpret_cast<uintptr_t>(src) & 3) == 0) && !getenv("AVB_K1_V1");
+                    ((reinterpret_cast<uintptr_t>(src) & 3) == 0) && force != AVB_K1_PATH_GENERIC;
   if (v2ok) {
     K1v2Params q;
     q.src = src; q.s_clip = s_clip; q.s_t = s_t; q.s_h = s_h;
@@ -1326,31 +1166,6 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
       head = (head + 15) & ~size_t(15);
       smem = head + 2 * (size_t)q.rows_cap * q.rowb_cap + sizeof(float) * (size_t)q.R * q.rowb_cap;
       if (smem <= 100 * 1024) break;
-    }
-    // v3 (streaming): ring of VR output rows must hold rows completed per chunk + rows in flight:
-    // at most SCH/s + 2*s + 2 <= VR with s = crop_h/Ht >= min over possible boxes ~ 1/Ht..;
-    // guaranteed when Ht <= H (downscale-or-equal targets) for SCH = 8, VR = 16.
-    int min_ch = 1;
-    if (boxes_host) {
-      min_ch = H;
-      for (int64_t i = 0; i < B; ++i) min_ch = std::min(min_ch, (int)boxes_host[4 * i + 3]);
-    }
-    // envelope of the streaming ring: target height <= 7x the crop height (checked when host boxes exist)
-    if ((!boxes_host || (int64_t)min_ch * 7 >= Ht) && getenv("AVB_K1_V3")) {
-      size_t head = sizeof(float) * ((size_t)q.cps * tx_cap + (size_t)Ht * ty_cap) +
-                    sizeof(int) * (2 * (size_t)q.cps + 2 * (size_t)Ht + 2 * SCH);
-      head = (head + 15) & ~size_t(15);
-      const size_t smem3 = head + 2 * (size_t)SCH * q.rowb_cap + sizeof(float) * (size_t)VR * q.rowb_cap;
-      if (smem3 <= 200 * 1024) {
-        static bool attr3 = false;
-        if (!attr3) {
-          cudaFuncSetAttribute(k1v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-          attr3 = true;
-        }
-        dim3 g3(q.strips, T, (unsigned)B);
-        k1v3_kernel<<<g3, kThreads, smem3, avb::as_stream(stream)>>>(q);
-        return avb::launch_status("avb_rrc_normalize");
-      }
     }
     if (q.R >= 1) {
       dim3 g2(q.strips, T, (unsigned)B);

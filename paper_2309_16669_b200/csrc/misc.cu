@@ -69,51 +69,98 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ X, int64_t ldx, 
 }
 
 // x[b, 0] = cls + pos[0];  x[b, 1+n] = pe[b*Np + n] + pos[1+n]
+// Separable space-time position embedding: PE[t*S + s] = PE_t[t] + PE_s[1 + s];
+// the cls token takes PE_s[0] (CLIP's spatial table keeps a cls slot).
 __global__ void tokens_fwd_kernel(const __nv_bfloat16* __restrict__ pe, const float* __restrict__ cls,
-                                  const float* __restrict__ pos, __nv_bfloat16* __restrict__ x, int B, int Np, int D) {
+                                  const float* __restrict__ pos_s, const float* __restrict__ pos_t,
+                                  __nv_bfloat16* __restrict__ x, int B, int Np, int S, int D) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int per_row = D / 8;
   const int64_t total = (int64_t)B * (Np + 1) * per_row;
   if (gid >= total) return;
   const int c = (gid % per_row) * 8;
   const int64_t tok = gid / per_row;
-  const int t = tok % (Np + 1);
+  const int n = tok % (Np + 1);
   const int b = tok / (Np + 1);
   float f[8];
-  if (t == 0) {
+  if (n == 0) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = cls[c + e] + pos[c + e];
+    for (int e = 0; e < 8; ++e) f[e] = cls[c + e] + pos_s[c + e];
   } else {
-    ld8f(pe + ((int64_t)b * Np + t - 1) * D + c, f);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] += pos[(int64_t)t * D + c + e];
+    const int t = (n - 1) / S, sp = (n - 1) - t * S;
+    ld8f(pe + ((int64_t)b * Np + n - 1) * D + c, f);
+    const float4* ps = reinterpret_cast<const float4*>(pos_s + (int64_t)(1 + sp) * D + c);
+    const float4* pt = reinterpret_cast<const float4*>(pos_t + (int64_t)t * D + c);
+    const float4 s0 = ps[0], s1 = ps[1], t0 = pt[0], t1 = pt[1];
+    f[0] += s0.x + t0.x; f[1] += s0.y + t0.y; f[2] += s0.z + t0.z; f[3] += s0.w + t0.w;
+    f[4] += s1.x + t1.x; f[5] += s1.y + t1.y; f[6] += s1.z + t1.z; f[7] += s1.w + t1.w;
   }
   st8f(x + tok * D + c, f);
 }
 
-// dpe = dx[:, 1:];  dpos[t] += sum_b dx[b, t];  dcls += sum_b dx[b, 0]
+// One thread per (token n, 8 columns): acc = sum_b dx[b, n]; dpe = dx[:, 1:];
+// dcls, dpos_s[0] += acc(n = 0); dpos_s[1+s] += acc; dpos_t[t] += acc (fp32 atomics: T' resp. S
+// contributions per element, so these two small gradients are not bit-reproducible run to run).
 __global__ void tokens_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_bfloat16* __restrict__ dpe,
-                                  float* __restrict__ dcls, float* __restrict__ dpos, int B, int Np, int D) {
+                                  float* __restrict__ dcls, float* __restrict__ dpos_s, float* __restrict__ dpos_t,
+                                  int B, int Np, int S, int D) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int per_row = D / 8;
   const int64_t total = (int64_t)(Np + 1) * per_row;
   if (gid >= total) return;
   const int c = (gid % per_row) * 8;
-  const int t = gid / per_row;
+  const int n = gid / per_row;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = 0; b < B; ++b) {
     float f[8];
-    const int64_t tok = (int64_t)b * (Np + 1) + t;
+    const int64_t tok = (int64_t)b * (Np + 1) + n;
     ld8f(dx + tok * D + c, f);
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] += f[e];
-    if (t > 0 && dpe) st8f(dpe + ((int64_t)b * Np + t - 1) * D + c, f);
+    if (n > 0 && dpe) st8f(dpe + ((int64_t)b * Np + n - 1) * D + c, f);
   }
+  if (n == 0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (dcls) dcls[c + e] += acc[e];
+      if (dpos_s) dpos_s[c + e] += acc[e];
+    }
+    return;
+  }
+  const int t = (n - 1) / S, sp = (n - 1) - t * S;
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    if (dpos) dpos[(int64_t)t * D + c + e] += acc[e];
-    if (t == 0 && dcls) dcls[c + e] += acc[e];
+    if (dpos_s) atomicAdd(dpos_s + (int64_t)(1 + sp) * D + c + e, acc[e]);
+    if (dpos_t) atomicAdd(dpos_t + (int64_t)t * D + c + e, acc[e]);
   }
+}
+
+// Tubelet patchify of normalised clips: x bf16 [B,3,T,H,W] (contiguous) -> rows [B*Np, 3*tt*th*tw] in
+// Conv3d-weight feature order ((c*tt + dt)*th + dy)*tw + dx, row n = (t/tt * H/th + y/th) * W/tw + x/tw.
+// One thread per (row, c, dt, dy) segment of tw elements (tw even: bf16 pairs).
+__global__ void patchify_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dst, int B, int T,
+                                int H, int W, int tt, int th, int tw) {
+  const int nT = T / tt, nH = H / th, nW = W / tw;
+  const int64_t segs_per_row = 3LL * tt * th;
+  const int64_t total = (int64_t)B * nT * nH * nW * segs_per_row;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total) return;
+  const int64_t row = gid / segs_per_row;
+  int seg = (int)(gid - row * segs_per_row);
+  const int dy = seg % th;
+  seg /= th;
+  const int dt = seg % tt;
+  const int c = seg / tt;
+  int64_t r = row;
+  const int px = r % nW; r /= nW;
+  const int py = r % nH; r /= nH;
+  const int pt = r % nT;
+  const int b = (int)(r / nT);
+  const int64_t src = ((((int64_t)b * 3 + c) * T + pt * tt + dt) * H + py * th + dy) * W + (int64_t)px * tw;
+  const int64_t dof = row * (3LL * tt * th * tw) + ((int64_t)(c * tt + dt) * th + dy) * tw;
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(x + src);
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + dof);
+  for (int k = 0; k < tw / 2; ++k) d32[k] = s32[k];
 }
 
 // one block per row: loss += scale * (lse - z[y]);  dlogits = scale * (softmax - onehot)
@@ -139,10 +186,13 @@ __global__ void xent_kernel(const float* __restrict__ logits, int64_t ld, const 
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
   const float lse = mx + __logf(s);
   const int y = labels[row];
-  if (threadIdx.x == 0) atomicAdd(loss, scale * (lse - z[y]));
+  // a label outside [0, C) never reads out of bounds: the row is ignored (no loss, zero gradient),
+  // like an ignore_index target
+  const bool valid = y >= 0 && y < C;
+  if (threadIdx.x == 0 && valid) atomicAdd(loss, scale * (lse - z[y]));
   if (dlogits) {
     for (int j = threadIdx.x; j < C; j += blockDim.x) {
-      const float p = __expf(z[j] - lse) - (j == y ? 1.f : 0.f);
+      const float p = valid ? __expf(z[j] - lse) - (j == y ? 1.f : 0.f) : 0.f;
       dlogits[(int64_t)row * ldd + j] = __float2bfloat16_rn(scale * p);
     }
   }
@@ -307,25 +357,48 @@ extern "C" int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float*
   return avb::launch_status("avb_colsum_accum");
 }
 
-extern "C" int avb_tokens_fwd(const void* pe, const float* cls, const float* pos, void* x, int B, int Np, int D,
-                              void* stream) {
+extern "C" int avb_tokens_fwd(const void* pe, const float* cls, const float* pos_s, const float* pos_t, void* x,
+                              int B, int Np, int S, int D, void* stream) {
   AVB_CHECK_ARG(B >= 0 && Np >= 0 && D % 8 == 0, "tokens: D must be a multiple of 8");
+  AVB_CHECK_ARG(S >= 1 && Np % S == 0, "tokens: Np=%d must be a multiple of the spatial count S=%d", Np, S);
   if (B == 0) return AVB_OK;
-  AVB_CHECK_ARG(pe && cls && pos && x, "null pointer");
+  AVB_CHECK_ARG(pe && cls && pos_s && pos_t && x, "null pointer");
+  AVB_CHECK_ARG((reinterpret_cast<uintptr_t>(pos_s) & 15) == 0 && (reinterpret_cast<uintptr_t>(pos_t) & 15) == 0,
+                "pos_s / pos_t must be 16-byte aligned");
   const int64_t total = (int64_t)B * (Np + 1) * (D / 8);
   tokens_fwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(pe), cls, pos, reinterpret_cast<__nv_bfloat16*>(x), B, Np, D);
+      reinterpret_cast<const __nv_bfloat16*>(pe), cls, pos_s, pos_t, reinterpret_cast<__nv_bfloat16*>(x), B, Np, S,
+      D);
   return avb::launch_status("avb_tokens_fwd");
 }
 
-extern "C" int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos, int B, int Np, int D, void* stream) {
+extern "C" int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos_s, float* dpos_t, int B, int Np,
+                              int S, int D, void* stream) {
   AVB_CHECK_ARG(B >= 0 && Np >= 0 && D % 8 == 0, "tokens: D must be a multiple of 8");
+  AVB_CHECK_ARG(S >= 1 && Np % S == 0, "tokens: Np=%d must be a multiple of the spatial count S=%d", Np, S);
   if (B == 0) return AVB_OK;
   AVB_CHECK_ARG(dx, "null pointer");
   const int64_t total = (int64_t)(Np + 1) * (D / 8);
   tokens_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(dx), reinterpret_cast<__nv_bfloat16*>(dpe), dcls, dpos, B, Np, D);
+      reinterpret_cast<const __nv_bfloat16*>(dx), reinterpret_cast<__nv_bfloat16*>(dpe), dcls, dpos_s, dpos_t, B, Np,
+      S, D);
   return avb::launch_status("avb_tokens_bwd");
+}
+
+extern "C" int avb_patchify(const void* x, int B, int T, int H, int W, int tt, int th, int tw, void* dst,
+                            void* stream) {
+  AVB_CHECK_ARG(B >= 0 && T >= 1 && H >= 1 && W >= 1 && tt >= 1 && th >= 1 && tw >= 2 && tw % 2 == 0,
+                "patchify: bad dims (tw must be even)");
+  AVB_CHECK_ARG(T % tt == 0 && H % th == 0 && W % tw == 0, "patchify: tubelet %dx%dx%d must tile %dx%dx%d", tt, th,
+                tw, T, H, W);
+  if (B == 0) return AVB_OK;
+  AVB_CHECK_ARG(x && dst, "null pointer");
+  AVB_CHECK_ARG((reinterpret_cast<uintptr_t>(x) & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 3) == 0,
+                "patchify: 4-byte aligned buffers");
+  const int64_t total = (int64_t)B * (T / tt) * (H / th) * (W / tw) * 3 * tt * th;
+  patchify_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(dst), B, T, H, W, tt, th, tw);
+  return avb::launch_status("avb_patchify");
 }
 
 extern "C" int avb_xent(const float* logits, int64_t ld, const int32_t* labels, int B, int C, float scale, float* loss,

@@ -1,8 +1,8 @@
 """Thin torch-facing wrappers over the C ABI (pointers + sizes + current stream).
 
 Every function here validates dtypes/shapes/devices on the host and then calls
-one `avb_*` entry point; none of them computes anything in PyTorch.  Autograd
-lives in `nn.py`.
+one `avb_*` entry point; none of them computes anything in PyTorch.  The
+torch.autograd.Function / nn.Module layer on top of these lives in `nn.py`.
 """
 
 from __future__ import annotations
@@ -17,6 +17,19 @@ EPI_BF16, EPI_BIAS_GELU, EPI_DGELU, EPI_F32, EPI_F32_ACCUM = 0, 1, 2, 3, 4
 
 def _ptr(t):
     return None if t is None else t.data_ptr()
+
+
+def _index(t: torch.Tensor, name: str, n: int | None = None) -> torch.Tensor:
+    """Index tensors (labels, token ids, row indices) are read as int32 by the kernels."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InputError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.int32:
+        raise InputError(f"{name} must be int32 (got {t.dtype}); the kernels read 32-bit indices")
+    if not t.is_contiguous():
+        raise InputError(f"{name} must be contiguous")
+    if n is not None and t.numel() != n:
+        raise InputError(f"{name} must have {n} elements, got {t.numel()}")
+    return t
 
 
 def _rowmajor(t: torch.Tensor, name: str) -> int:
@@ -102,6 +115,11 @@ def attn_fwd(q, k, v, H: int, *, scale: float | None = None, causal: bool = Fals
     _, _, ld_o, sb_o = _bnhd(out, "out", H)
     if lse is None:
         lse = torch.empty((B * H, npad(N)), dtype=torch.float32, device=q.device)
+    elif (lse.dtype != torch.float32 or tuple(lse.shape) != (B * H, npad(N)) or not lse.is_contiguous()
+          or not lse.is_cuda):
+        raise InputError(f"lse must be a contiguous fp32 CUDA tensor [B*H, roundup(N,128)] = [{B * H}, {npad(N)}]")
+    if tuple(out.shape[:2]) != (B, N):
+        raise InputError("out must match q's [B, N]")
     scale = 64 ** -0.5 if scale is None else float(scale)
     st = _lib.load().avb_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, out.data_ptr(), ld_o, sb_o,
                                   lse.data_ptr(), B, H, N, 64, scale, int(causal), _lib.stream_ptr())
@@ -113,13 +131,28 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
              dq=None, dk=None, dv=None):
     """dQ, dK, dV of blockwise attention (dq/dk/dv may be slices of one packed [B,N,3*H*64] buffer)."""
     B, N, ld, sb = _bnhd(q, "q", H)
-    _, _, ld_o, sb_o = _bnhd(o, "o", H)
-    if _bnhd(dout, "dout", H)[2:] != (ld_o, sb_o):
-        raise InputError("o and dout must share strides")
+    for t, nm in ((k, "k"), (v, "v")):
+        if _bnhd(t, nm, H) != (B, N, ld, sb):
+            raise InputError("q, k, v must share shape and strides (the kernel reads k and v with q's strides)")
+    Bo, No, ld_o, sb_o = _bnhd(o, "o", H)
+    if (Bo, No) != (B, N) or _bnhd(dout, "dout", H) != (B, N, ld_o, sb_o):
+        raise InputError("o and dout must be [B, N, H*64] views sharing strides")
+    if (lse.dtype != torch.float32 or tuple(lse.shape) != (B * H, npad(N)) or not lse.is_contiguous()
+            or not lse.is_cuda):
+        raise InputError(f"lse must be the forward's contiguous fp32 [{B * H}, {npad(N)}] tensor")
+    given = [t is not None for t in (dq, dk, dv)]
+    if any(given) and not all(given):
+        raise InputError("dq, dk, dv must be given together (or all omitted)")
     if dq is None:
         g = torch.empty((B, N, 3, H * 64), dtype=torch.bfloat16, device=q.device)
         dq, dk, dv = g[:, :, 0], g[:, :, 1], g[:, :, 2]
-    _, _, ld_g, sb_g = _bnhd(dq, "dq", H)
+    gq = _bnhd(dq, "dq", H)
+    for t, nm in ((dk, "dk"), (dv, "dv")):
+        if _bnhd(t, nm, H) != gq:
+            raise InputError("dq, dk, dv must share shape and strides (the kernel writes dk and dv with dq's strides)")
+    if gq[:2] != (B, N):
+        raise InputError("dq/dk/dv must match q's [B, N]")
+    _, _, ld_g, sb_g = gq
     delta = torch.empty((2, B * H, npad(N)), dtype=torch.float32, device=q.device)
     dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device)
     scale = 64 ** -0.5 if scale is None else float(scale)
@@ -161,21 +194,41 @@ def colsum_accum(x, out):
     return out
 
 
-def tokens_fwd(pe, cls, pos, B, Np, out):
+def tokens_fwd(pe, cls, pos_s, pos_t, B, Np, out):
+    """x = [cls | pe] + PE (PE[t*S+s] = pos_t[t] + pos_s[1+s]; cls + pos_s[0]), PAPER.md:727-729."""
     D = pe.shape[-1]
-    _lib.check(_lib.load().avb_tokens_fwd(pe.data_ptr(), cls.data_ptr(), pos.data_ptr(), out.data_ptr(), B, Np, D,
-                                          _lib.stream_ptr()), "tokens_fwd")
+    S = pos_s.shape[0] - 1
+    if pos_t.shape[0] * S != Np or pos_s.shape[1] != D or pos_t.shape[1] != D:
+        raise InputError(f"pos_s [1+S, D] and pos_t [T', D] must tile Np={Np} patches (S={S}, T'={pos_t.shape[0]})")
+    _lib.check(_lib.load().avb_tokens_fwd(pe.data_ptr(), cls.data_ptr(), pos_s.data_ptr(), pos_t.data_ptr(),
+                                          out.data_ptr(), B, Np, S, D, _lib.stream_ptr()), "tokens_fwd")
     return out
 
 
-def tokens_bwd(dx, dpe, dcls, dpos, B, Np):
+def tokens_bwd(dx, dpe, dcls, dpos_s, dpos_t, B, Np, S):
     D = dx.shape[-1]
-    _lib.check(_lib.load().avb_tokens_bwd(dx.data_ptr(), _ptr(dpe), _ptr(dcls), _ptr(dpos), B, Np, D,
-                                          _lib.stream_ptr()), "tokens_bwd")
+    _lib.check(_lib.load().avb_tokens_bwd(dx.data_ptr(), _ptr(dpe), _ptr(dcls), _ptr(dpos_s), _ptr(dpos_t), B, Np, S,
+                                          D, _lib.stream_ptr()), "tokens_bwd")
+
+
+def patchify(x, tubelet, out=None):
+    """bf16 [B,3,T,H,W] clips -> tubelet patch rows [B*Np, 3*t*h*w] (Conv3d feature order)."""
+    if x.dtype != torch.bfloat16 or not x.is_cuda or x.dim() != 5 or x.shape[1] != 3 or not x.is_contiguous():
+        raise InputError("patchify input must be a contiguous bf16 CUDA tensor [B,3,T,H,W]")
+    B, _, T, H, W = x.shape
+    tt, th, tw = tubelet
+    rows = B * (T // tt) * (H // th) * (W // tw)
+    if out is None:
+        out = torch.empty((rows, 3 * tt * th * tw), dtype=torch.bfloat16, device=x.device)
+    _lib.check(_lib.load().avb_patchify(x.data_ptr(), B, T, H, W, tt, th, tw, out.data_ptr(), _lib.stream_ptr()),
+               "patchify")
+    return out
 
 
 def xent(logits, labels, scale, loss, dlogits=None):
+    """Softmax CE; labels int32 [B] (a label outside [0, C) ignores its row, see avion_b200.h)."""
     B, C = logits.shape
+    _index(labels, "labels", B)
     ldd = dlogits.stride(0) if dlogits is not None else 0
     _lib.check(_lib.load().avb_xent(logits.data_ptr(), logits.stride(0), labels.data_ptr(), B, C, float(scale),
                                     loss.data_ptr(), _ptr(dlogits), ldd, _lib.stream_ptr()), "xent")
@@ -235,6 +288,9 @@ def infonce(v: torch.Tensor, t: torch.Tensor, log_scale: torch.Tensor, r0: int =
 def embed_fwd(tokens, table, pos, out):
     B, L = tokens.shape
     V, D = table.shape
+    _index(tokens, "tokens")
+    if L > pos.shape[0]:
+        raise InputError(f"{L} tokens per caption exceed the position table ({pos.shape[0]})")
     _lib.check(_lib.load().avb_embed_fwd(tokens.data_ptr(), table.data_ptr(), pos.data_ptr(), out.data_ptr(), B, L, D,
                                          V, _lib.stream_ptr()), "embed_fwd")
     return out
@@ -243,12 +299,18 @@ def embed_fwd(tokens, table, pos, out):
 def embed_bwd(tokens, dx, dtable, dpos):
     B, L = tokens.shape
     V, D = dtable.shape
+    _index(tokens, "tokens")
     _lib.check(_lib.load().avb_embed_bwd(tokens.data_ptr(), dx.data_ptr(), dtable.data_ptr(), _ptr(dpos), B, L, D, V,
                                          _lib.stream_ptr()), "embed_bwd")
 
 
 def rows_copy(src, dst, src_idx=None, dst_idx=None, n=None):
     n = (src_idx.numel() if src_idx is not None else src.shape[0]) if n is None else n
+    for t, nm in ((src_idx, "src_idx"), (dst_idx, "dst_idx")):
+        if t is not None:
+            _index(t, nm)
+            if t.numel() < n:
+                raise InputError(f"{nm} has {t.numel()} entries for {n} rows")
     D = src.shape[-1]
     _lib.check(_lib.load().avb_rows_copy(src.data_ptr(), _rowmajor(src, "src"), _ptr(src_idx), dst.data_ptr(),
                                          _rowmajor(dst, "dst"), _ptr(dst_idx), int(n), D, _lib.stream_ptr()),

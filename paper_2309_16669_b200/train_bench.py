@@ -18,6 +18,7 @@ from . import ops
 from .vit import CONFIG4_VIT_B_16F, CONFIG5_VIT_L_16F, FineTuneModel
 
 CLIPS_PER_GPU = 64
+ATTN_BWD_LAUNCHES = 3    # avb_attn_bwd = delta/lse prologue + K5 + dQ convert
 NUM_CLASSES = 3806
 SRC_T, SRC_H, SRC_W = 16, 320, 568
 
@@ -61,6 +62,54 @@ def golden_boxes(n: int, offset: int = 0):
     return np.ascontiguousarray(g[idx, :4]), np.ascontiguousarray(g[idx, 4].astype(np.uint8))
 
 
+INSTRUMENTED = ("attn_fwd", "attn_bwd", "gemm", "layernorm_fwd", "layernorm_bwd", "colsum_accum", "tokens_fwd",
+                "tokens_bwd", "xent", "adamw", "infonce_fwd", "infonce_bwd", "embed_fwd", "embed_bwd", "rows_copy",
+                "cast_bf16", "patchify")
+
+
+def gemm_key(a, b, a_mn=False, b_mn=False, epilogue=0, split_k=1, **k):
+    M, K = (a.shape[1], a.shape[0]) if a_mn else (a.shape[0], a.shape[1])
+    N = b.shape[1] if b_mn else b.shape[0]
+    return f"{M}x{N}x{K}/{'T' if a_mn else 'N'}{'T' if b_mn else 'N'}/epi{epilogue}/s{split_k}"
+
+
+def instrumented_pass(step, nb: int):
+    """Run `step` nb more times with CUDA events around every ops.* launch and K1 (`transform`):
+    returns (per-family timing summary, kernel launches per step, the grad memset included).
+    Used AFTER the timed region, never inside it."""
+    from . import transform as TR
+
+    if nb <= 0:
+        return {}, None
+    timer = LaunchTimer()
+    counts = {"n": 0}
+    orig = {n: getattr(ops, n) for n in INSTRUMENTED}
+    orig_tr = TR.transform
+    per_launch = {"attn_bwd": ATTN_BWD_LAUNCHES, "infonce_fwd": 3}
+
+    def counted(name, fn):
+        def inner(*a, **k):
+            counts["n"] += per_launch.get(name, 1)
+            return fn(*a, **k)
+        return inner
+
+    try:
+        for n, fn in orig.items():
+            setattr(ops, n, timer.wrap(n, counted(n, fn), keyfn=gemm_key if n == "gemm" else None))
+        TR.transform = timer.wrap("k1_transform", counted("k1_transform", orig_tr))
+        timer.active = True
+        for _ in range(nb):
+            counts["n"] += 1      # the gradient memset
+            step()
+        torch.cuda.synchronize()
+    finally:
+        timer.active = False
+        for n, fn in orig.items():
+            setattr(ops, n, fn)
+        TR.transform = orig_tr
+    return timer.summary(), counts["n"] // nb
+
+
 def traffic(kernel: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture (or None)."""
     import bench  # noqa: the driver script's helper (profiles/r01/traffic.json)
@@ -83,32 +132,6 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     patches = torch.empty((B * cfg.patches, cfg.patch_dim), dtype=torch.bfloat16, device=dev)
     loss = torch.zeros(1, dtype=torch.float32, device=dev)
 
-    # instrumentation: kernel-family timers + launch counter
-    timer = LaunchTimer()
-    counts = {"n": 0}
-    orig = {n: getattr(ops, n) for n in ("attn_fwd", "attn_bwd", "gemm", "layernorm_fwd", "layernorm_bwd",
-                                         "colsum_accum", "tokens_fwd", "tokens_bwd", "xent", "adamw")}
-    per_launch = {"attn_bwd": 3}
-
-    def gemm_key(a, b, a_mn=False, b_mn=False, epilogue=0, split_k=1, **k):
-        M, K = (a.shape[1], a.shape[0]) if a_mn else (a.shape[0], a.shape[1])
-        N = b.shape[1] if b_mn else b.shape[0]
-        return f"{M}x{N}x{K}/{'T' if a_mn else 'N'}{'T' if b_mn else 'N'}/epi{epilogue}/s{split_k}"
-
-    def counted(name, fn):
-        def inner(*a, **k):
-            counts["n"] += per_launch.get(name, 1)
-            return fn(*a, **k)
-        return inner
-
-    for n, fn in orig.items():
-        f = counted(n, fn)
-        if n == "gemm":
-            f = timer.wrap(n, f, keyfn=gemm_key)
-        else:
-            f = timer.wrap(n, f)
-        setattr(ops, n, f)
-
     from .dp import GradBucketReducer
 
     store = model.store
@@ -117,11 +140,13 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
 
     from . import transform as TR
 
-    k1 = timer.wrap("k1_transform", TR.transform)
-    zero = timer.wrap("grad_zero", lambda: store.grad.zero_())
+    def k1(*a, **k):
+        return TR.transform(*a, **k)
+
+    def zero():
+        store.grad.zero_()
 
     def step():
-        counts["n"] += 2  # grad memset + transform
         zero()
         loss.zero_()
         k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
@@ -132,13 +157,12 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
 
     for _ in range(args.warmup):
         step()
+    # ---- the timed region: K plain steps, no per-launch instrumentation of any kind
     barrier(world)
     clk = ClockSampler(local)
     clk.start()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    counts["n"] = 0
-    timer.active = True
     barrier(world)
     e0.record(stream)
     for _ in range(args.steps):
@@ -146,13 +170,15 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
-    timer.active = False
     clocks = clk.stop()
-    launches = counts["n"]
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     value = B * world / (ms / 1e3)
 
-    fam = timer.summary()
+    # ---- breakdown pass (separate, after the timed region): CUDA events around every kernel family
+    # and a launch counter; its shares explain `value`, they are not part of it
+    nb = 0 if args.no_breakdown else max(2, min(args.steps, 4))
+    fam, launches_per_step = instrumented_pass(step, nb)
+
     N, H = cfg.tokens, cfg.heads
     att_f = 4.0 * B * H * N * N * 64                    # per launch (one layer)
     att_b = 2.0 * att_f                                 # algorithmic (3x fwd convention, no recompute)
@@ -164,39 +190,44 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     if "attn_bwd" in fam:
         kern["attn_bwd"] = dict(fam["attn_bwd"], tflops=att_b / (fam["attn_bwd"]["avg_ms"] / 1e3) / 1e12)
     if "gemm" in fam:
-        gms = fam["gemm"]["total_ms"] / args.steps
+        gms = fam["gemm"]["total_ms"] / nb
         kern["gemm_all"] = dict(fam["gemm"], tflops=gemm_flops_step / (gms / 1e3) / 1e12)
     for k, v in fam.items():
         if ":" not in k and k not in ("attn_fwd", "attn_bwd", "gemm"):
             kern[k] = dict(v)
-    step_ms_events = ms
     for k in kern:
-        kern[k]["share_of_step"] = kern[k]["total_ms"] / args.steps / step_ms_events
+        kern[k]["share_of_step"] = kern[k]["total_ms"] / nb / ms
     shapes = {}
     for k, v in fam.items():
         if k.startswith("gemm:"):
             dims = k.split(":")[1].split("/")[0].split("x")
             fl = 2.0 * int(dims[0]) * int(dims[1]) * int(dims[2])
-            shapes[k[5:]] = {"ms_per_step": v["total_ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+            shapes[k[5:]] = {"ms_per_step": v["total_ms"] / nb, "launches_per_step": v["launches"] / nb,
                              "tflops": fl / (v["avg_ms"] / 1e3) / 1e12}
     shapes = dict(sorted(shapes.items(), key=lambda kv: -kv[1]["ms_per_step"])[:16])
-    # dominant single kernel: attention fwd/bwd are one kernel each; GEMM instantiations are split per shape
-    cands = {k: kern[k]["total_ms"] for k in ("attn_fwd", "attn_bwd") if k in kern}
-    for k, v in shapes.items():
-        cands["gemm:" + k] = v["ms_per_step"] * args.steps
-    dom = max(cands, key=cands.get)
-    if dom.startswith("gemm:"):
-        ach = shapes[dom[5:]]["tflops"]
-    else:
-        ach = kern[dom]["tflops"]
-    roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_tflops_sustained"],
-            "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"],
-            "traffic": None if large else traffic(dom),   # the committed capture is of the config-4 shape
-            "share_of_step": cands[dom] / args.steps / ms,
-            "algorithmic_flops_per_launch": (att_b if dom == "attn_bwd" else att_f if dom == "attn_fwd" else None),
-            "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
-    attn_total_ms = sum(kern[k]["total_ms"] for k in ("attn_fwd", "attn_bwd") if k in kern) / args.steps
+    roof = None
+    if kern:
+        # dominant single kernel: attention fwd/bwd are one kernel each; GEMM instantiations split per shape
+        cands = {k: kern[k]["total_ms"] / nb for k in ("attn_fwd", "attn_bwd") if k in kern}
+        for k, v in shapes.items():
+            cands["gemm:" + k] = v["ms_per_step"]
+        dom = max(cands, key=cands.get)
+        ach = shapes[dom[5:]]["tflops"] if dom.startswith("gemm:") else kern[dom]["tflops"]
+        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"],
+                "traffic": None if large else traffic(dom),   # the committed capture is of the config-4 shape
+                "share_of_step": cands[dom] / ms,
+                "algorithmic_flops_per_launch": (att_b if dom == "attn_bwd" else att_f if dom == "attn_fwd" else None),
+                "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)"}
+    attn_total_ms = sum(kern[k]["total_ms"] for k in ("attn_fwd", "attn_bwd") if k in kern) / max(nb, 1)
     attn_tflops = (att_f + att_b) * cfg.depth / (attn_total_ms / 1e3) / 1e12 if attn_total_ms else None
+    k1_roof = None
+    if "k1_transform" in fam:
+        algo = TR.algorithmic_bytes(boxes, SRC_T, (cfg.height, cfg.width), 2)
+        gbs = algo / (fam["k1_transform"]["avg_ms"] / 1e3) / 1e9
+        k1_roof = {"bound": "hbm", "kernel": "k1v4_kernel (tubelet layout)", "achieved": gbs, "peak": pk["hbm_gbs"],
+                   "unit": "GB/s", "frac": gbs / pk["hbm_gbs"], "algorithmic_bytes_per_launch": algo,
+                   "ms_per_launch": fam["k1_transform"]["avg_ms"], "peak_source": f"{src} hbm_gbs (in-step)"}
 
     # ---- e2e: public API from pinned host clips; every step's clips cross H2D inside the timed region.
     # Loader -> device hand-off: the next step's clips are copied on a side
@@ -204,31 +235,18 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     host = torch.empty((B, SRC_T, SRC_H, SRC_W, 3), dtype=torch.uint8, pin_memory=True)
     host.copy_(frames.cpu())
     loss_h = torch.empty(1, dtype=torch.float32, pin_memory=True)
-    dbuf = [frames, torch.empty_like(frames)]
-    copy_stream = torch.cuda.Stream()
-    ready = [torch.cuda.Event(), torch.cuda.Event()]
-    consumed = [torch.cuda.Event(), torch.cuda.Event()]
-    frames_ref = {"t": frames}
+    from .feeder import DeviceFeeder
 
-    def h2d(slot):
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(consumed[slot])
-            dbuf[slot].copy_(host, non_blocking=True)
-            ready[slot].record(copy_stream)
+    feeder = DeviceFeeder(B, SRC_T, SRC_H, SRC_W, (cfg.height, cfg.width), layout="tubelet",
+                          tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), channels_last=True, depth=2)
 
     def e2e_run(nsteps):
-        for s_ in range(2):
-            consumed[s_].record(stream)
-        h2d(0)
+        # public API: the feeder H2D-copies step i+1's pinned clips on its copy stream while step i computes
+        feeder.submit(host, boxes, flips)
         for i in range(nsteps):
-            slot = i & 1
             if i + 1 < nsteps:
-                h2d(slot ^ 1)                      # prefetch the next step's clips
-            stream.wait_event(ready[slot])
-            nonlocal_frames = dbuf[slot]
-            k1(nonlocal_frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
-               tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
-            consumed[slot].record(stream)
+                feeder.submit(host, boxes, flips)
+            feeder.next(out=patches)
             zero()
             loss.zero_()
             model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
@@ -245,27 +263,21 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
 
-    for n, fn in orig.items():
-        setattr(ops, n, fn)
     line = {
-        "metric": ("train clips/sec ViT-L/14 16x224^2 (long-sequence stress)" if large else
-                   "train clips/sec ViT-B/16 16x224^2 (fine-tune step); attn TFLOP/s vs bf16 peak"),
+        "metric": None,   # bench.py sets the workload's shared metric string and config
         "value": value, "unit": "clips/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic uint8 16x320x568 clips (device randint) -> K1 RRC boxes from the reference sampler; "
                 "random-init weights; random labels over 3806 classes",
-        "config": {"workload": ("configs[4] ViT-L/14 16x224^2, tubelet 2x14x14 (N=2049), D=1024, L=24" if large else
-                                "configs[3] ViT-B/16 fine-tune 16x224^2, tubelet 2x16x16 (N=1569), FlashAttention "
-                                "fwd/bwd"), "clips_per_gpu": B, "global_batch": B * world, "seq_len": N,
-                   "parallelism": f"dp{world}", "optimizer": "AdamW (fused kernel)",
-                   "l2": "per-step working set (activations ~30 GB) >> 126 MB L2; no flush needed"},
         "attn_tflops": attn_tflops,
         "kernels": kern,
         "gemm_shapes": shapes,
         "roofline": roof,
+        "k1_roofline": k1_roof,
+        "breakdown": f"{nb} extra steps after the timed region with CUDA events around every launch",
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "clips/s", "h2d_bytes_per_step": int(host.numel()),
                 "d2h_bytes_per_step": 4},
-        "gpu_launches": launches // max(1, args.steps) * args.steps,
+        "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
         "clocks": clocks,
         "loss": float(loss_h.item()),
         "memory": {"peak_bytes": int(torch.cuda.max_memory_allocated()), "clips_per_gpu": B},

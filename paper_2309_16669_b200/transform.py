@@ -20,7 +20,6 @@ import torch
 
 from . import _lib
 from .errors import InputError
-from .rrc import CropRect
 
 CLIP_MEAN = (0.48145466, 0.4578275, 0.40821073)
 CLIP_STD = (0.26862954, 0.26130258, 0.27577711)
@@ -32,7 +31,7 @@ _LAYOUT = {"cthw": _lib.AVB_LAYOUT_CTHW, "tchw": _lib.AVB_LAYOUT_TCHW, "tubelet"
 def _boxes_to_host(crops) -> np.ndarray:
     if isinstance(crops, torch.Tensor):
         return crops.detach().to("cpu", torch.int32).numpy().reshape(-1, 4)
-    if len(crops) and isinstance(crops[0], CropRect):
+    if len(crops) and all(hasattr(crops[0], f) for f in ("x", "y", "crop_w", "crop_h")):   # CropRect
         return np.asarray([(c.x, c.y, c.crop_w, c.crop_h) for c in crops], dtype=np.int32)
     return np.asarray(crops, dtype=np.int32).reshape(-1, 4)
 

@@ -4,7 +4,9 @@ Shape contract: `VitConfig` keeps the reference's field names and token rule
 (`pkg/src/vidpipe/models.py:34-74`): N = (frames/cube_t)(height/cube_h)(width/cube_w)
 + extra_tokens.  The architecture itself is absent from the reference and is
 restated from PAPER.md: non-overlapping t x h x w cubes linearly projected to D
-with PE = PE_t + PE_s folded into one learned table (:258-259, :727-729), a cls
+with the separable position embedding PE[i] = PE_t[i] + PE_s (:258-259, :727-729;
+PE_s is CLIP's spatial table incl. its cls slot, PE_t one row per temporal token
+index, linearly interpolated when T changes -- `interpolate_temporal_pe`), a cls
 token (extra_tokens = 1), L pre-LN blocks x += Proj(MHA(LN x)); x += FC2(act(FC1(LN x)))
 with CLIP's QuickGELU (:259-260, :727), blockwise attention (:265-272).
 
@@ -77,6 +79,14 @@ class VitConfig:
     @property
     def patches(self) -> int:
         return self.tokens - self.extra_tokens
+
+    @property
+    def spatial_tokens(self) -> int:
+        return (self.height // self.cube_h) * (self.width // self.cube_w)
+
+    @property
+    def temporal_tokens(self) -> int:
+        return self.frames // self.cube_t
 
     @property
     def patch_dim(self) -> int:
@@ -306,7 +316,8 @@ class VideoEncoder:
         s.add(f"{P}.pe.w", (D, F), True, "normal", f"{P}.embed")
         s.add(f"{P}.pe.b", (D,), False, "zeros", f"{P}.embed")
         s.add(f"{P}.cls", (D,), False, "normal", f"{P}.embed")
-        s.add(f"{P}.pos", (cfg.tokens, D), False, "normal", f"{P}.embed")
+        s.add(f"{P}.pos_s", (1 + cfg.spatial_tokens, D), False, "normal", f"{P}.embed")   # PE_s (+ cls slot)
+        s.add(f"{P}.pos_t", (cfg.temporal_tokens, D), False, "normal", f"{P}.embed")      # PE_t
         self.stack = TransformerStack(D, cfg.heads, cfg.depth, cfg.hidden, store, P)
 
     def forward(self, patches: torch.Tensor, B: int, save: bool = True):
@@ -314,7 +325,7 @@ class VideoEncoder:
         N, Np, D = cfg.tokens, cfg.patches, cfg.dim
         pe = ops.gemm(patches, s.w(f"{P}.pe.w"), bias=s.p(f"{P}.pe.b"))
         x = torch.empty((B * N, D), dtype=torch.bfloat16, device=patches.device)
-        ops.tokens_fwd(pe, s.p(f"{P}.cls"), s.p(f"{P}.pos"), B, Np, x)
+        ops.tokens_fwd(pe, s.p(f"{P}.cls"), s.p(f"{P}.pos_s"), s.p(f"{P}.pos_t"), B, Np, x)
         del pe
         x, saved = self.stack.forward(x, B, N, save)
         return x, {"patches": patches, "B": B, "saved": saved}
@@ -326,11 +337,28 @@ class VideoEncoder:
         N, Np, D = cfg.tokens, cfg.patches, cfg.dim
         dx = self.stack.backward(dx, ctx["saved"], B, N, on_layer_done)
         dpe = torch.empty((B * Np, D), dtype=torch.bfloat16, device=dx.device)
-        ops.tokens_bwd(dx, dpe, s.g(f"{P}.cls"), s.g(f"{P}.pos"), B, Np)
+        ops.tokens_bwd(dx, dpe, s.g(f"{P}.cls"), s.g(f"{P}.pos_s"), s.g(f"{P}.pos_t"), B, Np, cfg.spatial_tokens)
         ops.gemm(dpe, ctx["patches"], a_mn=True, b_mn=True, out=s.g(f"{P}.pe.w"), epilogue=ops.EPI_F32_ACCUM,
                  split_k=wgrad_split(D, cfg.patch_dim, B * Np), a_rowsum=s.g(f"{P}.pe.b"))
         if on_layer_done is not None:
             on_layer_done(f"{P}.embed")
+
+
+def interpolate_temporal_pe(pe_t, new_t: int):
+    """PE_t [T0, D] -> [new_t, D] by linear interpolation along time (T grows from 4 to 16
+    when fine-tuning).  Half-pixel-centre sampling (align_corners=False), i.e. the source coordinate of
+    row i is (i + 0.5) * T0 / new_t - 0.5, clamped to [0, T0 - 1].  A load-time parameter transform on
+    the host (numpy float64), not a training-step op."""
+    import numpy as np
+
+    src = np.asarray(pe_t.detach().cpu() if isinstance(pe_t, torch.Tensor) else pe_t, dtype=np.float64)
+    T0 = src.shape[0]
+    x = np.clip((np.arange(new_t) + 0.5) * T0 / new_t - 0.5, 0.0, T0 - 1)
+    i0 = np.floor(x).astype(np.int64)
+    i1 = np.minimum(i0 + 1, T0 - 1)
+    w = (x - i0)[:, None]
+    out = src[i0] * (1.0 - w) + src[i1] * w
+    return torch.from_numpy(out.astype(np.float32))
 
 
 @dataclass(frozen=True)

@@ -117,3 +117,76 @@ def test_clip_dp_gradient_rule_gloo():
         assert abs(l - loss.item()) < 1e-5
         assert torch.allclose(gW, Wr.grad, atol=1e-5, rtol=1e-4)
         assert torch.allclose(gs, sr.grad, atol=1e-6)
+
+
+# ----------------------------------------------------------------------------- the real DP step (GPU)
+def _ft_worker(rank, world, port, q):
+    """One rank of the data-parallel fine-tune step: its half of the clips, gradients all-reduced
+    per layer through GradBucketReducer while the backward runs (gloo carries CUDA tensors, so two
+    ranks can share the one GPU of the test box; the bench uses NCCL)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_16669_b200.dp import GradBucketReducer
+        cfg, C, B, patches, labels = _ft_inputs()
+        from paper_2309_16669_b200.vit import FineTuneModel
+        model = FineTuneModel(cfg, num_classes=C, seed=1)
+        s = model.store
+        red = GradBucketReducer(s.grad, {g: s.group_slice(g) for g in s.groups})
+        half = B // world
+        Np = cfg.patches
+        loss = torch.zeros(1, device="cuda")
+        model.zero_grad()
+        model.forward_backward(patches[rank * half * Np:(rank + 1) * half * Np].contiguous(),
+                               labels[rank * half:(rank + 1) * half].contiguous(), half, loss,
+                               loss_scale=1.0 / B, on_layer_done=red.on_layer_done)
+        done = red.finish()
+        torch.cuda.synchronize()
+        q.put((rank, s.grad.cpu(), done))
+    finally:
+        dist.destroy_process_group()
+
+
+def _ft_inputs():
+    from paper_2309_16669_b200.vit import VitConfig
+    cfg = VitConfig(frames=4, height=64, width=64, cube_t=2, depth=2, dim=128, heads=2)
+    C, B = 10, 4
+    g = torch.Generator(device="cuda").manual_seed(7)
+    patches = torch.randn(B * cfg.patches, cfg.patch_dim, generator=g, device="cuda").to(torch.bfloat16)
+    labels = torch.randint(0, C, (B,), generator=g, device="cuda", dtype=torch.int32)
+    return cfg, C, B, patches, labels
+
+
+@pytest.mark.gpu
+def test_dp_finetune_step_equals_single_rank_2x_batch():
+    from paper_2309_16669_b200.vit import FineTuneModel
+    res = _run(_ft_worker)
+    cfg, C, B, patches, labels = _ft_inputs()
+    model = FineTuneModel(cfg, num_classes=C, seed=1)
+    loss = torch.zeros(1, device="cuda")
+    model.zero_grad()
+    model.forward_backward(patches, labels, B, loss, loss_scale=1.0 / B)
+    ref = model.store.grad.cpu()
+    for rank, grad, done in res:
+        assert "head" in done and "enc.embed" in done and len(done) == cfg.depth + 2
+        # same kernels on half the clips each + the sum over ranks == one rank on all clips
+        assert ((grad - ref).norm() / ref.norm()).item() < 1e-3, rank
+
+
+def test_bench_self_launch_command(monkeypatch):
+    """`bench.py --gpus N` outside a launcher re-executes itself under torch.distributed.run."""
+    import sys
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench.os, "execvpe", lambda f, cmd, env: seen.update(cmd=cmd, env=env))
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "5"])
+
+    class A:
+        gpus = 4
+    bench._relaunch(A())
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"

@@ -133,20 +133,19 @@ def test_full_config2_size_properties():
 
 
 # ---------------------------------------------------------------- v4 (default streaming kernel) coverage
-class _Env:
-    def __init__(self, **kv):
-        self.kv = kv
+class _Path:
+    """Pin K1's kernel choice for the process (avb_k1_force_path test hook), restored on exit."""
+
+    def __init__(self, path):
+        self.path = path
 
     def __enter__(self):
-        self.old = {k: os.environ.get(k) for k in self.kv}
-        os.environ.update(self.kv)
+        from paper_2309_16669_b200 import _lib
+        self.old = _lib.load().avb_k1_force_path(self.path)
 
     def __exit__(self, *a):
-        for k, v in self.old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        from paper_2309_16669_b200 import _lib
+        _lib.load().avb_k1_force_path(self.old)
 
 
 @pytest.mark.parametrize("Tn", [1, 3, 4])
@@ -158,7 +157,8 @@ def test_v4_matches_v2_and_oracle(Tn):
     ref = O.transform_batch(fr.numpy(), boxes, flips)
     d = fr.cuda()
     o4 = T.transform(d, boxes, flips, out_dtype=torch.float32)
-    with _Env(AVB_K1_V2="1"):
+    from paper_2309_16669_b200 import _lib
+    with _Path(_lib.AVB_K1_PATH_STRIP):
         o2 = T.transform(d, boxes, flips, out_dtype=torch.float32)
     assert np.abs(o4.cpu().numpy() - ref).max() <= 1e-3
     assert (o4 - o2).abs().max().item() <= 2e-5
@@ -173,6 +173,35 @@ def test_v4_tubelet_layout():
     # [B, T/2, 14, 14, 3, 2, 16, 16] -> rows (t', py, px), features (c, dt, y, x)
     r = ref.reshape(B, 3, Tn // 2, 2, 14, 16, 14, 16).transpose(0, 2, 4, 6, 1, 3, 5, 7).reshape(-1, 1536)
     assert np.abs(tub.cpu().numpy() - r).max() <= 1e-3
+
+
+@pytest.mark.parametrize("tub", [(1, 16, 16), (2, 14, 14), (2, 16, 16)])
+def test_tubelet_layouts_configs_3_4_5(tub):
+    """The patch-embed operand for config 3 (1x16x16), config 4 (2x16x16) and config 5 (2x14x14)."""
+    from oracle import vit_oracle as VO
+    from paper_2309_16669_b200.vit import VitConfig
+    tt, ph, pw = tub
+    B, Tn = 3, 4
+    fr = frames_u8(B, Tn, 320, 568, seed=30 + pw)
+    boxes, flips = CFG2[40:40 + B, :4], CFG2[40:40 + B, 4]
+    ref = O.transform_batch(fr.numpy(), boxes, flips)                      # [B,3,T,224,224] float64
+    cfg = VitConfig(frames=Tn, cube_t=tt, cube_h=ph, cube_w=pw)
+    r = VO.patchify(torch.from_numpy(ref), cfg).numpy()
+    tubf = T.transform(fr.cuda(), boxes, flips, out_dtype=torch.float32, layout="tubelet", tubelet=tub)
+    assert tubf.shape == (B * cfg.patches, cfg.patch_dim)
+    assert np.abs(tubf.cpu().numpy() - r).max() <= 1e-3
+    tubh = T.transform(fr.cuda(), boxes, flips, layout="tubelet", tubelet=tub).float().cpu().numpy()
+    assert np.all(np.abs(tubh - r) <= bf16_ulp(r) + 1e-6)
+
+
+def test_forced_generic_path_matches_oracle():
+    from paper_2309_16669_b200 import _lib
+    fr = frames_u8(2, 3, 320, 568, seed=33)
+    boxes, flips = CFG2[50:52, :4], CFG2[50:52, 4]
+    ref = O.transform_batch(fr.numpy(), boxes, flips)
+    with _Path(_lib.AVB_K1_PATH_GENERIC):
+        out = T.transform(fr.cuda(), boxes, flips, out_dtype=torch.float32)
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
 
 
 @pytest.mark.parametrize("H,W,Ht,Wt,box,flip", [
