@@ -425,28 +425,54 @@ def run_reference(args, rank, world):
     base = {"impl": "reference", "metric": METRICS[wl], "unit": UNITS[wl], "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "config": workload_config(wl, world)}
-    if wl in ("augment", "feed"):
+    if wl == "feed":
+        # the reference has no device hand-off: its CPU equivalent of "uint8 Batch.frames -> normalised
+        # bf16 clips" is the normalise + cast it defers, restated in torch on all cores
+        import torch
+
+        from oracle import cpu_baseline as CB
+
+        torch.set_num_threads(cores)
+        fr = torch.randint(0, 256, (FEED_B, FEED_T, 3, 224, 224), dtype=torch.uint8)
+        m = torch.tensor(CB.CLIP_MEAN).view(1, 1, 3, 1, 1)
+        sd = torch.tensor(CB.CLIP_STD).view(1, 1, 3, 1, 1)
+
+        def job():
+            return ((fr.float() / 255.0 - m) / sd).permute(0, 2, 1, 3, 4).to(torch.bfloat16).contiguous()
+
+        for _ in range(args.warmup):
+            job()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            job()
+        sec = time.perf_counter() - t0
+        v = FEED_B * args.steps / sec
+        return dict(base, value=v, ms_per_step=sec / args.steps * 1e3, dtype="f32->bf16",
+                    data="synthetic uint8 Batch.frames", cpu_baseline={
+                        "value": v, "unit": UNITS[wl], "cores": cores, "kind": "port",
+                        "sample": f"one {FEED_B}-clip batch per step: normalise + cast + re-layout in torch on "
+                                  f"{cores} threads"},
+                    e2e={"value": v, "unit": UNITS[wl], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    if wl == "augment":
         boxes, flips = golden_boxes(AUG_B)
         try:
             from oracle import swscale_ref as SW
 
-            per_step = cores                        # one clip per host thread per step
+            per_step = AUG_B                        # one step = the config's whole 64-clip batch
             sws = SW.load()
             if sws is None:
                 raise RuntimeError("no libswscale")
             from concurrent.futures import ThreadPoolExecutor
 
             rng = np.random.default_rng(0)
-            if wl == "augment":
-                frames = [rng.integers(0, 256, (AUG_T, AUG_H, AUG_W, 3), dtype=np.uint8) for _ in range(2)]
-                job = lambda i: SW.scale_clip(sws, frames[i % 2], boxes[i % len(boxes)], bool(flips[i % len(flips)]))
-                what = (f"{per_step} clips per step: crop -> hflip -> sws_scale(SWS_BILINEAR|SWS_ACCURATE_RND) "
-                        f"320x568 -> 224^2 per frame (codec.cpp:226-246) via ctypes on {SW.version_tag()}")
-            else:
-                frames = [rng.integers(0, 256, (FEED_T, 224, 224, 3), dtype=np.uint8) for _ in range(2)]
-                full = (0, 0, 224, 224)
-                job = lambda i: SW.scale_clip(sws, frames[i % 2], full, False)
-                what = f"{per_step} clips per step: same-size sws_scale (the reference's fused-decode output copy)"
+            frames = [rng.integers(0, 256, (AUG_T, AUG_H, AUG_W, 3), dtype=np.uint8) for _ in range(2)]
+
+            def job(i):
+                return SW.scale_clip(sws, frames[i % 2], boxes[i % len(boxes)], bool(flips[i % len(flips)]))
+
+            what = (f"one {per_step}-clip batch per step: crop -> hflip -> sws_scale(SWS_BILINEAR|SWS_ACCURATE_RND) "
+                    f"320x568 -> 224^2 per frame (codec.cpp:226-246) via ctypes on {SW.version_tag()}, "
+                    f"{cores} clips in flight; no normalise/cast (the reference defers them)")
             ex = ThreadPoolExecutor(cores)
             for w in range(args.warmup):
                 list(ex.map(job, range(w * per_step, (w + 1) * per_step)))

@@ -104,7 +104,7 @@ def clip_loss(v, t, logit_scale):
     v = F.normalize(v, dim=-1)
     t = F.normalize(t, dim=-1)
     s = logit_scale * v @ t.t()
-    y = torch.arange(v.shape[0])
+    y = torch.arange(v.shape[0], device=v.device)
     return 0.5 * (F.cross_entropy(s, y) + F.cross_entropy(s.t(), y))
 
 

@@ -99,3 +99,24 @@ def test_fwd_large_dynamic_range(causal):
     assert torch.isfinite(o.float()).all()
     assert rel(o.view(B, N, H, 64), ro) < 2e-2
     assert ((lse.view(B, H, -1)[:, :, :N] - rlse).abs() / rlse.abs().clamp_min(1.0)).max().item() < 1e-3
+
+
+@pytest.mark.parametrize("B,N,H,causal", [(4, 1569, 6, False), (2, 300, 2, True), (1, 77, 1, True), (12, 785, 12, False)])
+def test_bwd_variants_agree(B, N, H, causal):
+    """The default K5 (double-buffered S^T regions) and the v1 kernel give the same gradients up to
+    the fp32 dQ reduce-add order; both match the fp32 reference."""
+    from paper_2309_16669_b200 import _lib
+    qkv = packed(B, N, H, seed=31 + N)
+    q, k, v = (qkv[:, :, i].contiguous().view(B, N, H * 64) for i in range(3))
+    o, lse = ops.attn_fwd(q, k, v, H, causal=causal)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    do = torch.randn(B, N, H * 64, generator=g, device="cuda").to(torch.bfloat16)
+    lib = _lib.load()
+    old = lib.avb_attn_bwd_variant(1)
+    try:
+        g1 = [t.clone() for t in ops.attn_bwd(q, k, v, o, do, lse, H, causal=causal)]
+    finally:
+        lib.avb_attn_bwd_variant(old)
+    g2 = ops.attn_bwd(q, k, v, o, do, lse, H, causal=causal)
+    for a, b in zip(g1, g2):
+        assert rel(b, a) < 2e-3
