@@ -148,10 +148,6 @@ int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_
                  float* delta, float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g,
                  int B, int H, int N, int head_dim, float softmax_scale, int causal, void* stream);
 
-/* Test hook: pick the K5 kernel for the calling process (0 = default, 1 = the v1 single-S^T-buffer
- * kernel kept for same-box A/B and parity cross-checks).  Returns the previous setting. */
-int avb_attn_bwd_variant(int variant);
-
 /* K6: LayerNorm over rows of D (<= 1024, multiple of 8) bf16 elements, fp32 gamma/beta/stats. */
 int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma, const float* beta, void* y,
                       int64_t ldy, float* mean, float* rstd, int M, int D, float eps, void* stream);

@@ -54,7 +54,6 @@ EXPORTS: dict[str, tuple] = {
     "avb_rows_copy": (_i32, [_vp, _i64, _vp, _vp, _i64, _vp, _i32, _i32, _vp]),
     "avb_gemm": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _vp,
                         C.c_float, _i32, _vp, _vp]),
-    "avb_attn_bwd_variant": (_i32, [_i32]),
     "avb_attn_fwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _i32, C.c_float,
                             _i32, _vp]),
     "avb_attn_bwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64,

@@ -22,7 +22,6 @@
 //   red.global.add.v4.f32 into an fp32 accumulator, converted to bf16 by a tiny kernel.
 #include "tc_common.cuh"
 
-#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -920,489 +919,6 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   }
 }
 
-// ---------------------------------------------------------------------------------- backward v2 (default)
-// Same work items, persistent grid, warp roles and dQ drain as v1 above, with the TMEM plan changed so
-// the exp chain is off the critical path (v1's loop was exp(g) -> p_ready -> dV(g) -> S(g+1) ->
-// exp(g+1): ~1.7 K + ~1.5 K cycles per step, because P^T(g) lived over S^T's only buffer):
-//   TMEM  region 0 [0,128) | region 1 [128,256) | dP^T (dS^T packed over it) [256,384) | dV | dK
-//   * S^T(g) goes to region g&1, so S(g+1) is issued at the top of step g, before dV(g), and the exp
-//     group runs exp(g+1) back to back with exp(g);
-//   * P^T(g) is packed into the upper half of its region (each exp warp stores both of its chunks
-//     over its own already-read chunk hh+2), leaving the lower half [0,64) free once read;
-//   * dQ(g) accumulates into the lower half of region (g+1)&1 -- S^T(g+1)'s chunks 0/1, released by
-//     the exp warps (s_lo_read) -- so the region S(g+2) overwrites is never the one being drained:
-//     S(g+3) waits for dQ(g)'s drain a full step later;
-//   * K and V stay in shared memory (SS MMAs for S^T and dP^T; K double-buffered across items, V
-//     reloaded once the item's last dP^T has run).
-// MMA issue order per step g: S(g+1) | dV(g) | dK(g) | dP(g+1) | dQ(g).
-constexpr int C_SK = 0;                                    // K double buffer, 2 x 16 KB
-constexpr int C_SV = 32768;                                // V, 16 KB
-constexpr int C_SQD = 49152;                               // 3 stages x (Q 16 KB + dO 16 KB)
-constexpr int C_SDS = C_SQD + B_QD_STAGES * 32768;         // 2 buffers x dS^T 32 KB (then dQ staging)
-constexpr int C_SLD = C_SDS + 2 * 32768;                   // 3 stages x (lse 512 + delta 512)
-constexpr int C_BAR = C_SLD + B_QD_STAGES * 1024;
-constexpr int C_SMEM = C_BAR + 256;
-static_assert(C_SQD % 1024 == 0 && C_SDS % 1024 == 0, "attn bwd v2 alignment");
-static_assert(C_SMEM <= 232448, "attn bwd v2 smem");
-
-// TMEM column of P^T chunk c (16 packed columns) inside its S^T region: exp warp hh stores chunks
-// hh+2 and hh over its own chunk hh+2 (c=2 -> 64, c=0 -> 80, c=3 -> 96, c=1 -> 112)
-__device__ __forceinline__ uint32_t p_loc(int c) { return 64u + 16u * (2u * (c & 1) + 1u - (c >> 1)); }
-
-__global__ void __launch_bounds__(32 * kBwdWarps, 1)
-    attn_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                     const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
-                     const __grid_constant__ CUtensorMap tmDV, const BwdArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if ((reinterpret_cast<uintptr_t>(smem) & 1023) != 0) __trap();
-  auto sKb = [&](int it) { return smem + C_SK + (it & 1) * 16384; };
-  uint8_t* sV = smem + C_SV;
-  uint8_t* sQD = smem + C_SQD;
-  uint8_t* sDS = smem + C_SDS;
-  float* sLD = reinterpret_cast<float*>(smem + C_SLD);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C_BAR);
-  // Barriers a producer can complete two steps ahead of one of its waiters come in pairs indexed by
-  // the step's parity (waited with parity (g >> 1) & 1), so a phase is never aliased; so do barriers
-  // a producer re-arms while an earlier phase may still be in flight (K is loaded an item ahead) and
-  // arriving groups whose members can be a step apart (a fast exp warp reaches step g+1's arrive
-  // while a slow one has not arrived for step g).
-  uint64_t* k_full = bars + 0;                   // [2] per K buffer: K_it landed (parity (it >> 1) & 1)
-  uint64_t* v_full = bars + 2;                   // per item: V_it landed
-  uint64_t* qd_full = bars + 3;                  // [3]
-  uint64_t* qd_empty = bars + 6;                 // [3]
-  uint64_t* s_full = bars + 9;                   // [2] per S^T region
-  uint64_t* dp_full = bars + 11;
-  uint64_t* p_ready = bars + 12;                 // [2] exp group stored P^T(g)
-  uint64_t* s_lo_read = bars + 14;               // [2] exp group read S^T(g) chunks 0/1 (dQ(g-1) may land there)
-  uint64_t* pt_read = bars + 16;                 // [2] dS group read P^T(g)
-  uint64_t* ds_ready = bars + 18;
-  uint64_t* mma_done = bars + 19;                // [2] dK(g) / dQ(g) complete
-  uint64_t* dq_free = bars + 21;                 // [2] dQ(g) read out of TMEM
-  uint64_t* stage_free = bars + 23;              // [2] dQ staging (a dS^T buffer) read by its TMA reduce
-  uint64_t* acc_free = bars + 25;                // per item: dK / dV read out of TMEM
-  uint64_t* kst_free = bars + 26;                // [2] per item: its K buffer is free
-  uint64_t* v_free = bars + 28;                  // per item: its last dP^T MMA has read V
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int stride = gridDim.x;
-  constexpr int kDrain0 = kBwdCompute, kTMA = kBwdCompute + kBwdDrain, kMMA = kTMA + 1;
-
-  if (warp == kTMA && lane == 0) {
-    tc::tma_prefetch(&tmQ);
-    tc::tma_prefetch(&tmK);
-    tc::tma_prefetch(&tmV);
-    tc::tma_prefetch(&tmdO);
-    tc::tma_prefetch(&tmDQ);
-    tc::tma_prefetch(&tmDK);
-    tc::tma_prefetch(&tmDV);
-    tc::mbar_init(&k_full[0], 1);
-    tc::mbar_init(&k_full[1], 1);
-    tc::mbar_init(v_full, 1);
-    for (int s = 0; s < B_QD_STAGES; ++s) {
-      tc::mbar_init(&qd_full[s], 1);
-      tc::mbar_init(&qd_empty[s], 1);
-    }
-    tc::mbar_init(&s_full[0], 1);
-    tc::mbar_init(&s_full[1], 1);
-    tc::mbar_init(dp_full, 1);
-    for (int x = 0; x < 2; ++x) {
-      tc::mbar_init(&p_ready[x], kBwdCompute / 2);
-      tc::mbar_init(&pt_read[x], kBwdCompute / 2);
-      tc::mbar_init(&mma_done[x], 1);
-      tc::mbar_init(&dq_free[x], kBwdDrain);
-      tc::mbar_init(&s_lo_read[x], kBwdCompute / 2);
-    }
-    tc::mbar_init(ds_ready, kBwdCompute / 2);
-    tc::mbar_init(&stage_free[0], kBwdDrain);
-    tc::mbar_init(&stage_free[1], kBwdDrain);
-    tc::mbar_init(acc_free, kBwdDrain);
-    tc::mbar_init(&kst_free[0], kBwdDrain);
-    tc::mbar_init(&kst_free[1], kBwdDrain);
-    tc::mbar_init(v_free, 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == kMMA) tc::tmem_alloc(tmem_slot, 512);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tDPT = tmem + 256, tDV = tmem + 384, tDK = tmem + 448;
-  auto region = [&](int g) { return tmem + (uint32_t)(g & 1) * 128u; };
-
-  if (warp == kTMA) {
-    if (lane == 0) {
-      int g = 0, it = 0;
-      for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
-        const BwdItem t = bwd_item(a, w);
-        const int64_t bh = (int64_t)t.b * a.H + t.h;
-        if (it >= 2) tc::mbar_wait(&kst_free[it & 1], ((it >> 1) - 1) & 1);  // item it-2 done with this K buffer
-        tc::mbar_arrive_expect_tx(&k_full[it & 1], 16384);
-        tc::tma_load_3d(sKb(it), &tmK, &k_full[it & 1], t.h * HD, t.kt * BT, t.b);
-        for (int ii = 0; ii < t.nq; ++ii, ++g) {
-          const int i = t.i0 + ii, st = g % B_QD_STAGES;
-          if (g >= B_QD_STAGES) tc::mbar_wait(&qd_empty[st], ((g / B_QD_STAGES) - 1) & 1);
-          tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
-          tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], t.h * HD, i * BT, t.b);
-          tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], t.h * HD, i * BT, t.b);
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                           smem_u32(sLD + st * 256)),
-                       "l"(a.nlse2 + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
-                       : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                           smem_u32(sLD + st * 256 + 128)),
-                       "l"(a.ndelta + bh * a.Npad + i * BT), "r"(smem_u32(&qd_full[st]))
-                       : "memory");
-          if (ii == 0) {   // V_it once the previous item's last dP^T has read V_{it-1}
-            if (it >= 1) tc::mbar_wait(v_free, (it - 1) & 1);
-            tc::mbar_arrive_expect_tx(v_full, 16384);
-            tc::tma_load_3d(sV, &tmV, v_full, t.h * HD, t.kt * BT, t.b);
-          }
-        }
-      }
-    }
-  } else if (warp == kMMA) {
-    // all 32 lanes run the issue loop (warp-uniform values); one elected lane issues
-    constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T = K Q^T, dP^T = V dO^T (SS)
-    constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV / dK: A in TMEM, B (dO / Q) MN-major
-    constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
-    auto issue_s = [&](int gg, int itk) {    // S_gg^T = K Q_gg^T into region gg&1 (qd_full(gg) observed)
-      const uint32_t aQ = smem_u32(sQD + (gg % B_QD_STAGES) * 32768), aK = smem_u32(sKb(itk));
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        tc::umma_f16_ss_w(region(gg), tc::sdesc_sw128(aK + kk * 32, 16, 1024), tc::sdesc_sw128(aQ + kk * 32, 16, 1024),
-                          idSS, kk > 0);
-      tc::umma_commit_w(&s_full[gg & 1]);
-    };
-    auto issue_dp = [&](int gg) {            // dP_gg^T = V dO_gg^T (qd_full(gg), v_full observed)
-      const uint32_t aDO = smem_u32(sQD + (gg % B_QD_STAGES) * 32768) + 16384, aV = smem_u32(sV);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        tc::umma_f16_ss_w(tDPT, tc::sdesc_sw128(aV + kk * 32, 16, 1024), tc::sdesc_sw128(aDO + kk * 32, 16, 1024),
-                          idSS, kk > 0);
-      tc::umma_commit_w(dp_full);
-    };
-    int g = 0, it = 0;
-    for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
-      const BwdItem t = bwd_item(a, w);
-      const bool has_next = w + stride < a.items;
-      const int nq_next = has_next ? bwd_item(a, w + stride).nq : 0;
-      const uint32_t aK = smem_u32(sKb(it));
-      if (it == 0) {                         // prologue: S(0), dP(0)
-        tc::mbar_wait(&k_full[0], 0);
-        tc::mbar_wait(&qd_full[0], 0);
-        tc::tc_fence_after();
-        issue_s(0, 0);
-        tc::mbar_wait(v_full, 0);
-        tc::tc_fence_after();
-        issue_dp(0);
-        if (t.nq == 1) tc::umma_commit_w(v_free);   // dP(0) was item 0's last dP^T
-      }
-      for (int ii = 0; ii < t.nq; ++ii, ++g) {
-        const int st = g % B_QD_STAGES;
-        const uint32_t aQ = smem_u32(sQD + st * 32768), aDO = aQ + 16384;
-        const uint32_t aDS = smem_u32(sDS + (g & 1) * 32768);
-        const uint32_t acc = (ii > 0) ? 1u : 0u;
-        const bool last = ii + 1 == t.nq, nxt = !last || has_next;
-        // 1. S(g+1) into region (g+1)&1: P(g-1) read by dV(g-1) (issue order) and the dS group,
-        //    dQ(g-2) drained out of its lower half
-        if (nxt) {
-          const int g1 = g + 1;
-          if (last) tc::mbar_wait(&k_full[(it + 1) & 1], ((it + 1) >> 1) & 1);
-          tc::mbar_wait(&qd_full[g1 % B_QD_STAGES], (g1 / B_QD_STAGES) & 1);
-          if (g >= 1) tc::mbar_wait(&pt_read[(g - 1) & 1], ((g - 1) >> 1) & 1);
-          if (g >= 2) tc::mbar_wait(&dq_free[g & 1], ((g - 2) >> 1) & 1);
-          tc::tc_fence_after();
-          issue_s(g1, last ? it + 1 : it);
-        }
-        BWD_TRACE(0, g);
-        // 2. dV(g) += P^T(g) dO(g), A = P^T packed in region g&1
-        tc::mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
-        if (ii == 0 && it > 0) tc::mbar_wait(acc_free, (it - 1) & 1);   // previous item's dK / dV read out
-        tc::tc_fence_after();
-        BWD_TRACE(1, g);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)   // K step kk = queries [16kk, 16kk+16) = chunk kk/2, half kk&1
-          tc::umma_f16_ts_w(tDV, region(g) + p_loc(kk >> 1) + 8 * (kk & 1),
-                            tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024), idG, (acc | kk) ? 1u : 0u);
-        // 3. dK(g) += dS^T(g) Q(g), A = dS^T packed over dP^T
-        BWD_TRACE(2, g);
-        tc::mbar_wait(ds_ready, g & 1);
-        tc::tc_fence_after();
-        BWD_TRACE(3, g);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::umma_f16_ts_w(tDK, tDPT + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aQ + kk * 2048, 8192, 1024),
-                            idG, (acc | kk) ? 1u : 0u);
-        tc::umma_commit_w(&qd_empty[st]);    // Q(g) / dO(g) fully consumed (dP(g), S(g) ran earlier)
-        // 4. dP(g+1): overwrites dS^T(g) after dK(g) read it (issue order)
-        if (nxt) {
-          if (last) tc::mbar_wait(v_full, (it + 1) & 1);
-          tc::tc_fence_after();
-          issue_dp(g + 1);
-          const bool lastdp = last ? (nq_next == 1) : (ii + 2 == t.nq);
-          if (lastdp) tc::umma_commit_w(v_free);   // that was the item's last read of V
-        }
-        // 5. dQ(g) = dS(g) K into region (g+1)&1's lower half, once exp(g+1) has read it
-        BWD_TRACE(4, g);
-        if (nxt) tc::mbar_wait(&s_lo_read[(g + 1) & 1], ((g + 1) >> 1) & 1);
-        tc::tc_fence_after();
-        BWD_TRACE(5, g);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          // A = dS [q][kv]: the dS^T tile (rows kv, 128B-swizzled q chunks) seen MN-major:
-          // q chunks 16 KB apart (LBO), 8-row kv groups 1 KB apart (SBO), K step = 16 kv rows
-          const uint64_t dA = tc::sdesc_sw128(aDS + kk * 2048, 16384, 1024);
-          tc::umma_f16_ss_w(region(g + 1), dA, tc::sdesc_sw128(aK + kk * 2048, 8192, 1024), idQ, kk > 0);
-        }
-        tc::umma_commit_w(&mma_done[g & 1]);
-        BWD_TRACE(6, g);
-#ifdef K5_DBG_SERIAL
-        tc::mbar_wait(&mma_done[g & 1], (g >> 1) & 1);
-#endif
-      }
-    }
-  } else if (warp >= kDrain0) {
-    // ------------------------------------------------------------ drain warps (one per TMEM lane quadrant)
-    const int quad = warp & 3;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    int g = 0, it = 0;
-    for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
-      const BwdItem t = bwd_item(a, w);
-      for (int ii = 0; ii < t.nq; ++ii, ++g) {
-        const int pb = g & 1;
-        tc::mbar_wait(&mma_done[g & 1], (g >> 1) & 1);   // dK_g / dQ_g complete: dQ_g final, dS^T_g buffer free
-        tc::tc_fence_after();
-        if (warp == kDrain0) BWD_TRACE(12, g);
-        if (ii + 1 == t.nq) {
-          // the item's dK / dV are final and its K buffer is free (last dQ MMA done): bf16 tiles
-          // staged there (this warp's 32 rows = 4 KB, 128B-swizzled) and written by TMA stores
-          uint8_t* stg = sKb(it) + quad * 4096;
-          uint32_t kb[32];
-#pragma unroll
-          for (int hh = 0; hh < 4; ++hh) {   // dV cols [0,32) [32,64), then dK
-            uint32_t r[32];
-            tc::tmem_ld_32x32b_x32((hh < 2 ? tDV : tDK) + lane_off + (hh & 1) * 32, r);
-            tc::tmem_ld_wait();
-            const float osc = hh < 2 ? 1.f : a.scale;
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const uint32_t p = pack_bf16x2(__uint_as_float(r[2 * e]) * osc, __uint_as_float(r[2 * e + 1]) * osc);
-              if (hh < 2) r[e] = p; else kb[(hh & 1) * 16 + e] = p;
-            }
-            if (hh < 2) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                *reinterpret_cast<uint4*>(stg + lane * 128 + ((((hh & 1) * 4 + u) ^ (lane & 7)) << 4)) =
-                    make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
-            }
-          }
-          tc::tc_fence_before();
-          tc::fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tc::mbar_arrive(acc_free);   // the next item's first dV / dK MMA may overwrite them
-            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                             reinterpret_cast<uint64_t>(&tmDV)),
-                         "r"(smem_u32(stg)), "r"(t.h * HD), "r"(t.kt * BT + quad * 32), "r"(t.b)
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          }
-          __syncwarp();
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((u ^ (lane & 7)) << 4)) =
-                make_uint4(kb[4 * u], kb[4 * u + 1], kb[4 * u + 2], kb[4 * u + 3]);
-          tc::fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                             reinterpret_cast<uint64_t>(&tmDK)),
-                         "r"(smem_u32(stg)), "r"(t.h * HD), "r"(t.kt * BT + quad * 32), "r"(t.b)
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            tc::mbar_arrive(&kst_free[it & 1]);   // the TMA may load K of item it+2 here
-          }
-          __syncwarp();
-        }
-        uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
-        const uint32_t tDQ = region(g + 1);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t r[32];
-          tc::tmem_ld_32x32b_x32(tDQ + lane_off + hh * 32, r);
-          tc::tmem_ld_wait();
-          if (hh == 1) {
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&dq_free[g & 1]);
-            if (warp == kDrain0) BWD_TRACE(13, g);
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            *reinterpret_cast<uint4*>(stage + hh * 4096 + lane * 128 + ((u ^ (lane & 7)) << 4)) =
-                make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
-        }
-        tc::fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          const int q0 = (t.i0 + ii) * BT + quad * 32;
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-            asm volatile(
-                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tmDQ)),
-                "r"(smem_u32(stage + hh * 4096)), "r"(t.h * HD + hh * 32), "r"(q0), "r"(t.b)
-                : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          tc::mbar_arrive(&stage_free[pb]);   // the buffer may take dS^T_{g+2}
-        }
-        __syncwarp();
-      }
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    __syncwarp();
-  } else {
-    // ------------------------------------------------------------ compute warps, two groups
-    // warps 0-7 "exp group": P^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 into the upper half of
-    //   S^T's region; warp w owns TMEM lane quadrant (w & 3) and query chunks {hh, hh+2}, hh = (w>>2)&1
-    // warps 8-15 "dS group": dS^T = P^T (dP^T - delta) -> bf16 over dP^T (TMEM) and into smem;
-    //   warp w owns quadrant (w & 3) and chunks {2hh, 2hh+1}
-    const int quad = warp & 3, hh = (warp >> 2) & 1;
-    const bool exp_group = warp < 8;
-    const int row = quad * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
-    int g = 0;
-    for (int w = blockIdx.x; w < a.items; w += stride) {
-      const BwdItem t = bwd_item(a, w);
-      const int kv0 = t.kt * BT, kvi = kv0 + row;
-      for (int ii = 0; ii < t.nq; ++ii, ++g) {
-        const int i = t.i0 + ii, st = g % B_QD_STAGES;
-        const int q0 = i * BT;
-        const uint32_t reg = region(g);
-        if (exp_group) {
-          if (warp == 0) BWD_TRACE(14, g);
-          tc::mbar_wait(&s_full[g & 1], (g >> 1) & 1);
-          tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -lse*log2e landed
-          tc::tc_fence_after();
-          if (warp == 0) BWD_TRACE(7, g);
-          if (warp == 0) BWD_TRACE_NS(15, g);
-#pragma unroll 1
-          for (int cc = 0; cc < 2; ++cc) {
-            const int c = cc == 0 ? hh + 2 : hh;
-            const float* sl = sLD + st * 256 + c * 32;
-            const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
-                              (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
-            uint32_t rs[32], pk[16];
-            tc::tmem_ld_32x32b_x32(reg + lane_off + c * 32, rs);
-            tc::tmem_ld_wait();
-            if (cc == 1) {   // chunks 0 / 1 of S^T(g) read: dQ(g-1) may accumulate over them
-              tc::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&s_lo_read[g & 1]);
-            }
-            auto pbody = [&](auto edge_tag) {
-              constexpr bool EDGE = decltype(edge_tag)::value;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
-                const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
-                const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                      make_float2(l1.z, l1.w)};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 sv =
-                      make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
-                  const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
-                  float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
-                  if (EDGE) {
-                    const int qi = q0 + c * 32 + u * 8 + 2 * e;
-                    const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-                    const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
-                    p.x = ok0 ? p.x : 0.f;
-                    p.y = ok1 ? p.y : 0.f;
-                  }
-                  pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
-                }
-              }
-            };
-            if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
-            tc::tmem_st_32x32b_x16(reg + lane_off + p_loc(c), pk);   // over this warp's read chunk hh+2
-          }
-          tc::tmem_st_wait();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&p_ready[g & 1]);
-          if (warp == 0) BWD_TRACE(8, g);
-          if (warp == 7) BWD_TRACE(16, g);
-        } else {
-          tc::mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
-          tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -delta landed
-          tc::tc_fence_after();
-          uint32_t pk[2][16];
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) tc::tmem_ld_32x32b_x16(reg + lane_off + p_loc(2 * hh + cc), pk[cc]);
-          tc::tmem_ld_wait();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (warp == 8) BWD_TRACE(9, g);
-          if (lane == 0) tc::mbar_arrive(&pt_read[g & 1]);   // S(g+2) may now overwrite the region
-          tc::mbar_wait(dp_full, g & 1);
-          tc::tc_fence_after();
-          if (warp == 8) BWD_TRACE(10, g);
-          if (g >= 2) tc::mbar_wait(&stage_free[g & 1], ((g - 2) >> 1) & 1);  // dQ_{g-2} staging read out
-          uint8_t* ds_t = sDS + (g & 1) * 32768;
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * hh + cc;
-            const float* sd = sLD + st * 256 + 128 + c * 32;
-            uint32_t rp[32], dsk[16];
-            tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
-              const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
-              const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
-                                    make_float2(d1.z, d1.w)};
-              uint4 wv;
-              uint32_t* wp = &wv.x;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 dp =
-                    make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
-                const float2 ds = f2mul(unpack_bf16x2(pk[cc][u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
-                wp[e] = pack_bf16x2(ds.x, ds.y);
-                dsk[u * 4 + e] = wp[e];
-              }
-              st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
-            }
-            tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
-          }
-          tc::tmem_st_wait();
-          tc::fence_proxy_async();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(ds_ready);
-          if (warp == 8) BWD_TRACE(11, g);
-          if (warp == 15) BWD_TRACE(17, g);
-        }
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == kMMA) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
-  }
-}
-
 // ndelta[b,h,n] = -sum_d dO*O and nlse2[b,h,n] = -lse*log2(e) (fp32, padded rows), both in the
 // caller's delta workspace; also zeroes the dQ accumulator rows.
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o, int64_t sb_o,
@@ -1483,14 +999,7 @@ int make_maps(CUtensorMap* m, const void* p, int B, int H, int N, int64_t ld, in
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-std::atomic<int> g_bwd_variant{0};
-
 }  // namespace
-
-extern "C" int avb_attn_bwd_variant(int variant) {
-  AVB_CHECK_ARG(variant == 0 || variant == 1, "bad attention-backward variant %d", variant);
-  return g_bwd_variant.exchange(variant);
-}
 
 extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb, void* o, int64_t ld_o,
                             int64_t sb_o, float* lse, int B, int H, int N, int head_dim, float softmax_scale,
@@ -1592,15 +1101,9 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
 #ifdef AVB_DEBUG_KNOBS
   if (const char* gs = getenv("AVB_ATTN_BWD_GRID")) grid = std::min(grid, atoi(gs));
 #endif
-  if (g_bwd_variant.load() == 1) {
-    if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(attn_bwd_kernel), B_SMEM, "attn_bwd smem attr"))
-      return e;
-    attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
-  } else {
-    if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(attn_bwd2_kernel), C_SMEM, "attn_bwd smem attr"))
-      return e;
-    attn_bwd2_kernel<<<grid, 32 * kBwdWarps, C_SMEM, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
-  }
+  if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(attn_bwd_kernel), B_SMEM, "attn_bwd smem attr"))
+    return e;
+  attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(

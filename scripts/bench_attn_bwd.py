@@ -1,4 +1,4 @@
-"""K5 variants (default v2 / v1) and K4 at the config-4 and config-5 shapes: ms and TFLOP/s (algorithmic)."""
+"""K5 and K4 at the config-4 and config-5 shapes: ms and TFLOP/s (algorithmic)."""
 import json
 import os
 import sys
@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_2309_16669_b200 import _lib, ops
+from paper_2309_16669_b200 import ops
 
 
 def tm(fn, n=10):
@@ -22,7 +22,6 @@ def tm(fn, n=10):
     return e0.elapsed_time(e1) / n
 
 
-lib = _lib.load()
 for (B, N, H) in [(64, 1569, 12), (24, 2049, 16)]:
     D = H * 64
     qkv = (torch.randn(B, N, 3 * D, device="cuda") * 0.5).to(torch.bfloat16)
@@ -32,11 +31,7 @@ for (B, N, H) in [(64, 1569, 12), (24, 2049, 16)]:
     g = torch.empty(B, N, 3, D, dtype=torch.bfloat16, device="cuda")
     fl = 4.0 * B * H * N * N * 64
     res = {"shape": [B, N, H], "fwd_ms": tm(lambda: ops.attn_fwd(q, k, v, H, out=o, lse=lse))}
-    for var in (int(x) for x in os.environ.get("VARIANTS", "0,1").split(",")):
-        lib.avb_attn_bwd_variant(var)
-        res[f"bwd_v{var}_ms"] = tm(lambda: ops.attn_bwd(q, k, v, o, do, lse, H, dq=g[:, :, 0], dk=g[:, :, 1],
-                                                        dv=g[:, :, 2]))
-        res[f"bwd_v{var}_tflops"] = 2 * fl / res[f"bwd_v{var}_ms"] / 1e9
-    lib.avb_attn_bwd_variant(0)
+    res["bwd_ms"] = tm(lambda: ops.attn_bwd(q, k, v, o, do, lse, H, dq=g[:, :, 0], dk=g[:, :, 1], dv=g[:, :, 2]))
+    res["bwd_tflops"] = 2 * fl / res["bwd_ms"] / 1e9
     res["fwd_tflops"] = fl / res["fwd_ms"] / 1e9
     print(json.dumps(res), flush=True)

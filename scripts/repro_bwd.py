@@ -5,11 +5,9 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from paper_2309_16669_b200 import _lib, ops
+from paper_2309_16669_b200 import ops
 
 B, N, H, causal = (int(x) for x in sys.argv[1:5])
-var = int(sys.argv[5]) if len(sys.argv) > 5 else 0
-_lib.load().avb_attn_bwd_variant(var)
 g = torch.Generator(device="cuda").manual_seed(7)
 q, k, v = ((torch.randn(B, N, H * 64, generator=g, device="cuda")).to(torch.bfloat16) for _ in range(3))
 o, lse = ops.attn_fwd(q, k, v, H, causal=bool(causal))

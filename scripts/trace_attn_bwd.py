@@ -1,21 +1,14 @@
-"""Per-step event timeline of K5 (default kernel) for CTA 0 on the config-4 shape (trace build only):
-  AVB_NVCC_DEFS=-DAVB_ATTN_TRACE_HOOKS python -c "from paper_2309_16669_b200 import build as B; B.build()"
-Events (clock64 cycles): MMA warp 0 S(g+1) issued, 1 p_ready seen, 2 dV issued, 3 ds_ready seen,
-4 dK+dP issued, 5 s_lo_read seen, 6 dQ issued; exp warp 0: 14 top, 7 S ready, 8 P stored (16: warp 7);
-dS warp 8: 9 P read, 10 dP ready, 11 dS stored (17: warp 15); drain warp 16: 12 mma_done, 13 dQ read.
+"""Per-step event timeline of K5 for CTA (0,0,0) on the config-4 shape (AVB_ATTN_TRACE debug hook).
+Needs a build with the hooks compiled in:
+  AVB_NVCC_DEFS=-DAVB_ATTN_TRACE_HOOKS python -c "from paper_2309_16669_b200 import build as B; B.build(clean=True)"
 """
-import os
-import sys
-
+import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
-
-B, N, H = (int(x) for x in os.environ.get("SHAPE", "64,1569,12").split(","))
+B, N, H = 64, 1569, 12
 tr = torch.zeros(1024 * 32, dtype=torch.int64, device="cuda")
 os.environ["AVB_ATTN_TRACE"] = str(tr.data_ptr())
-from paper_2309_16669_b200 import ops  # noqa: E402
-
+from paper_2309_16669_b200 import ops
 D = H * 64
 qkv = (torch.randn(B, N, 3 * D, device="cuda") * 0.5).to(torch.bfloat16)
 q, k, v = qkv[:, :, :D], qkv[:, :, D:2 * D], qkv[:, :, 2 * D:]
@@ -24,19 +17,31 @@ do = torch.randn_like(o)
 for _ in range(3):
     ops.attn_bwd(q, k, v, o, do, lse, H)
 torch.cuda.synchronize()
-t = tr.view(1024, 32).cpu().numpy().astype(np.int64)
-names = {0: "m:S+1", 1: "m:p_rdy", 2: "m:dV", 3: "m:ds_rdy", 4: "m:dKdP", 5: "m:slo", 6: "m:dQ", 14: "e:top",
-         7: "e:S", 8: "e:P", 16: "e7:P", 9: "d:Prd", 10: "d:dP", 11: "d:dS", 17: "d15:dS", 12: "r:mma", 13: "r:dq"}
-order = (14, 7, 8, 16, 9, 10, 11, 17, 0, 1, 2, 3, 4, 5, 6, 12, 13)
-n = int((t[:, 7] != 0).sum())
-base = int(t[0, 7])
-for g in [int(x) for x in os.environ.get("TRACE_STEPS", "20,21,22,23,24,25").split(",")]:
-    print(g, "  ".join(f"{names[e]}={int(t[g, e]) - base}" for e in order if t[g, e] != 0))
-top = t[:n, 7]
-print("steps", n, "mean cycles/step", (top[n - 1] - top[0]) / (n - 1))
-d = lambda a, b: np.median(t[5:n - 5, b] - t[5:n - 5, a])   # noqa: E731
-print("median phases (cycles): exp S->P", d(7, 8), " exp warp7 S->P", d(7, 16), " dS dP->dS", d(10, 11),
-      " dS P->dP wait", d(9, 10), " p_rdy->dV issued", d(1, 2), " ds_rdy->dKdP issued", d(3, 4),
-      " slo wait", d(4, 5), " dQ issue", d(5, 6), " e:P(g) -> m:p_rdy(g)", d(8, 1), " d:dS -> m:ds_rdy", d(11, 3))
-s_next = np.median(t[6:n - 5, 7] - t[5:n - 6, 0])
-print("m:S(g+1) issued -> e:S(g+1) ready", s_next, "  e:P(g) -> e:S(g+1)", np.median(t[6:n - 5, 7] - t[5:n - 6, 8]))
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    ops.attn_bwd(q, k, v, o, do, lse, H)
+e1.record(); torch.cuda.synchronize()
+print("bwd ms", e0.elapsed_time(e1) / 3)
+t = tr.view(1024, 32).cpu()
+split = False
+t0 = int(t[0, 9 if split else 13])
+names = ({0: "m:p_rdy", 1: "m:dV_iss", 2: "m:ds_rdy", 3: "m:dK_iss", 4: "m:dPS_iss", 9: "c:top", 5: "c:s_full",
+          6: "c:p_arr", 7: "c:dp_full", 8: "c:ds_arr"} if split else
+         {8: "m:wait_p", 0: "m:p_rdy", 9: "m:dV_iss", 10: "m:pt_rd", 11: "m:S_iss", 1: "m:ds_rdy",
+          2: "m:dK,dP_iss", 12: "m:dQ_iss", 4: "e:top", 5: "e:s_full", 6: "d:dp_full", 7: "d:ds_arr",
+          16: "w0:copied", 17: "w4:copied", 19: "w4:s_full", 18: "w0:p_arr", 20: "w4:p_arr", 21: "w7:p_arr",
+          23: "dr:acc_free", 24: "d0:mma", 25: "d1:mma", 26: "d2:mma", 27: "d3:mma", 28: "d0:dv", 29: "d1:dv", 30: "d2:dv", 31: "d3:dv"})
+for ii in [int(x) for x in os.environ.get('TRACE_STEPS', '0,1,2,12').split(',')]:
+    print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in ((9, 5, 6, 0, 1, 7, 8, 2, 3, 4) if split else (16, 17, 4, 5, 19, 18, 20, 21, 6, 7, 8, 0, 9, 10, 11, 1, 2, 12, 24, 25, 26, 27, 28, 29, 30, 31, 23)) if int(t[ii, e]) != 0))
+if not split:
+    print("kernel start->first step top", int(t[0, 4]) - t0, " last ds_arr -> kernel end", int(t[0, 14]) - int(t[12, 7]),
+          " total", int(t[0, 14]) - t0)
+if not split:
+    import numpy as np
+    top = t[:, 4].numpy().astype(np.int64); ns = t[:, 15].numpy().astype(np.int64)
+    n = int((top != 0).sum())
+    print("steps traced", n, " mean cycles/step", (top[n - 1] - top[0]) / (n - 1), " mean ns/step", (ns[n - 1] - ns[0]) / (n - 1),
+          " clock GHz", (top[n - 1] - top[0]) / max(1, ns[n - 1] - ns[0]))
+    d = np.diff(top[:n]); print("per-13-step blocks (cycles):", [int(d[i:i + 13].sum()) for i in range(0, n - 13, 13 * 8)])
+

@@ -101,22 +101,19 @@ def test_fwd_large_dynamic_range(causal):
     assert ((lse.view(B, H, -1)[:, :, :N] - rlse).abs() / rlse.abs().clamp_min(1.0)).max().item() < 1e-3
 
 
-@pytest.mark.parametrize("B,N,H,causal", [(4, 1569, 6, False), (2, 300, 2, True), (1, 77, 1, True), (12, 785, 12, False)])
-def test_bwd_variants_agree(B, N, H, causal):
-    """The default K5 (double-buffered S^T regions) and the v1 kernel give the same gradients up to
-    the fp32 dQ reduce-add order; both match the fp32 reference."""
-    from paper_2309_16669_b200 import _lib
+# short work items (nq = 1 / 2 query tiles per key tile) with several items per persistent CTA: the
+# item-transition paths (next item's K/V, dK/dV epilogue staged through the freed K buffer) every step
+@pytest.mark.parametrize("B,N,H,causal", [(64, 128, 12, False), (64, 256, 12, True), (20, 300, 12, True)])
+def test_bwd_short_items(B, N, H, causal):
     qkv = packed(B, N, H, seed=31 + N)
-    q, k, v = (qkv[:, :, i].contiguous().view(B, N, H * 64) for i in range(3))
-    o, lse = ops.attn_fwd(q, k, v, H, causal=causal)
+    q, k, v = (qkv[:, :, i].contiguous() for i in range(3))
+    D = H * 64
+    o, lse = ops.attn_fwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), H, causal=causal)
     g = torch.Generator(device="cuda").manual_seed(5)
-    do = torch.randn(B, N, H * 64, generator=g, device="cuda").to(torch.bfloat16)
-    lib = _lib.load()
-    old = lib.avb_attn_bwd_variant(1)
-    try:
-        g1 = [t.clone() for t in ops.attn_bwd(q, k, v, o, do, lse, H, causal=causal)]
-    finally:
-        lib.avb_attn_bwd_variant(old)
-    g2 = ops.attn_bwd(q, k, v, o, do, lse, H, causal=causal)
-    for a, b in zip(g1, g2):
-        assert rel(b, a) < 2e-3
+    do = torch.randn(B, N, D, generator=g, device="cuda").to(torch.bfloat16)
+    dq, dk, dv = ops.attn_bwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), o, do, lse, H, causal=causal)
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    ro, _ = ref_attn(qf, kf, vf, 0.125, causal)
+    ro.backward(do.float().view(B, N, H, 64))
+    for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
+        assert rel(got.reshape(B, N, H, 64), ref) < 2e-2
