@@ -491,9 +491,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   uint64_t* dq_free = s_full + 4;
   uint64_t* stage_free = s_full + 5;             // [2]
   uint64_t* acc_free = s_full + 7;               // per item: dK / dV read out of TMEM by the drain warps
-  uint64_t* p_ready = s_full + 8;                // P_g^T stored in TMEM by every exp-group warp
+  uint64_t* p_ready = s_full + 8;                // P_g^T stored in TMEM by every compute warp
   uint64_t* kv_tmem = s_full + 9;                // per item: K and V copied into TMEM (A operands of S^T / dP^T)
-  uint64_t* pt_read = s_full + 10;               // the dS group has read P_g^T (S^T columns reusable)
   uint64_t* kst_free = s_full + 11;              // [2] per item: its K buffer is free (dQ MMAs done, dK/dV staged out)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 13);
 
@@ -517,15 +516,14 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     }
     tc::mbar_init(s_full, 1);
     tc::mbar_init(dp_full, 1);
-    tc::mbar_init(ds_ready, kBwdCompute / 2);   // the dS group
+    tc::mbar_init(ds_ready, kBwdCompute);       // every compute warp
     tc::mbar_init(mma_done, 1);
     tc::mbar_init(dq_free, kBwdDrain);
     tc::mbar_init(&stage_free[0], kBwdDrain);
     tc::mbar_init(&stage_free[1], kBwdDrain);
     tc::mbar_init(acc_free, kBwdDrain);
-    tc::mbar_init(p_ready, kBwdCompute / 2);    // the exp group
-    tc::mbar_init(kv_tmem, kBwdCompute / 2);    // the exp group
-    tc::mbar_init(pt_read, kBwdCompute / 2);    // the dS group
+    tc::mbar_init(p_ready, kBwdCompute);        // every compute warp
+    tc::mbar_init(kv_tmem, kBwdCompute / 2);    // the chunk-0 (K) and chunk-1 (V) warps
     tc::mbar_init(&kst_free[0], kBwdDrain);
     tc::mbar_init(&kst_free[1], kBwdDrain);
     tc::fence_barrier_init();
@@ -597,7 +595,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         const bool has_next = w + stride < a.items;
         const uint32_t aK = smem_u32(sKb(it));
         if (it == 0) {
-          tc::mbar_wait(kv_tmem, 0);      // K, V of the first item in TMEM (exp-group warps copied them)
+          tc::mbar_wait(kv_tmem, 0);      // K, V of the first item in TMEM (compute warps copied them)
           tc::tc_fence_after();
           issue_s(0);
           issue_dp(0);
@@ -620,7 +618,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
             tc::umma_f16_ts_w(tDV, tST + 32 * (kk >> 1) + 8 * (kk & 1), tc::sdesc_sw128(aDO + kk * 2048, 8192, 1024),
                             idG, (acc | kk) ? 1u : 0u);
           BWD_TRACE(9, g);
-          tc::mbar_wait(pt_read, g & 1);     // the dS group holds P_g in registers: S^T columns are free
+          // S_{g+1} overwrites P_g^T: dV(g) read it (issue order); the compute warps keep their own
+          // copy of P_g in registers for dS, so nothing else reads those columns
           if (last && has_next) tc::mbar_wait(kv_tmem, (it + 1) & 1);   // next item's K / V in TMEM
           tc::tc_fence_after();
           BWD_TRACE(10, g);
@@ -764,13 +763,15 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ compute warps, two groups
-    // warps 0-7 "exp group": P^T = exp2(S^T*scale*log2e - lse*log2e) -> bf16 over S^T (TMEM);
-    // warps 8-15 "dS group": dS^T = P^T (dP^T - delta) -> bf16 over dP^T (TMEM) and into smem.
-    // The exp group runs one tile ahead: exp(g+1) overlaps dS(g) and the MMAs of tile g.
-    // warp w: TMEM lane quadrant (w & 3) -> key rows; query chunks {2h, 2h+1}, h = (w >> 2) & 1
-    const int quad = warp & 3, hh = (warp >> 2) & 1;
-    const bool exp_group = warp < 8;
+    // ------------------------------------------------------------ compute warps
+    // warp w owns TMEM lane quadrant (w & 3) -> key rows, and query chunk c = w >> 2 (32 queries).
+    // Per step it forms P^T = exp2(S^T*scale*log2e - lse*log2e) for its chunk, stores it (bf16) over
+    // the consumed S^T chunk (dV's A operand) and, keeping P in registers, forms
+    // dS^T = P^T (dP^T - delta) once dP^T has landed -> bf16 over the consumed dP^T chunk (dK's A
+    // operand) and into the smem tile (dQ's A operand).  All 16 warps take part in both phases, so
+    // the exp phase -- on the critical chain exp(g) -> dV(g) -> S(g+1) -> exp(g+1) -- is spread over
+    // four warps per SMSP, and dS(g) runs while dV(g) / S(g+1) execute.
+    const int quad = warp & 3, c = warp >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float2 sl2 = make_float2(a.scale_log2, a.scale_log2);
@@ -778,27 +779,25 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
     for (int w = blockIdx.x; w < a.items; w += stride, ++it) {
       const BwdItem t = bwd_item(a, w);
       const int kv0 = t.kt * BT, kvi = kv0 + row;
-      if (exp_group) {
-        // this item's K (warps 0-3) / V (warps 4-7) rows -> TMEM (bf16 pairs, 32 columns): the A
-        // operands of S^T = K Q^T and dP^T = V dO^T, once the previous item's last S^T / dP^T
-        // MMAs are done reading them (dp_full of its last step: dP was issued after S)
+      if (c < 2) {
+        // this item's K (chunk-0 warps) / V (chunk-1 warps) rows -> TMEM (bf16 pairs, 32 columns): the
+        // A operands of S^T = K Q^T and dP^T = V dO^T.  The previous item's last S^T / dP^T MMAs are
+        // done reading them: this warp's dS of that step waited for its dP^T (issued after S^T).
         tc::mbar_wait(kv_full, it & 1);
-        if (g > 0) tc::mbar_wait(dp_full, (g - 1) & 1);
         tc::tc_fence_after();
-        const uint8_t* src = (hh ? sV : sKb(it)) + row * 128;
+        const uint8_t* src = (c ? sV : sKb(it)) + row * 128;
         uint32_t r[32];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint4 q = *reinterpret_cast<const uint4*>(src + ((u ^ (row & 7)) << 4));
           r[4 * u] = q.x; r[4 * u + 1] = q.y; r[4 * u + 2] = q.z; r[4 * u + 3] = q.w;
         }
-        tc::tmem_st_32x32b_x32((hh ? tV : tK) + lane_off, r);
+        tc::tmem_st_32x32b_x32((c ? tV : tK) + lane_off, r);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(kv_tmem);
         if (warp == 0) BWD_TRACE(16, g);
-        if (warp == 4) BWD_TRACE(17, g);
       }
       for (int ii = 0; ii < t.nq; ++ii, ++g) {
         const int i = t.i0 + ii, st = g % B_QD_STAGES;
@@ -807,106 +806,88 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           BWD_TRACE(4, g);
           BWD_TRACE_NS(15, g);
         }
-        if (exp_group) {
-          tc::mbar_wait(s_full, g & 1);
-          tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -lse*log2e landed
-          tc::tc_fence_after();
-          if (warp == 0) BWD_TRACE(5, g);
-          if (warp == 4) BWD_TRACE(19, g);
-#pragma unroll 1
-          for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * hh + cc;
-            const float* sl = sLD + st * 256 + c * 32;
-            const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
-                              (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
-            uint32_t rs[32], pk[16];
-            tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
-            tc::tmem_ld_wait();
-            auto pbody = [&](auto edge_tag) {
-              constexpr bool EDGE = decltype(edge_tag)::value;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
-                const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
-                const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                      make_float2(l1.z, l1.w)};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 sv =
-                      make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
-                  const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
-                  float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
-                  if (EDGE) {
-                    const int qi = q0 + c * 32 + u * 8 + 2 * e;
-                    const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
-                    const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
-                    p.x = ok0 ? p.x : 0.f;
-                    p.y = ok1 ? p.y : 0.f;
-                  }
-                  pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
-                }
-              }
-            };
-            if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
-            tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
-          }
-          tc::tmem_st_wait();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(p_ready);
-          if (warp == 0) BWD_TRACE(18, g);
-          if (warp == 4) BWD_TRACE(20, g);
-          if (warp == 7) BWD_TRACE(21, g);
-        } else {
-          tc::mbar_wait(p_ready, g & 1);
-          tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -delta landed
-          tc::tc_fence_after();
-          uint32_t pk[2][16];
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) tc::tmem_ld_32x32b_x16(tST + lane_off + (2 * hh + cc) * 32, pk[cc]);
+        // ---- P^T for this chunk
+        tc::mbar_wait(s_full, g & 1);
+        tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -lse*log2e and -delta landed
+        tc::tc_fence_after();
+        if (warp == 0) BWD_TRACE(5, g);
+        const float* sl = sLD + st * 256 + c * 32;
+        const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
+                          (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
+        uint32_t pk[16];
+        {
+          uint32_t rs[32];
+          tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
           tc::tmem_ld_wait();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(pt_read);   // S_{g+1} may now overwrite these columns
-          tc::mbar_wait(dp_full, g & 1);
-          tc::tc_fence_after();
-          if (warp == 8) BWD_TRACE(6, g);
-          if (g >= 2) tc::mbar_wait(&stage_free[g & 1], ((g - 2) >> 1) & 1);  // dQ_{g-2} staging read out
-          uint8_t* ds_t = sDS + (g & 1) * 32768;
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * hh + cc;
-            const float* sd = sLD + st * 256 + 128 + c * 32;
-            uint32_t rp[32], dsk[16];
-            tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-            tc::tmem_ld_wait();
+          auto pbody = [&](auto edge_tag) {
+            constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
-              const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
-              const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
-                                    make_float2(d1.z, d1.w)};
-              uint4 wv;
-              uint32_t* wp = &wv.x;
+              const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
+              const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
+              const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                    make_float2(l1.z, l1.w)};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float2 dp =
-                    make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
-                const float2 ds = f2mul(unpack_bf16x2(pk[cc][u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
-                wp[e] = pack_bf16x2(ds.x, ds.y);
-                dsk[u * 4 + e] = wp[e];
+                const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
+                const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
+                float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                if (EDGE) {
+                  const int qi = q0 + c * 32 + u * 8 + 2 * e;
+                  const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
+                  const bool ok1 = (qi + 1 < a.N) && (kvi < a.N) && (!a.causal || qi + 1 >= kvi);
+                  p.x = ok0 ? p.x : 0.f;
+                  p.y = ok1 ? p.y : 0.f;
+                }
+                pk[u * 4 + e] = pack_bf16x2(p.x, p.y);
               }
-              st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
             }
-            tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
-          }
-          tc::tmem_st_wait();
-          tc::fence_proxy_async();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(ds_ready);
-          if (warp == 8) BWD_TRACE(7, g);
+          };
+          if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
         }
+        tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_ready);
+        if (warp == 0) BWD_TRACE(18, g);
+        if (warp == 15) BWD_TRACE(21, g);
+        // ---- dS^T for this chunk (P from registers)
+        tc::mbar_wait(dp_full, g & 1);
+        tc::tc_fence_after();
+        if (warp == 0) BWD_TRACE(6, g);
+        if (g >= 2) tc::mbar_wait(&stage_free[g & 1], ((g - 2) >> 1) & 1);  // dQ_{g-2} staging read out
+        uint8_t* ds_t = sDS + (g & 1) * 32768;
+        {
+          const float* sd = sLD + st * 256 + 128 + c * 32;
+          uint32_t rp[32], dsk[16];
+          tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
+            const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
+            const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
+                                  make_float2(d1.z, d1.w)};
+            uint4 wv;
+            uint32_t* wp = &wv.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
+              const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
+              wp[e] = pack_bf16x2(ds.x, ds.y);
+              dsk[u * 4 + e] = wp[e];
+            }
+            st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
+          }
+          tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
+        }
+        tc::tmem_st_wait();
+        tc::fence_proxy_async();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(ds_ready);
+        if (warp == 0) BWD_TRACE(7, g);
       }
     }
   }
