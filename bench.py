@@ -62,12 +62,12 @@ UNITS = {"train": "clips/s", "train-l14": "clips/s", "clip": "pairs/s", "augment
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r02", "traffic.json")
 
 
 def ncu_traffic(kernel: str):
     """DRAM bytes (read + write) per launch of `kernel` from the committed `ncu --set full` capture
-    (profiles/r01/traffic.json, written by scripts/traffic_from_ncu.py), or None."""
+    (profiles/r02/traffic.json, written by scripts/traffic_from_ncu.py), or None."""
     try:
         with open(TRAFFIC_PATH) as fh:
             ent = json.load(fh).get(kernel)

@@ -1112,6 +1112,9 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
       q.dst = dst; q.out_dtype = out_dtype; q.out_layout = out_layout; q.tt = tt; q.tph = tph; q.tpw = tpw;
       q.tpf = (Wt + 1) / 2;
       q.fpc = std::max(1, std::min(T, 224 / q.tpf));
+#ifdef AVB_DEBUG_KNOBS
+      if (const char* e = getenv("AVB_K1_FPC")) q.fpc = std::max(1, std::min(T, atoi(e)));
+#endif
       q.ncomp = ((q.fpc * q.tpf + 31) / 32) * 32;
       // a window read ends <= 15 (misalignment) + 3*cw + 4*(NW+1) bytes into the slot
       q.slot_bytes = ((3 * cw_max + 4 * (NW + 1) + 15 + 15) / 16) * 16;

@@ -1,12 +1,13 @@
-"""Write profiles/r01/traffic.json: DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
-of the dominant kernels from `ncu --set full` reports (scripts/gpu_traffic.sh)."""
+"""Write profiles/<round>/traffic.json: DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+of the dominant kernels from the `ncu --set full` reports of scripts/profile_round.sh."""
 import csv, io, json, os, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+RND = sys.argv[1] if len(sys.argv) > 1 else "r02"
 REPORTS = {  # bench key -> (report, kernel-name substring)
-    "attn_bwd": ("gpurun_out/traffic_attn_bwd.ncu-rep", "attn_bwd_kernel"),
-    "attn_fwd": ("gpurun_out/traffic_attn_fwd.ncu-rep", "attn_fwd_kernel"),
-    "k1_rrc_normalize": ("gpurun_out/traffic_k1.ncu-rep", "k1v4_kernel"),
+    "attn_bwd": (f"gpurun_out/{RND}/attn_bwd.ncu-rep", "attn_bwd_kernel"),
+    "attn_fwd": (f"gpurun_out/{RND}/attn_fwd.ncu-rep", "attn_fwd_kernel"),
+    "k1_rrc_normalize": (f"gpurun_out/{RND}/k1.ncu-rep", "k1v4_kernel"),
 }
 out = {}
 for key, (rep, name) in REPORTS.items():
@@ -30,6 +31,7 @@ for key, (rep, name) in REPORTS.items():
                     * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(unit["gpu__time_duration.sum"], 1.0),
                     "source": rep.replace("gpurun_out/", "ncu --set full: ")}
         break
-dst = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+dst = os.path.join(ROOT, "profiles", RND, "traffic.json")
+os.makedirs(os.path.dirname(dst), exist_ok=True)
 json.dump(out, open(dst, "w"), indent=1)
 print(json.dumps(out, indent=1))
