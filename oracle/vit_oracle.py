@@ -169,7 +169,7 @@ class CpuTrainStep:
         self.opt.zero_grad()
         loss.backward()
         self.opt.step()
-        return float(loss)
+        return float(loss.detach())
 
 
 def cpu_train_step_time(cfg, num_classes: int, clips: int, threads: int, steps: int = 1):
