@@ -14,7 +14,14 @@ Modules:
                     bilinear; libswscale (the reference's scaler) is
                     cross-checked when a copy is loadable.
   vit_oracle        torch fp32 restatement of the ViT video encoder, blockwise
-                    attention and CLIP InfoNCE from PAPER.md.  PARITY UNPINNED:
-                    the reference has no encoder/attention/loss code or tests
-                    (SURVEY.md 8(c)); these follow the paper text only.
+                    attention and CLIP InfoNCE from PAPER.md.  The reference has
+                    no encoder/attention/loss code or tests, so
+                    there is no reference output to pin against; instead
+                    tests/test_vit_oracle_pins.py pins it to independent public
+                    formulations: scaled_dot_product_attention, nn.Conv3d tubelet
+                    embedding, TransformerEncoderLayer(norm_first) and open_clip's
+                    ClipLoss formula.
+  swscale_ref       libswscale (the reference's own scaler) via ctypes, called as
+                    codec.cpp:226-246 does: the augment workload's reference arm.
+  cpu_baseline      timed CPU restatement of K1 (the `port` baseline).
 """

@@ -1,7 +1,10 @@
 """Encoder / attention / loss oracle: plain torch fp32 (TEST INFRASTRUCTURE ONLY).
 
-PARITY UNPINNED: the reference package has no encoder, attention or loss code and
-no tests for them; this restates PAPER.md directly:
+The reference package has no encoder, attention or loss code and no tests for them
+(SURVEY.md 0.3, 8(c)), so there is no reference output to pin against; this restates
+PAPER.md directly, and tests/test_vit_oracle_pins.py checks it against independent public
+formulations (F.scaled_dot_product_attention, nn.Conv3d tubelet embedding,
+nn.TransformerEncoderLayer(norm_first=True), open_clip's ClipLoss formula):
   * tubelet patch-embed: non-overlapping t x h x w cubes -> Linear(3*t*h*w, D), plus the
     separable position embedding PE[t*S + s] = PE_t[t] + PE_s[1 + s] (cls: PE_s[0]) and a cls
     token;
