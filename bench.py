@@ -554,6 +554,7 @@ def main():
     ap.add_argument("--workload", default="train", choices=list(METRICS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-breakdown", action="store_true", help="skip the per-kernel breakdown pass")
+    ap.add_argument("--eager", action="store_true", help="no CUDA-graph replay of the training step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

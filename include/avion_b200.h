@@ -187,6 +187,12 @@ int avb_xent(const float* logits, int64_t ld, const int32_t* labels, int B, int 
 int avb_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask, int64_t n, float lr,
               float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
               void* stream);
+/* The same update with the step count kept on the device: *step_dev += 1 (a one-thread kernel on the
+ * stream), then the bias corrections are computed from *step_dev -- a step captured in a CUDA graph
+ * replays with the right step. */
+int avb_adamw_dev(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask, int64_t n,
+                  float lr, float beta1, float beta2, float eps, float weight_decay, int* step_dev, float grad_scale,
+                  void* stream);
 int avb_cast_bf16(const float* src, void* dst, int64_t n, void* stream);
 
 /*

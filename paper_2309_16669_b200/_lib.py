@@ -45,6 +45,8 @@ EXPORTS: dict[str, tuple] = {
     "avb_xent": (_i32, [_vp, _i64, _vp, _i32, _i32, C.c_float, _vp, _vp, _i64, _vp]),
     "avb_adamw": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, _i32,
                          C.c_float, _vp]),
+    "avb_adamw_dev": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
+                             _vp, C.c_float, _vp]),
     "avb_cast_bf16": (_i32, [_vp, _vp, _i64, _vp]),
     "avb_infonce_fwd": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "avb_infonce_bwd": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, C.c_float, _vp, _vp,

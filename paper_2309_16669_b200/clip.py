@@ -94,8 +94,8 @@ class CLIPModel:
     def optimizer_step(self, grad_scale: float = 1.0):
         self.step_num += 1
         s, o = self.store, self.opt
-        ops.adamw(s.data, s.grad, s.m, s.v, s.shadow, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, self.step_num,
-                  grad_scale, s.decay_mask)
+        ops.adamw_dev(s.data, s.grad, s.m, s.v, s.shadow, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, s.step_dev,
+                      grad_scale, s.decay_mask)
 
     def zero_grad(self):
         self.store.grad.zero_()

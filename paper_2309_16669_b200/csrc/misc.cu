@@ -198,11 +198,24 @@ __global__ void xent_kernel(const float* __restrict__ logits, int64_t ld, const 
   }
 }
 
+// bias corrections 1 - beta^step, from the host value or (step_dev != null) from a device counter,
+// so a captured CUDA graph replays the optimizer with the right step
+__device__ __forceinline__ void adamw_bc(const int* step_dev, float b1, float b2, float& bc1, float& bc2) {
+  if (step_dev) {
+    const float st = (float)*step_dev;
+    bc1 = 1.f - powf(b1, st);
+    bc2 = 1.f - powf(b2, st);
+  }
+}
+
+__global__ void adamw_tick_kernel(int* step_dev) { *step_dev += 1; }
+
 // AdamW (decoupled weight decay), bias-corrected; optional bf16 shadow of the updated weights
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, __nv_bfloat16* __restrict__ pb, const uint8_t* __restrict__ mask,
                              int64_t n, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                             float gscale) {
+                             float gscale, const int* __restrict__ step_dev) {
+  adamw_bc(step_dev, b1, b2, bc1, bc2);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i] * gscale;
     const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -222,7 +235,8 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
 __global__ void adamw_vec4_kernel(float4* __restrict__ p, const float4* __restrict__ g, float4* __restrict__ m,
                                   float4* __restrict__ v, uint2* __restrict__ pb, const uchar4* __restrict__ mask,
                                   int64_t n4, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                                  float gscale) {
+                                  float gscale, const int* __restrict__ step_dev) {
+  adamw_bc(step_dev, b1, b2, bc1, bc2);
   const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 g4 = g[i], m4 = m[i], v4 = v[i], p4 = p[i];
@@ -411,13 +425,12 @@ extern "C" int avb_xent(const float* logits, int64_t ld, const int32_t* labels, 
   return avb::launch_status("avb_xent");
 }
 
-extern "C" int avb_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask,
-                         int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay, int step,
-                         float grad_scale, void* stream) {
-  AVB_CHECK_ARG(n >= 0 && step >= 1, "adamw: n >= 0, step >= 1");
+static int adamw_launch(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask,
+                        int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                        const int* step_dev, float grad_scale, void* stream) {
   if (n == 0) return AVB_OK;
   AVB_CHECK_ARG(p && g && m && v, "null pointer");
-  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  const float bc1 = step_dev ? 1.f : 1.f - powf(beta1, (float)step), bc2 = step_dev ? 1.f : 1.f - powf(beta2, (float)step);
   auto al = [](const void* q, uintptr_t b) { return (reinterpret_cast<uintptr_t>(q) & (b - 1)) == 0; };
   const bool vec = al(p, 16) && al(g, 16) && al(m, 16) && al(v, 16) && (!p_bf16 || al(p_bf16, 8)) &&
                    (!decay_mask || al(decay_mask, 4));
@@ -428,7 +441,7 @@ extern "C" int avb_adamw(float* p, const float* g, float* m, float* v, void* p_b
     adamw_vec4_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(
         reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g), reinterpret_cast<float4*>(m),
         reinterpret_cast<float4*>(v), reinterpret_cast<uint2*>(p_bf16), reinterpret_cast<const uchar4*>(decay_mask),
-        n4, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
+        n4, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale, step_dev);
     int s = avb::launch_status("avb_adamw");
     if (s) return s;
     done = n4 * 4;
@@ -438,8 +451,26 @@ extern "C" int avb_adamw(float* p, const float* g, float* m, float* v, void* p_b
   const int blocks = (int)std::min<int64_t>((r + 255) / 256, (int64_t)avb::sm_count() * 8);
   adamw_kernel<<<blocks, 256, 0, avb::as_stream(stream)>>>(
       p + done, g + done, m + done, v + done, p_bf16 ? reinterpret_cast<__nv_bfloat16*>(p_bf16) + done : nullptr,
-      decay_mask ? decay_mask + done : nullptr, r, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
+      decay_mask ? decay_mask + done : nullptr, r, lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale, step_dev);
   return avb::launch_status("avb_adamw");
+}
+
+extern "C" int avb_adamw(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask,
+                         int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+                         float grad_scale, void* stream) {
+  AVB_CHECK_ARG(n >= 0 && step >= 1, "adamw: n >= 0, step >= 1");
+  return adamw_launch(p, g, m, v, p_bf16, decay_mask, n, lr, beta1, beta2, eps, weight_decay, step, nullptr,
+                      grad_scale, stream);
+}
+
+extern "C" int avb_adamw_dev(float* p, const float* g, float* m, float* v, void* p_bf16, const uint8_t* decay_mask,
+                             int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay,
+                             int* step_dev, float grad_scale, void* stream) {
+  AVB_CHECK_ARG(n >= 0 && step_dev, "adamw_dev: n >= 0 and a device step counter");
+  adamw_tick_kernel<<<1, 1, 0, avb::as_stream(stream)>>>(step_dev);
+  if (int s = avb::launch_status("avb_adamw_dev (tick)")) return s;
+  return adamw_launch(p, g, m, v, p_bf16, decay_mask, n, lr, beta1, beta2, eps, weight_decay, 0, step_dev, grad_scale,
+                      stream);
 }
 
 extern "C" int avb_cast_bf16(const float* src, void* dst, int64_t n, void* stream) {

@@ -185,6 +185,6 @@ class VideoEncoder(torch.nn.Module):
             return
         self._adamw_step += 1
         s = self.store
-        ops.adamw(s.data, self.flat.grad, s.m, s.v, s.shadow, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay,
-                  self._adamw_step, grad_scale, s.decay_mask)
+        ops.adamw_dev(s.data, self.flat.grad, s.m, s.v, s.shadow, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay,
+                      s.step_dev, grad_scale, s.decay_mask)
         self._shadow_version = self.flat._version

@@ -241,6 +241,16 @@ def adamw(p, g, m, v, p_bf16, lr, beta1, beta2, eps, wd, step, grad_scale=1.0, d
                                      float(grad_scale), _lib.stream_ptr()), "adamw")
 
 
+def adamw_dev(p, g, m, v, p_bf16, lr, beta1, beta2, eps, wd, step_dev, grad_scale=1.0, decay_mask=None):
+    """AdamW with the step counter in device memory (int32 [1], incremented by the call): graph-capturable."""
+    if step_dev.dtype != torch.int32 or step_dev.numel() != 1 or not step_dev.is_cuda:
+        raise InputError("step_dev must be a 1-element int32 CUDA tensor")
+    _lib.check(_lib.load().avb_adamw_dev(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(p_bf16),
+                                         _ptr(decay_mask), p.numel(), float(lr), float(beta1), float(beta2),
+                                         float(eps), float(wd), step_dev.data_ptr(), float(grad_scale),
+                                         _lib.stream_ptr()), "adamw_dev")
+
+
 def cast_bf16(src, dst):
     _lib.check(_lib.load().avb_cast_bf16(src.data_ptr(), dst.data_ptr(), src.numel(), _lib.stream_ptr()), "cast_bf16")
 

@@ -146,7 +146,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     def zero():
         store.grad.zero_()
 
-    def step():
+    def eager_step():
         zero()
         loss.zero_()
         k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
@@ -154,6 +154,22 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
         model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
         reducer.finish()
         model.optimizer_step(grad_scale=1.0 / world)
+
+    # single process: the model part of the step (everything after K1) replays from one captured CUDA
+    # graph; with N ranks the step stays eager (the DP all-reduce overlaps the backward on NCCL's stream)
+    graphed = None
+    if world == 1 and not args.eager:
+        k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
+           tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
+        graphed = model.capture_train_step(patches, labels, B, loss, warmup=args.warmup)
+
+    def step():
+        if graphed is None:
+            eager_step()
+            return
+        k1(frames, boxes_d, flips_d, (cfg.height, cfg.width), out=patches, layout="tubelet", crops_host=boxes,
+           tubelet=(cfg.cube_t, cfg.cube_h, cfg.cube_w), validate=False)
+        graphed()
 
     for _ in range(args.warmup):
         step()
@@ -177,7 +193,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
     # ---- breakdown pass (separate, after the timed region): CUDA events around every kernel family
     # and a launch counter; its shares explain `value`, they are not part of it
     nb = 0 if args.no_breakdown else max(2, min(args.steps, 4))
-    fam, launches_per_step = instrumented_pass(step, nb)
+    fam, launches_per_step = instrumented_pass(eager_step, nb)
 
     N, H = cfg.tokens, cfg.heads
     att_f = 4.0 * B * H * N * N * 64                    # per launch (one layer)
@@ -247,11 +263,14 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
             if i + 1 < nsteps:
                 feeder.submit(host, boxes, flips)
             feeder.next(out=patches)
-            zero()
-            loss.zero_()
-            model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
-            reducer.finish()
-            model.optimizer_step(grad_scale=1.0 / world)
+            if graphed is not None:
+                graphed()
+            else:
+                zero()
+                loss.zero_()
+                model.forward_backward(patches, labels, B, loss, on_layer_done=on_layer_done)
+                reducer.finish()
+                model.optimizer_step(grad_scale=1.0 / world)
             loss_h.copy_(loss, non_blocking=True)
 
     e2e_run(2)
@@ -274,7 +293,9 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks, 
         "gemm_shapes": shapes,
         "roofline": roof,
         "k1_roofline": k1_roof,
-        "breakdown": f"{nb} extra steps after the timed region with CUDA events around every launch",
+        "breakdown": f"{nb} extra eager steps after the timed region with CUDA events around every launch",
+        "execution": ("K1 launch + the model step replayed from one captured CUDA graph" if graphed is not None
+                      else "eager launches"),
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "clips/s", "h2d_bytes_per_step": int(host.numel()),
                 "d2h_bytes_per_step": 4},
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,

@@ -161,6 +161,7 @@ class ParamStore:
                 mask[o:o + numel] = 1
         self.data.copy_(host)
         self.decay_mask = mask.to(dev)
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)   # AdamW step count (device side)
         ops.cast_bf16(self.data, self.shadow)
 
     def p(self, name):
@@ -478,10 +479,43 @@ class FineTuneModel:
         self.encoder.backward(dx, ctx, on_layer_done)
 
     def optimizer_step(self, grad_scale: float = 1.0):
+        """Fused AdamW (K8); the step count lives on the device (graph-capturable), `step_num` mirrors it."""
         self.step_num += 1
         s, o = self.store, self.opt
-        ops.adamw(s.data, s.grad, s.m, s.v, s.shadow, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, self.step_num,
-                  grad_scale, s.decay_mask)
+        ops.adamw_dev(s.data, s.grad, s.m, s.v, s.shadow, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, s.step_dev,
+                      grad_scale, s.decay_mask)
 
     def zero_grad(self):
         self.store.grad.zero_()
+
+    def capture_train_step(self, patches: torch.Tensor, labels: torch.Tensor, B: int, loss: torch.Tensor,
+                           grad_scale: float = 1.0, warmup: int = 3):
+        """The whole model step -- zero grads, forward, head + CE, backward, fused AdamW -- captured into one
+        CUDA graph over the static buffers `patches` / `labels` / `loss` (K1 writes the next clips into
+        `patches` in place).  Replaying it launches the same ~250 kernels with no host work per launch.
+        `warmup` eager steps run first (on a side stream, as graph capture requires) and do train.
+        Single-process only: the DP gradient all-reduce is not captured."""
+        def body():
+            self.zero_grad()
+            loss.zero_()
+            self.forward_backward(patches, labels, B, loss)
+            self.optimizer_step(grad_scale)
+        return CapturedStep(body, warmup)
+
+
+class CapturedStep:
+    """A training-step callable captured into one CUDA graph and replayed on the current stream."""
+
+    def __init__(self, fn, warmup: int = 3):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            fn()
+
+    def __call__(self):
+        self.graph.replay()

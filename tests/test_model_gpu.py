@@ -121,3 +121,45 @@ def test_tubelet_layout_matches_patchify():
     cthw = TR.transform(fr.cuda(), boxes, flips, (64, 96), out_dtype=torch.float32)
     tub = TR.transform(fr.cuda(), boxes, flips, (64, 96), out_dtype=torch.float32, layout="tubelet", tubelet=(2, 16, 16))
     assert torch.equal(tub, VO.patchify(cthw, cfg))
+
+
+def test_adamw_dev_counter_matches_host_step():
+    """avb_adamw_dev (step count on the device, incremented per call) == avb_adamw with host steps."""
+    g0 = torch.Generator(device="cuda").manual_seed(8)
+    n = 4099
+    p1 = torch.randn(n, device="cuda", generator=g0)
+    p2 = p1.clone()
+    m1, v1, m2, v2 = (torch.zeros(n, device="cuda") for _ in range(4))
+    step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for i in range(3):
+        gr = torch.randn(n, device="cuda", generator=g0)
+        ops.adamw(p1, gr, m1, v1, None, 1e-3, 0.9, 0.999, 1e-8, 0.01, i + 1)
+        ops.adamw_dev(p2, gr, m2, v2, None, 1e-3, 0.9, 0.999, 1e-8, 0.01, step)
+    assert step.item() == 3
+    assert (p1 - p2).abs().max().item() < 1e-7
+
+
+def test_captured_train_step_matches_eager():
+    """FineTuneModel.capture_train_step: 1 warm-up step + 2 graph replays == 3 eager steps."""
+    cfg = VitConfig(frames=4, height=64, width=64, cube_t=2, depth=2, dim=128, heads=2)
+    B, C = 3, 10
+    g = torch.Generator(device="cuda").manual_seed(9)
+    patches = torch.randn(B * cfg.patches, cfg.patch_dim, generator=g, device="cuda").to(torch.bfloat16)
+    labels = torch.randint(0, C, (B,), generator=g, device="cuda", dtype=torch.int32)
+    eager = FineTuneModel(cfg, num_classes=C, seed=1)
+    graphed = FineTuneModel(cfg, num_classes=C, seed=1)
+    loss_e = torch.zeros(1, device="cuda")
+    for _ in range(3):
+        eager.zero_grad()
+        loss_e.zero_()
+        eager.forward_backward(patches, labels, B, loss_e)
+        eager.optimizer_step()
+    loss_g = torch.zeros(1, device="cuda")
+    step = graphed.capture_train_step(patches, labels, B, loss_g, warmup=1)
+    step()
+    step()
+    torch.cuda.synchronize()
+    assert graphed.store.step_dev.item() == 3
+    d = (graphed.store.data - eager.store.data).abs().max().item()
+    assert d < 1e-5, d
+    assert abs(loss_g.item() - loss_e.item()) < 1e-4 * abs(loss_e.item())
