@@ -39,14 +39,35 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     store = model.store
     reducer = GradBucketReducer(store.grad, {gname: store.group_slice(gname) for gname in store.groups})
 
-    def step():
-        store.grad.zero_()
-        loss.zero_()
+    def k1():
         TR.transform(frames, boxes_d, flips_d, (vc.height, vc.width), out=patches, layout="tubelet", crops_host=boxes,
                      tubelet=(vc.cube_t, vc.cube_h, vc.cube_w), validate=False)
+
+    def model_step():
+        store.grad.zero_()
+        loss.zero_()
         model.forward_backward(patches, tokens, eot, loss, on_layer_done=reducer.on_layer_done)
         reducer.finish()
         model.optimizer_step(grad_scale=1.0 / world)
+
+    def eager_step():
+        k1()
+        model_step()
+
+    # single process: both towers' step replays from one captured CUDA graph (as the train workload)
+    graphed = None
+    if world == 1 and not args.eager:
+        from .vit import CapturedStep
+
+        k1()
+        graphed = CapturedStep(model_step, warmup=args.warmup)
+
+    def step():
+        if graphed is None:
+            eager_step()
+        else:
+            k1()
+            graphed()
 
     for _ in range(args.warmup):
         step()
@@ -93,7 +114,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     from .train_bench import instrumented_pass
 
     nb = 0 if args.no_breakdown else 2
-    fam, lps = instrumented_pass(step, nb)
+    fam, lps = instrumented_pass(eager_step, nb)
     roof = None
     if fam:
         N, Hh = vc.tokens, vc.heads
@@ -125,6 +146,8 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
         "config": {"workload": "configs[2] ViT-B/16 CLIP dual encoder 4x224^2 (N=785) + 12L/512 text, proj 256",
                    "pairs_per_gpu": B, "global_batch": B * world, "parallelism": f"dp{world}"},
         "model_tflops": flops / (ms / 1e3) / 1e12 / world,
+        "execution": ("K1 launch + both towers' step replayed from one captured CUDA graph" if graphed is not None
+                      else "eager launches"),
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "pairs/s",
                 "h2d_bytes_per_step": int(host.numel() + tok_h.numel() * 4), "d2h_bytes_per_step": 4},
         "clocks": clocks, "loss": float(loss_h.item()),

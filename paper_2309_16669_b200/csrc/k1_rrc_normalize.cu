@@ -507,6 +507,8 @@ struct K1v4Params {
   int ncomp;       // compute threads (multiple of 32); the producer warp follows
   int slot_bytes;  // bytes per staged row (multiple of 16)
   int64_t total_bytes;
+  int nband;       // output-row bands per frame group (grid.x = frame groups * nband): finer work units
+                   // balance the waves (each band re-reads the <= 3 source rows its neighbour also needs)
 };
 
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
@@ -620,11 +622,24 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   static_assert(NOPEN <= 3, "emission count lives in rowtab.w");
   const int tid = threadIdx.x;
   const int64_t b = blockIdx.y;
-  const int t0 = blockIdx.x * p.fpc;
+  const int band = blockIdx.x % p.nband;
+  const int t0 = (blockIdx.x / p.nband) * p.fpc;
   const int4 box = *reinterpret_cast<const int4*>(p.boxes + 4 * b);
   const int x0 = box.x, y0 = box.y, cw = box.z, ch = box.w;
   if (x0 < 0 || y0 < 0 || cw < p.Wt || ch < p.Ht || x0 + cw > p.W || y0 + ch > p.H) return;
   const bool flip = p.flips ? (p.flips[b] != 0) : false;
+  // this CTA emits output rows [i_lo, i_hi) and streams the source rows [ys, ye) their windows span;
+  // the first row it pushes into is r0 = #rows closed before ys (rows < i_lo are accumulated, not stored)
+  const int i_lo = band * p.Ht / p.nband, i_hi = (band + 1) * p.Ht / p.nband;
+  int ys, ye;
+  {
+    const long long c2 = 2LL * p.Ht;
+    long long lo = floordiv_i64((long long)ch * (2 * i_lo - 1) + p.Ht, c2);
+    long long hi = floordiv_i64((long long)ch * (2 * (i_hi - 1) + 3) + p.Ht, c2);
+    ys = lo < 0 ? 0 : (int)lo;
+    ye = hi > ch ? ch : (int)hi;
+  }
+  const int r0 = k1_rows_done(ch, p.Ht, ys);
 
   // ---- smem: full [RS] | empty [RS] | rowtab [H] | ring [RS][fpc][slot_bytes]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -637,13 +652,13 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   // Built per output row (one fp64 normalisation per row, the same math and summation order as
   // k1_row_weight, so the weights are bit-identical) and scattered into the source rows it spans.
   float* rowtab_f = reinterpret_cast<float*>(rowtab);
-  for (int y = tid; y < ch; y += blockDim.x) {
+  for (int y = ys + tid; y < ye; y += blockDim.x) {
     const int base = k1_rows_done(ch, p.Ht, y);
     const int next = (y + 1 < ch) ? k1_rows_done(ch, p.Ht, y + 1) : p.Ht;
     rowtab[y] = make_float4(0.f, 0.f, 0.f, __int_as_float(next - base));
   }
   __syncthreads();
-  for (int i = tid; i < p.Ht; i += blockDim.x) {
+  for (int i = r0 + tid; i < i_hi; i += blockDim.x) {
     const long long c2 = 2LL * p.Ht;
     long long lo = floordiv_i64((long long)ch * (2 * i - 1) + p.Ht, c2);
     long long hi = floordiv_i64((long long)ch * (2 * i + 3) + p.Ht, c2);
@@ -660,6 +675,7 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
     const double r = tot > 0.0 ? 1.0 / tot : 0.0;
     for (long long k = 0; k < hi - lo; ++k) {
       const int y = (int)(lo + k);
+      if (y < ys || y >= ye) continue;
       const int q = i - k1_rows_done(ch, p.Ht, y);   // slot of row i among the rows open at y
       const double d = fabs((lo + k + 0.5 - cc) * inv);
       if (q >= 0 && q < NOPEN) rowtab_f[4 * y + q] = static_cast<float>((d < 1.0 ? 1.0 - d : 0.0) * r);
@@ -668,7 +684,7 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   if (tid == 0) {
     for (int s = 0; s < V4_RS; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], p.ncomp / 32);
+      tc::mbar_init(&empty[s], p.ncomp);   // every compute thread arrives (no elected-lane branch)
     }
     tc::fence_barrier_init();
   }
@@ -682,16 +698,16 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
     const int nf = min(p.fpc, p.T - t0);
     const uint32_t span = 3u * cw;
     // first row whose rounded-up copy (of the last frame) could reach past the tensor end
-    int tail_y = ch;
+    int tail_y = ye;
     {
       const uint8_t* last = row0 + (int64_t)(nf - 1) * p.s_t;
-      for (int y = ch - 1; y >= 0 && last + (int64_t)y * p.s_h + span + 15 > src_end; --y) tail_y = y;
+      for (int y = ye - 1; y >= ys && last + (int64_t)y * p.s_h + span + 15 > src_end; --y) tail_y = y;
     }
     int s = 0;
     uint32_t ph = 0;
-    const uint8_t* a_row = row0;
-    for (int y = 0; y < ch; ++y, a_row += p.s_h) {
-      if (y >= V4_RS) tc::mbar_wait(&empty[s], ph ^ 1);
+    const uint8_t* a_row = row0 + (int64_t)ys * p.s_h;
+    for (int y = ys; y < ye; ++y, a_row += p.s_h) {
+      if (y - ys >= V4_RS) tc::mbar_wait(&empty[s], ph ^ 1);
       uint8_t* dst = ring + (size_t)s * stage_stride;
       if (y < tail_y) {
         uint32_t tx = 0;
@@ -776,7 +792,7 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   uint8_t* dbase = reinterpret_cast<uint8_t*>(p.dst) + obase * (bf16 ? 2 : 4);
   // low bits of each row's global address (its misalignment inside the 16-byte-aligned copy)
   uint32_t alo = (uint32_t)reinterpret_cast<uintptr_t>(p.src + b * p.s_clip + (int64_t)(active ? t : t0) * p.s_t +
-                                                       (int64_t)y0 * p.s_h + (int64_t)x0 * 3);
+                                                       (int64_t)(y0 + ys) * p.s_h + (int64_t)x0 * 3);
   const uint32_t sh_lo = (uint32_t)p.s_h;
   const uint8_t* slot = ring + (size_t)(active ? f : 0) * p.slot_bytes;
   const uint8_t* slot0 = slot;
@@ -794,10 +810,14 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   for (int q = 0; q < NOPEN; ++q)
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc[q][c] = make_float2(0.f, 0.f);
-  int rowoff = 0;
+  // output row r0's offset (rows advance small_step within a tubelet band of ph_rows, big_step across)
+  int rowoff = (ph_rows >= (1 << 29)) ? r0 * small_step
+                                      : (r0 / ph_rows) * (big_step + (ph_rows - 1) * small_step) + (r0 % ph_rows) * small_step;
+  rph = (ph_rows >= (1 << 29)) ? 0 : r0 % ph_rows;
+  int orow = r0;
   int s = 0;
   uint32_t ph = 0;
-  for (int y = 0; y < ch; ++y) {
+  for (int y = ys; y < ye; ++y) {
     tc::mbar_wait(&full[s], ph);
     const float4 rw = rowtab[y];
     float2 h[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -810,8 +830,7 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
       K1HTap<NT, 1>::run(s0, s1, wp, h[1]);
       K1HTap<NT, 2>::run(s0, s1, wp, h[2]);
     }
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(&empty[s]);
+    tc::mbar_arrive(&empty[s]);
     alo += sh_lo;
     slot += stage_stride;
     if (++s == V4_RS) { s = 0; ph ^= 1; slot = slot0; }
@@ -821,8 +840,8 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[q][c] = ffma2(make_float2(wq[q], wq[q]), h[c], acc[q][c]);
     const int ne = __float_as_int(rw.w);
-    for (int e = 0; e < ne; ++e) {
-      if (active) {
+    for (int e = 0; e < ne; ++e, ++orow) {
+      if (active && orow >= i_lo && orow < i_hi) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const float2 v = ffma2(acc[0][c], sc2[c], bi2[c]);
@@ -1122,7 +1141,17 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
       const size_t smem4 = sizeof(uint64_t) * 2 * V4_RS + sizeof(float4) * (size_t)H +
                            (size_t)V4_RS * q.fpc * q.slot_bytes;
       if (smem4 <= 200 * 1024) {
-        dim3 g4((T + q.fpc - 1) / q.fpc, (unsigned)B);
+        // output-row bands per frame group: enough CTAs that the last wave is a small fraction
+        // (config 2: 8 frame groups x 64 clips = 512 CTAs on 592 slots -> 2 bands, 1024 CTAs)
+        const int64_t groups = (int64_t)((T + q.fpc - 1) / q.fpc) * B;
+        const int64_t slots = (int64_t)avb::sm_count() * 4;
+        q.nband = groups >= 2 * slots ? 1 : (groups * 2 >= slots ? 2 : 4);   // same-box sweep: 1/2/3/4/6 bands
+                                                                          // = 0.280/0.243/0.252/0.245/0.252 ms
+        q.nband = std::min(q.nband, std::max(1, Ht / 16));
+#ifdef AVB_DEBUG_KNOBS
+        if (const char* e = getenv("AVB_K1_NBAND")) q.nband = std::max(1, std::min(Ht, atoi(e)));
+#endif
+        dim3 g4((unsigned)(((T + q.fpc - 1) / q.fpc) * q.nband), (unsigned)B);
         int ast = AVB_OK;
         auto launch = [&](auto kern) {
           ast = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(kern), 200 * 1024, "k1 v4 attr");
