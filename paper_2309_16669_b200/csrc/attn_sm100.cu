@@ -8,18 +8,23 @@
 // (elements), e.g. the packed QKV GEMM output [B*N, 3*H*64] with q=qkv, k=qkv+D, v=qkv+2D.
 // LSE / delta are fp32 [B*H, Npad], Npad = roundup(N, 128).
 //
-// Forward, one CTA per (128-query tile, head, clip), 2 CTAs per SM (112 KB smem, 256 TMEM cols):
-//   warp 4  TMA: Q once, then K_j/V_j through a 2-stage ring
-//   warp 5  MMA: S = Q K_j^T (M128 N128 K64) -> TMEM; O_j = P_j V_j (M128 N64 K128, V MN-major)
-//   warps 0-3 softmax, thread = query row: two TMEM passes over S (row max, then exp2 + sum +
-//           bf16 pack into the 128B-swizzled P tile in smem), O_j folded into registers with the
-//           online-softmax rescale.
-// Backward, one CTA per (128-key tile, head, clip), 1 CTA per SM:
-//   S^T = K Q_i^T and dP^T = V dO_i^T into TMEM; warps 0-3 (thread = key row) form
-//   P^T = exp2(S^T*scale*log2e - LSE*log2e) and dS^T = scale * P^T (dP^T - delta) in smem;
-//   dV += P^T dO_i, dK += dS^T Q_i accumulate in TMEM across query tiles; dQ_i = dS_i K
-//   (dS^T's smem tile re-read as an MN-major A operand) is drained from TMEM with
-//   red.global.add.v4.f32 into an fp32 accumulator, converted to bf16 by a tiny kernel.
+// Forward (K4), one CTA per (two 128-query tiles, head, clip), 2 CTAs per SM (~100 KB smem, 256 TMEM
+// columns each), 320 threads:
+//   warp 8  TMA: both Q tiles once, then K_j/V_j (64-key tiles) through a 4-stage ring
+//   warp 9  MMA (all lanes run the loop, one elected lane issues): S_g = Q_g K_j^T (M128 N64 K64, SS)
+//           into TMEM; O_g += P_g V_j (M128 N64 K64, A = P_g read from TMEM, V MN-major)
+//   warps 0-7 two softmax groups (group g = warps 4g..4g+3, thread = query row): row max over S_g,
+//           exp2 (2 of 8 pairs on the FMA pipe), bf16 P_g packed over the consumed S_g columns, lazy
+//           (> 2^8) rescale of O_g in TMEM; O / LSE written at the end.
+// Backward (K5), persistent, one CTA per SM walking (128-key tile, head, clip) items, 704 threads:
+//   warp 21 MMA: dV += P^T dO, S^T = K Q^T (next step), dK += dS^T Q, dP^T = V dO^T (next step),
+//           dQ = dS K -- K and V live in TMEM as the A operands of S^T / dP^T;
+//   warp 20 TMA: K/V per item, Q/dO/-lse*log2e/-delta through a 3-stage ring;
+//   warps 0-15 (quadrant = w & 3 -> key rows, chunk = w >> 2 -> 32 queries): P^T = exp2(...) over the
+//           S^T chunk (TMEM), then dS^T = P^T (dP^T - delta) over the dP^T chunk (TMEM) and into a
+//           128B-swizzled smem tile (dQ's A operand), P kept in registers between the two;
+//   warps 16-19 drain: dQ TMEM -> fp32 smem staging -> TMA reduce-add into the fp32 accumulator; at
+//           an item's end dK / dV TMEM -> bf16 -> TMA stores.  A tiny kernel converts dQ to bf16.
 #include "tc_common.cuh"
 
 #include <cstdlib>

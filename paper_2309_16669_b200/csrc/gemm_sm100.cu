@@ -8,12 +8,16 @@
 // Each operand may be K-major (A:[M,K], B:[N,K]) or MN-major (A:[K,M], B:[K,N]) so
 // forward (X W^T), dgrad (dY W) and wgrad (dY^T X) all run without transposes.
 //
-// Warp roles (256 threads, 1 CTA/SM):
-//   warp 0     TMA producer (one lane)
-//   warp 1     MMA issuer   (one lane)
-//   warp 2     TMEM allocator
-//   warps 4-7  epilogue: tcgen05.ld 32 lanes x 32 columns -> bias / QuickGELU / residual /
-//              dGELU / fp32 split-K reduction -> global.
+// Warp roles (384 threads, 1 CTA/SM; the scheduler prefers the highest warp ids, so the producer
+// and MMA issuer sit above the epilogue):
+//   warps 0-7  epilogue: TMEM lane quadrant (w & 3) x column half (w >> 2); tcgen05.ld 32 lanes x 32
+//              columns -> bias / QuickGELU / residual / dGELU / fp32 split-K reduction -> bf16 tiles
+//              staged in 64B-swizzled smem and written by TMA stores (aux tiles TMA-prefetched)
+//   warp 8     TMA producer (one elected lane)
+//   warp 9     MMA issuer (all lanes run the loop, elect.sync issues)
+//   warp 10    TMEM allocator
+// CTA-pair mode (cluster of 2, tcgen05 cta_group::2, M = 256) for the large BN = 256 shapes: each
+// CTA loads its own 128 A rows and half the B rows; the leader's MMA thread commits to both CTAs.
 //
 // No reference code exists for this (absent in the reference,
 // restated from PAPER.md:258-260,727).
