@@ -62,18 +62,25 @@ def scale_clip(sws, frames_thwc: np.ndarray, box, flip: bool, target=(224, 224))
                              None, None, None)
     if not ctx:
         raise RuntimeError("sws_getContext failed")
+    # FFmpeg's SIMD scalers may read / write up to AV_INPUT_BUFFER_PADDING_SIZE (64) bytes past a plane:
+    # both planes live in padded buffers (an unpadded crop copy ending at a page boundary segfaults)
+    pad = 64
+    src_buf = np.empty(h * w * 3 + pad, dtype=np.uint8)
+    dst_buf = np.empty(th * tw * 3 + pad, dtype=np.uint8)
+    src = src_buf[:h * w * 3].reshape(h, w, 3)
+    dst = dst_buf[:th * tw * 3].reshape(th, tw, 3)
     out = np.empty((T, th, tw, 3), dtype=np.uint8)
+    sp = (ctypes.c_void_p * 4)(src_buf.ctypes.data, None, None, None)
+    ss = (ctypes.c_int * 4)(w * 3, 0, 0, 0)
+    dp = (ctypes.c_void_p * 4)(dst_buf.ctypes.data, None, None, None)
+    ds = (ctypes.c_int * 4)(tw * 3, 0, 0, 0)
     try:
         for t in range(T):
             crop = frames_thwc[t, y:y + h, x:x + w]
-            if flip:
-                crop = crop[:, ::-1]                       # hflip_planes: a reversed copy (codec.cpp:201-224)
-            src = np.ascontiguousarray(crop)
-            sp = (ctypes.c_void_p * 4)(src.ctypes.data, None, None, None)
-            ss = (ctypes.c_int * 4)(w * 3, 0, 0, 0)
-            dp = (ctypes.c_void_p * 4)(out[t].ctypes.data, None, None, None)
-            ds = (ctypes.c_int * 4)(tw * 3, 0, 0, 0)
+            # hflip_planes is a reversed copy (codec.cpp:201-224); the crop itself is pointer arithmetic
+            np.copyto(src, crop[:, ::-1] if flip else crop)
             sws.sws_scale(ctx, sp, ss, 0, h, dp, ds)   # ctypes releases the GIL around the call
+            out[t] = dst
     finally:
         sws.sws_freeContext(ctx)
     return out

@@ -31,4 +31,19 @@ for layout, shape in (("cthw", (B, 3, 16, 224, 224)), ("tubelet", (B * 8 * 14 * 
     ms = e0.elapsed_time(e1) / 20
     algo = TR.algorithmic_bytes(boxes, 16, (224, 224), 2)
     res[layout] = {"ms": ms, "GBs": algo / ms / 1e6}
+# the reference loader's planar layout [B,T,3,H,W] with crops (the generic any-stride path)
+planar = fr.permute(0, 1, 4, 2, 3).contiguous()
+out = torch.empty((B, 3, 16, 224, 224), dtype=torch.bfloat16, device="cuda")
+kw = dict(layout="cthw", crops_host=boxes, validate=False, channels_last=False)
+for _ in range(2):
+    TR.transform(planar, bd, fd, out=out, **kw)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    TR.transform(planar, bd, fd, out=out, **kw)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+res["planar_generic"] = {"ms": ms, "GBs": TR.algorithmic_bytes(boxes, 16, (224, 224), 2) / ms / 1e6}
 print(json.dumps(res))

@@ -11,8 +11,6 @@
   interior within 1 LSB.
 """
 
-import ctypes
-import glob
 import json
 import math
 import os
@@ -114,47 +112,19 @@ def test_bad_box_rejected():
         O.transform_clip(frames, (5, 0, 6, 10), False, (4, 4))
 
 
-def _load_swscale():
-    libs = glob.glob("/opt/prime-rl/.venv/lib/python3.12/site-packages/opencv_python_headless.libs/libswscale*.so*")
-    if not libs:
-        return None
-    d = os.path.dirname(libs[0])
-    try:
-        deps = [glob.glob(os.path.join(d, p + "*.so*"))[0] for p in ("libdrm", "libcrypto", "libavutil")]
-        for dep in deps:
-            ctypes.CDLL(dep, mode=ctypes.RTLD_GLOBAL)
-        return ctypes.CDLL(libs[0])
-    except (OSError, IndexError):
-        return None
-
-
 def test_swscale_cross_check_interior():
-    """Secondary cross-check against libswscale (the reference's scaler, codec.cpp:28-30,233-241)."""
-    sws = _load_swscale()
+    """Secondary cross-check against libswscale (the reference's scaler, codec.cpp:28-30,233-241), called
+    through oracle/swscale_ref.py exactly as convert_to_rgb does (padded planes)."""
+    from oracle import swscale_ref as SW
+    sws = SW.load()
     if sws is None:
         pytest.skip("no loadable libswscale copy")
-    sws.sws_getContext.restype = ctypes.c_void_p
-    sws.sws_getContext.argtypes = [ctypes.c_int] * 6 + [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                                                        ctypes.c_void_p]
-    sws.sws_scale.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
-                              ctypes.c_void_p, ctypes.c_void_p]
-    sws.sws_freeContext.argtypes = [ctypes.c_void_p]
-    rng = np.random.default_rng(3)
     # smooth image: per-pixel differences stay within the fixed-point rounding
     yy, xx = np.mgrid[0:303, 0:392]
     img = np.stack([(127 + 100 * np.sin(xx / 17.0 + c) * np.cos(yy / 13.0)) for c in range(3)], -1)
     img = np.ascontiguousarray(img.astype(np.uint8))
     w, h, tw, th = 392, 303, 224, 224
-    ctx = sws.sws_getContext(w, h, 2, tw, th, 2, 2 | 0x40000, None, None, None)
-    assert ctx
-    out = np.zeros((th, tw, 3), dtype=np.uint8)
-    src_p = (ctypes.c_void_p * 4)(img.ctypes.data, None, None, None)
-    src_s = (ctypes.c_int * 4)(w * 3, 0, 0, 0)
-    dst_p = (ctypes.c_void_p * 4)(out.ctypes.data, None, None, None)
-    dst_s = (ctypes.c_int * 4)(tw * 3, 0, 0, 0)
-    sws.sws_scale(ctx, src_p, src_s, 0, h, dst_p, dst_s)
-    sws.sws_freeContext(ctx)
+    out = SW.scale_clip(sws, img[None], (0, 0, w, h), False, (th, tw))[0]
     o = O.transform_clip(img[None], (0, 0, w, h), False, (th, tw), normalize=False)[:, 0].transpose(1, 2, 0)
     d = np.abs(o - out.astype(np.float64))[2:-2, 2:-2]
     assert d.max() <= 1.0 + 1e-9, d.max()
-    del rng
