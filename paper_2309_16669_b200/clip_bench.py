@@ -54,6 +54,14 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
         k1()
         model_step()
 
+    # breakdown pass first (eager, CUDA events around every launch), then the graph takes its own pool
+    from .train_bench import instrumented_pass
+
+    for _ in range(args.warmup):
+        eager_step()
+    nb = 0 if args.no_breakdown else 2
+    fam, lps = instrumented_pass(eager_step, nb)
+
     # single process: both towers' step replays from one captured CUDA graph (as the train workload)
     graphed = None
     if world == 1 and not args.eager:
@@ -110,11 +118,7 @@ def run(args, rank, world, local, ClockSampler, barrier, max_over_ranks, peaks):
     flops = B * world * 3.0 * (vc.forward_flops_per_clip() + 2.0 * tcfg.context * tcfg.dim * tcfg.dim * 12 *
                                 tcfg.depth + 4.0 * tcfg.context ** 2 * tcfg.dim * tcfg.depth)
     pk, src = peaks()
-    # breakdown pass after the timed region: the dominant kernel's achieved rate = the roofline
-    from .train_bench import instrumented_pass
-
-    nb = 0 if args.no_breakdown else 2
-    fam, lps = instrumented_pass(eager_step, nb)
+    # the dominant kernel of the breakdown pass: its achieved rate = the roofline
     roof = None
     if fam:
         N, Hh = vc.tokens, vc.heads

@@ -390,6 +390,8 @@ struct BwdArgs {
   int nkt, items;         // key tiles per (clip, head); work items = B * H * nkt (persistent grid)
   long long* trace;       // debug: per-step clock64 events of CTA 0 (AVB_ATTN_TRACE), else null
   int dbg;                // debug experiment flags (AVB_ATTN_DBG): 1 = skip the dQ drain
+  int dq_bf16;            // 1: dQ_g (scaled) reduce-added straight into the bf16 dq view; 0: into the fp32
+                          // accumulator (+ a convert kernel)
 };
 
 // smem (dynamic base must be 1 KB aligned; checked): all 128B-swizzled bf16 tiles first.
@@ -731,6 +733,45 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           continue;
         }
 #endif
+        if (a.dq_bf16) {
+          // dQ_g (softmax scale folded in: dS carries none) as bf16 pairs in one 4 KB SW128 box per warp
+          // (32 query rows x 64), reduce-added by TMA straight into the bf16 dq rows
+          uint8_t* stage = sDS + pb * 32768 + quad * 4096;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(tDQ + lane_off + hh * 32, r);
+            tc::tmem_ld_wait();
+            if (hh == 1) {
+              tc::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(dq_free);
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              pk[e] = pack_bf16x2(__uint_as_float(r[2 * e]) * a.scale, __uint_as_float(r[2 * e + 1]) * a.scale);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<uint4*>(stage + lane * 128 + ((((hh * 4) + u) ^ (lane & 7)) << 4)) =
+                  make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          }
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            const int q0 = (t.i0 + ii) * BT + quad * 32;
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmDQ)),
+                "r"(smem_u32(stage)), "r"(t.h * HD), "r"(q0), "r"(t.b)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            tc::mbar_arrive(&stage_free[pb]);   // the buffer may take dS^T_{g+2}
+          }
+          __syncwarp();
+          continue;
+        }
         uint8_t* stage = sDS + pb * 32768 + quad * 8192;   // 32 query rows x 64 fp32, two 4 KB SW128 boxes
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -910,7 +951,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o, int64_t sb_o,
                                     const __nv_bfloat16* __restrict__ dout, int64_t ld_do, int64_t sb_do,
                                     const float* __restrict__ lse, float* __restrict__ delta,
-                                    float* __restrict__ dq_acc, int B, int H, int N, int Npad) {
+                                    float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int64_t ld_g,
+                                    int64_t sb_g, int B, int H, int N, int Npad) {
   // 8 threads per (b, n, h) row of 64 elements
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t item = gid >> 3;
@@ -954,6 +996,8 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
     float4* z = reinterpret_cast<float4*>(dq_acc + item * HD + sub * 8);
     z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
     z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else if (dq) {   // the bf16 dQ rows are the reduce-add target themselves
+    *reinterpret_cast<uint4*>(dq + b * sb_g + (int64_t)n * ld_g + h * HD + sub * 8) = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -1032,9 +1076,10 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   AVB_CHECK_ARG(head_dim == HD, "head_dim must be 64 (got %d)", head_dim);
   AVB_CHECK_ARG(B >= 0 && H >= 1 && N >= 0, "bad attention dims");
   if (B == 0 || N == 0) return AVB_OK;
-  AVB_CHECK_ARG(q && k && v && o && dout && lse && delta && dq_acc && dq && dk && dv, "null pointer");
+  AVB_CHECK_ARG(q && k && v && o && dout && lse && delta && dq && dk && dv, "null pointer");
   AVB_CHECK_ARG(aligned16(q) && aligned16(k) && aligned16(v) && aligned16(o) && aligned16(dout) && aligned16(dq) &&
-                    aligned16(dk) && aligned16(dv) && aligned16(lse) && aligned16(delta) && aligned16(dq_acc),
+                    aligned16(dk) && aligned16(dv) && aligned16(lse) && aligned16(delta) &&
+                    (!dq_acc || aligned16(dq_acc)),
                 "pointers must be 16-byte aligned");
   AVB_CHECK_ARG(ld % 8 == 0 && sb % 8 == 0 && ld_o % 8 == 0 && sb_o % 8 == 0 && ld_g % 8 == 0 && sb_g % 8 == 0,
                 "strides must be multiples of 8 elements");
@@ -1044,7 +1089,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     const int64_t threads = (int64_t)B * N * H * 8 + (int64_t)B * H * (Npad - N);
     attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(o), ld_o, sb_o, reinterpret_cast<const __nv_bfloat16*>(dout), ld_o,
-        sb_o, lse, delta, dq_acc, B, H, N, Npad);
+        sb_o, lse, delta, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N, Npad);
     int s = avb::launch_status("attn_bwd_pre");
     if (s) return s;
   }
@@ -1057,9 +1102,13 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   CUtensorMap mdq, mdk, mdv;
   if ((s = make_maps(&mdk, dk, B, H, N, ld_g, sb_g, 32))) return s;   // dK / dV TMA stores: 32-row boxes
   if ((s = make_maps(&mdv, dv, B, H, N, ld_g, sb_g, 32))) return s;
-  if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
-                                 (uint64_t)N * H * HD, 32, 32, 1, 128)))
+  if (dq_acc) {
+    if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
+                                   (uint64_t)N * H * HD, 32, 32, 1, 128)))
+      return s;
+  } else if ((s = make_maps(&mdq, dq, B, H, N, ld_g, sb_g, 32))) {   // bf16 dq rows, 32-row boxes
     return s;
+  }
   BwdArgs a;
   a.B = B;
   a.H = H;
@@ -1076,6 +1125,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.causal = causal;
   a.nkt = (N + BT - 1) / BT;
   a.items = B * H * a.nkt;
+  a.dq_bf16 = dq_acc ? 0 : 1;
   a.trace = nullptr;
   a.dbg = 0;
 #ifdef AVB_ATTN_TRACE_HOOKS   // trace build only (scripts/trace_attn_bwd.py)
@@ -1091,6 +1141,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     return e;
   attn_bwd_kernel<<<grid, 32 * kBwdWarps, B_SMEM, st>>>(mq, mk, mv, mdo, mdq, mdk, mdv, a);
   if ((s = avb::launch_status("avb_attn_bwd"))) return s;
+  if (!dq_acc) return AVB_OK;   // dQ was reduce-added in bf16 directly
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
       dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N, softmax_scale);

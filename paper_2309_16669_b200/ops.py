@@ -128,8 +128,11 @@ def attn_fwd(q, k, v, H: int, *, scale: float | None = None, causal: bool = Fals
 
 
 def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causal: bool = False,
-             dq=None, dk=None, dv=None):
-    """dQ, dK, dV of blockwise attention (dq/dk/dv may be slices of one packed [B,N,3*H*64] buffer)."""
+             dq=None, dk=None, dv=None, fp32_dq: bool = False):
+    """dQ, dK, dV of blockwise attention (dq/dk/dv may be slices of one packed [B,N,3*H*64] buffer).
+
+    fp32_dq=False (default): every 128-key tile's dQ contribution is reduce-added in bf16 straight into
+    dq (no fp32 accumulator, no convert pass); True: fp32 accumulation + one convert kernel."""
     B, N, ld, sb = _bnhd(q, "q", H)
     for t, nm in ((k, "k"), (v, "v")):
         if _bnhd(t, nm, H) != (B, N, ld, sb):
@@ -154,10 +157,10 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
         raise InputError("dq/dk/dv must match q's [B, N]")
     _, _, ld_g, sb_g = gq
     delta = torch.empty((2, B * H, npad(N)), dtype=torch.float32, device=q.device)
-    dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device)
+    dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device) if fp32_dq else None
     scale = 64 ** -0.5 if scale is None else float(scale)
     st = _lib.load().avb_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(),
-                                  ld_o, sb_o, lse.data_ptr(), delta.data_ptr(), dq_acc.data_ptr(), dq.data_ptr(),
+                                  ld_o, sb_o, lse.data_ptr(), delta.data_ptr(), _ptr(dq_acc), dq.data_ptr(),
                                   dk.data_ptr(), dv.data_ptr(), ld_g, sb_g, B, H, N, 64, scale, int(causal),
                                   _lib.stream_ptr())
     _lib.check(st, "attn_bwd")

@@ -117,3 +117,24 @@ def test_bwd_short_items(B, N, H, causal):
     ro.backward(do.float().view(B, N, H, 64))
     for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
         assert rel(got.reshape(B, N, H, 64), ref) < 2e-2
+
+
+@pytest.mark.parametrize("B,N,H,causal", [(4, 1569, 6, False), (2, 300, 2, True), (64, 128, 12, False)])
+def test_bwd_dq_bf16_direct_vs_fp32_accumulator(B, N, H, causal):
+    """Default dQ path (each key tile's contribution reduce-added in bf16 into dq) vs the fp32 accumulator
+    path (fp32_dq=True): both within 2e-2 of fp32 math; dK / dV identical (same kernel path)."""
+    qkv = packed(B, N, H, seed=41 + N)
+    q, k, v = (qkv[:, :, i].contiguous() for i in range(3))
+    D = H * 64
+    o, lse = ops.attn_fwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), H, causal=causal)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    do = torch.randn(B, N, D, generator=g, device="cuda").to(torch.bfloat16)
+    args = (q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), o, do, lse, H)
+    d_bf = [t.clone() for t in ops.attn_bwd(*args, causal=causal)]
+    d_32 = ops.attn_bwd(*args, causal=causal, fp32_dq=True)
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    ro, _ = ref_attn(qf, kf, vf, 0.125, causal)
+    ro.backward(do.float().view(B, N, H, 64))
+    assert rel(d_bf[0].reshape(B, N, H, 64), qf.grad) < 2e-2
+    assert rel(d_32[0].reshape(B, N, H, 64), qf.grad) < 2e-2
+    assert torch.equal(d_bf[1], d_32[1]) and torch.equal(d_bf[2], d_32[2])
