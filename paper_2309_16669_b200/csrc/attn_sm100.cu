@@ -389,7 +389,8 @@ struct BwdArgs {
   int causal;
   int nkt, items;         // key tiles per (clip, head); work items = B * H * nkt (persistent grid)
   long long* trace;       // debug: per-step clock64 events of CTA 0 (AVB_ATTN_TRACE), else null
-  int dbg;                // debug experiment flags (AVB_ATTN_DBG): 1 = skip the dQ drain
+  int dbg;                // trace-build experiment flags (AVB_ATTN_DBG): 1 skip the dQ drain, 2 skip the dS smem
+                          // stores, 4 skip the dS-phase TMEM ld/st, 8 skip the exp-phase TMEM ld/st, 16 no exp2
   int dq_bf16;            // 1: dQ_g (scaled) reduce-added straight into the bf16 dq view; 0: into the fp32
                           // accumulator (+ a convert kernel)
 };
@@ -431,7 +432,9 @@ constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
       a.trace[(ii) * 32 + (ev)] = (long long)ns;                                                \
     }                                                                                           \
   } while (0)
+#define BWD_DBG(f) ((a.dbg & (f)) != 0)
 #else
+#define BWD_DBG(f) false
 #define BWD_TRACE(ev, ii) \
   do {                    \
   } while (0)
@@ -863,8 +866,14 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         uint32_t pk[16];
         {
           uint32_t rs[32];
-          tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
-          tc::tmem_ld_wait();
+          if (BWD_DBG(8)) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) rs[e] = __float_as_uint(-(float)(lane + e));
+          } else {
+            tc::tmem_ld_32x32b_x32(tST + lane_off + c * 32, rs);
+            tc::tmem_ld_wait();
+          }
+          if (warp == 0) BWD_TRACE(3, g);
           auto pbody = [&](auto edge_tag) {
             constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
@@ -877,7 +886,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
               for (int e = 0; e < 4; ++e) {
                 const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
                 const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
-                float2 p = (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                float2 p = BWD_DBG(16) ? arg : (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
                 if (EDGE) {
                   const int qi = q0 + c * 32 + u * 8 + 2 * e;
                   const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
@@ -891,8 +900,10 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           };
           if (edge) pbody(std::true_type{}); else pbody(std::false_type{});
         }
-        tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
+        if (warp == 0) BWD_TRACE(17, g);
+        if (!BWD_DBG(8)) tc::tmem_st_32x32b_x16(tST + lane_off + c * 32, pk);   // P^T over the consumed S^T chunk
         tc::tmem_st_wait();
+        if (warp == 0) BWD_TRACE(22, g);
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_ready);
@@ -907,8 +918,14 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         {
           const float* sd = sLD + st * 256 + 128 + c * 32;
           uint32_t rp[32], dsk[16];
-          tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
-          tc::tmem_ld_wait();
+          if (BWD_DBG(4)) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) rp[e] = __float_as_uint((float)(lane - e));
+          } else {
+            tc::tmem_ld_32x32b_x32(tDPT + lane_off + c * 32, rp);
+            tc::tmem_ld_wait();
+          }
+          if (warp == 0) BWD_TRACE(19, g);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
@@ -924,9 +941,10 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
               wp[e] = pack_bf16x2(ds.x, ds.y);
               dsk[u * 4 + e] = wp[e];
             }
-            st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
+            if (!BWD_DBG(2)) st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
           }
-          tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
+          if (warp == 0) BWD_TRACE(20, g);
+          if (!BWD_DBG(4)) tc::tmem_st_32x32b_x16(tDPT + lane_off + c * 32, dsk);   // dK's A operand, over the consumed dP^T chunk
         }
         tc::tmem_st_wait();
         tc::fence_proxy_async();

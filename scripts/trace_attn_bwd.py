@@ -30,10 +30,11 @@ names = ({0: "m:p_rdy", 1: "m:dV_iss", 2: "m:ds_rdy", 3: "m:dK_iss", 4: "m:dPS_i
           6: "c:p_arr", 7: "c:dp_full", 8: "c:ds_arr"} if split else
          {8: "m:wait_p", 0: "m:p_rdy", 9: "m:dV_iss", 10: "m:pt_rd", 11: "m:S_iss", 1: "m:ds_rdy",
           2: "m:dK,dP_iss", 12: "m:dQ_iss", 4: "e:top", 5: "e:s_full", 6: "d:dp_full", 7: "d:ds_arr",
-          16: "w0:copied", 17: "w4:copied", 19: "w4:s_full", 18: "w0:p_arr", 20: "w4:p_arr", 21: "w7:p_arr",
+          16: "w0:copied", 3: "e:ld_done", 17: "e:math_done", 22: "e:st_done", 19: "d:ld_done", 20: "d:math_done",
+          18: "w0:p_arr", 21: "w15:p_arr",
           23: "dr:acc_free", 24: "d0:mma", 25: "d1:mma", 26: "d2:mma", 27: "d3:mma", 28: "d0:dv", 29: "d1:dv", 30: "d2:dv", 31: "d3:dv"})
 for ii in [int(x) for x in os.environ.get('TRACE_STEPS', '0,1,2,12').split(',')]:
-    print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in ((9, 5, 6, 0, 1, 7, 8, 2, 3, 4) if split else (16, 17, 4, 5, 19, 18, 20, 21, 6, 7, 8, 0, 9, 10, 11, 1, 2, 12, 24, 25, 26, 27, 28, 29, 30, 31, 23)) if int(t[ii, e]) != 0))
+    print(ii, "  ".join(f"{names[e]}={int(t[ii, e]) - t0}" for e in ((9, 5, 6, 0, 1, 7, 8, 2, 3, 4) if split else (16, 4, 5, 3, 17, 22, 18, 21, 6, 19, 20, 7, 8, 0, 9, 10, 11, 1, 2, 12, 23)) if int(t[ii, e]) != 0))
 if not split:
     print("kernel start->first step top", int(t[0, 4]) - t0, " last ds_arr -> kernel end", int(t[0, 14]) - int(t[12, 7]),
           " total", int(t[0, 14]) - t0)
