@@ -4,6 +4,6 @@
 S=$1; shift
 for rep in 1 2; do
   for L in cur "$@"; do
-    if [ "$L" = cur ]; then echo "== cur"; timeout 300 python $S; else echo "== $L"; AVB_LIB=$L timeout 300 python $S; fi
+    if [ "$L" = cur ]; then echo "== cur"; timeout ${ABT:-300} python $S; else echo "== $L"; AVB_LIB=$L timeout ${ABT:-300} python $S; fi
   done
 done
