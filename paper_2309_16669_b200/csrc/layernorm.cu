@@ -35,30 +35,79 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// Per-lane software pipeline: every lane cp.async-copies its own 16-byte pieces of the rows S-1
+// rows ahead into a warp-private smem ring and later reads back exactly those bytes, so a
+// cp.async.wait_group is the only synchronisation (no barriers) and each warp keeps S-1 rows of
+// every input in flight without spending registers on them.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kLnFwdWarps = 8, kLnFwdStages = 4;   // 4 blocks / SM: 32 warps x 3 rows in flight
+constexpr int kLnBwdWarps = 8, kLnBwdStages = 4;   // 1 block / SM: 8 warps x 3 rows (x, dy, dx) in flight
+
 template <int NC>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
+constexpr int ln_fwd_smem() { return kLnFwdWarps * kLnFwdStages * NC * 512; }
+template <int NC>
+constexpr int ln_bwd_smem() { return kLnBwdWarps * kLnBwdStages * (3 * NC * 512 + 256) + 3 * NC * 256 * 4; }
+
+template <int NC>
+__global__ void __launch_bounds__(32 * kLnFwdWarps) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ beta,
                                                      __nv_bfloat16* __restrict__ y, int64_t ldy, float* __restrict__ mean,
                                                      float* __restrict__ rstd, int M, int D, float eps) {
+  constexpr int S = kLnFwdStages;
+  extern __shared__ uint4 ln_ring[];   // [warp][stage][NC][32 lanes]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * 8;
-  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < M; row += nwarps) {
-    uint4 raw[NC];
-    bool ok[NC];
+  uint4* ring = ln_ring + warp * S * NC * 32 + lane;
+  const int64_t nw = (int64_t)gridDim.x * kLnFwdWarps;
+  bool ok[NC];
+  float gg[NC][8], bb[NC][8];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      ok[k] = k * 256 + lane * 8 < D;
-      raw[k] = ok[k] ? *reinterpret_cast<const uint4*>(x + row * ldx + k * 256 + lane * 8) : make_uint4(0, 0, 0, 0);
+  for (int k = 0; k < NC; ++k) {
+    const int c = k * 256 + lane * 8;
+    ok[k] = c < D;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      gg[k][e] = ok[k] ? __ldg(gamma + c + e) : 0.f;
+      bb[k][e] = ok[k] ? __ldg(beta + c + e) : 0.f;
     }
-    float s = 0.f;
+  }
+  auto issue = [&](int64_t row, int s) {
+    if (row < M) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        cp_async16(ring + (s * NC + k) * 32, ok[k] ? x + row * ldx + k * 256 + lane * 8 : x, ok[k]);
+    }
+    cp_async_commit();   // one group per row slot, empty or not, so wait_group<S-1> counts rows
+  };
+  int64_t row = (int64_t)blockIdx.x * kLnFwdWarps + warp;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(row + s * nw, s);
+  for (int s = 0; row < M; row += nw, s = (s + 1 == S) ? 0 : s + 1) {
+    issue(row + (S - 1) * nw, s == 0 ? S - 1 : s - 1);
+    cp_async_wait<S - 1>();
+    uint4 raw[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) raw[k] = ok[k] ? ring[(s * NC + k) * 32] : make_uint4(0, 0, 0, 0);
+    float sum = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       float f[8];
       unpack8(raw[k], f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += f[e];
+      for (int e = 0; e < 8; ++e) sum += f[e];
     }
-    const float mu = warp_sum(s) / D;
+    const float mu = warp_sum(sum) / D;
     float q = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
@@ -75,72 +124,85 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      const int c = k * 256 + lane * 8;
       float f[8];
       unpack8(raw[k], f);
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
-      const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + c));
-      const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c + 4));
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gg[e] + bb[e];
-      *reinterpret_cast<uint4*>(y + row * ldy + c) = pack8(f);
+      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gg[k][e] + bb[k][e];
+      *reinterpret_cast<uint4*>(y + row * ldy + k * 256 + lane * 8) = pack8(f);
     }
     if (lane == 0) {
       mean[row] = mu;
       rstd[row] = rs;
     }
   }
+  cp_async_wait<0>();
 }
 
 template <int NC, bool SUM>
-__global__ void __launch_bounds__(256, (NC <= 3 ? 2 : 1)) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
+__global__ void __launch_bounds__(32 * kLnBwdWarps, 1) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy, int64_t lddy,
                                                      const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, __nv_bfloat16* dx, int64_t lddx,
                                                      float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                      float* __restrict__ dsum, int M, int D, int accumulate) {
-  extern __shared__ float red[];  // [3][D]: dgamma, dbeta, column sums of the output dx
+  constexpr int S = kLnBwdStages;
+  constexpr int SLOT = 3 * NC * 32 + 16;   // uint4 per (warp, stage): x, dy, dx pieces + mean/rstd per lane
+  extern __shared__ uint4 ln_ring[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint4* ring = ln_ring + warp * S * SLOT;
+  float* red = reinterpret_cast<float*>(ln_ring + kLnBwdWarps * S * SLOT);   // [3][D]: dgamma, dbeta, dx column sums
   for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) red[i] = 0.f;
   __syncthreads();
-  float dg[NC][8], db[NC][8], cs[NC][8];
+  bool ok[NC];
+  float gm[NC][8], dg[NC][8], db[NC][8], cs[NC][8];
 #pragma unroll
-  for (int k = 0; k < NC; ++k)
+  for (int k = 0; k < NC; ++k) {
+    const int c = k * 256 + lane * 8;
+    ok[k] = c < D;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) dg[k][e] = db[k][e] = cs[k][e] = 0.f;
-  const int64_t nwarps = (int64_t)gridDim.x * 8;
-  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < M; row += nwarps) {
-    const float mu = mean[row], rs = rstd[row];
-    // every load of the row (x, dy and the residual-stream gradient dx) issued up front: one
-    // memory round trip per row instead of two (the dx read does not depend on the row sums)
-    uint4 rx[NC], rd[NC], rp[NC];
-    bool ok[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      const int c = k * 256 + lane * 8;
-      ok[k] = c < D;
-      rx[k] = ok[k] ? *reinterpret_cast<const uint4*>(x + row * ldx + c) : make_uint4(0, 0, 0, 0);
-      rd[k] = ok[k] ? *reinterpret_cast<const uint4*>(dy + row * lddy + c) : make_uint4(0, 0, 0, 0);
-      rp[k] = (ok[k] && accumulate) ? *reinterpret_cast<const uint4*>(dx + row * lddx + c) : make_uint4(0, 0, 0, 0);
+    for (int e = 0; e < 8; ++e) {
+      gm[k][e] = ok[k] ? __ldg(gamma + c + e) : 0.f;
+      dg[k][e] = db[k][e] = cs[k][e] = 0.f;
     }
+  }
+  const int64_t nw = (int64_t)gridDim.x * kLnBwdWarps;
+  auto issue = [&](int64_t row, int s) {
+    if (row < M) {
+      uint4* slot = ring + s * SLOT;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const int c = k * 256 + lane * 8;
+        cp_async16(slot + k * 32 + lane, ok[k] ? x + row * ldx + c : x, ok[k]);
+        cp_async16(slot + (NC + k) * 32 + lane, ok[k] ? dy + row * lddy + c : dy, ok[k]);
+        cp_async16(slot + (2 * NC + k) * 32 + lane, (ok[k] && accumulate) ? dx + row * lddx + c : dx,
+                   ok[k] && accumulate);
+      }
+      float* st = reinterpret_cast<float*>(slot + 3 * NC * 32) + 2 * lane;   // this lane's private copy
+      cp_async4(st, mean + row);
+      cp_async4(st + 1, rstd + row);
+    }
+    cp_async_commit();
+  };
+  int64_t row = (int64_t)blockIdx.x * kLnBwdWarps + warp;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(row + s * nw, s);
+  for (int s = 0; row < M; row += nw, s = (s + 1 == S) ? 0 : s + 1) {
+    issue(row + (S - 1) * nw, s == 0 ? S - 1 : s - 1);
+    cp_async_wait<S - 1>();
+    const uint4* slot = ring + s * SLOT;
+    const float2 st = reinterpret_cast<const float2*>(slot + 3 * NC * 32)[lane];
+    const float mu = st.x, rs = st.y;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      const int c = k * 256 + lane * 8;
       float xv[8], dv[8];
-      unpack8(rx[k], xv);
-      unpack8(rd[k], dv);
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
-      const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      unpack8(slot[k * 32 + lane], xv);
+      unpack8(slot[(NC + k) * 32 + lane], dv);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float xh = (xv[e] - mu) * rs;
-        const float g = dv[e] * gm[e];
+        const float g = dv[e] * gm[k][e];
         s1 += g;
         s2 += g * xh;
         dg[k][e] += dv[e] * xh;
@@ -151,21 +213,17 @@ __global__ void __launch_bounds__(256, (NC <= 3 ? 2 : 1)) ln_bwd_kernel(const __
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      const int c = k * 256 + lane * 8;
       float xv[8], dv[8], pv[8], o[8];
-      unpack8(rx[k], xv);
-      unpack8(rd[k], dv);
-      unpack8(rp[k], pv);
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
-      const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      unpack8(slot[k * 32 + lane], xv);
+      unpack8(slot[(NC + k) * 32 + lane], dv);
+      unpack8(slot[(2 * NC + k) * 32 + lane], pv);   // zero-filled when !accumulate
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float xh = (xv[e] - mu) * rs;
-        o[e] = rs * (dv[e] * gm[e] - m1 - xh * m2) + pv[e];
+        o[e] = rs * (dv[e] * gm[k][e] - m1 - xh * m2) + pv[e];
       }
       const uint4 q = pack8(o);
-      *reinterpret_cast<uint4*>(dx + row * lddx + c) = q;
+      *reinterpret_cast<uint4*>(dx + row * lddx + k * 256 + lane * 8) = q;
       if (SUM) {
         float ob[8];
         unpack8(q, ob);   // sum what was stored (bf16), like a separate column-sum pass would
@@ -174,6 +232,7 @@ __global__ void __launch_bounds__(256, (NC <= 3 ? 2 : 1)) ln_bwd_kernel(const __
       }
     }
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c = k * 256 + lane * 8;
@@ -213,9 +272,13 @@ extern "C" int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma,
   if (M == 0) return AVB_OK;
   AVB_CHECK_ARG(x && gamma && beta && y && mean && rstd, "null pointer");
   AVB_CHECK_ARG(ldx % 8 == 0 && ldy % 8 == 0, "row strides must be multiples of 8");
-  const int blocks = (int)std::min<int64_t>((M + 7) / 8, (int64_t)avb::sm_count() * 8);
+  const int blocks = (int)std::min<int64_t>((M + kLnFwdWarps - 1) / kLnFwdWarps, (int64_t)avb::sm_count() * 4);
   return dispatch_nc(D, [&](auto nc) {
-    ln_fwd_kernel<decltype(nc)::value><<<blocks, 256, 0, avb::as_stream(stream)>>>(
+    constexpr int NCv = decltype(nc)::value;
+    constexpr int smem = ln_fwd_smem<NCv>();
+    if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(ln_fwd_kernel<NCv>), smem, "ln_fwd smem attr"))
+      return e;
+    ln_fwd_kernel<NCv><<<blocks, 32 * kLnFwdWarps, smem, avb::as_stream(stream)>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma, beta, reinterpret_cast<__nv_bfloat16*>(y), ldy, mean,
         rstd, M, D, eps);
     return avb::launch_status("avb_layernorm_fwd");
@@ -229,17 +292,17 @@ extern "C" int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, in
   if (M == 0) return AVB_OK;
   AVB_CHECK_ARG(dy && x && gamma && mean && rstd && dx, "null pointer");
   AVB_CHECK_ARG(lddy % 8 == 0 && ldx % 8 == 0 && lddx % 8 == 0, "row strides must be multiples of 8");
-  const int blocks = (int)std::min<int64_t>((M + 7) / 8, (int64_t)avb::sm_count() * 2);
+  const int blocks = (int)std::min<int64_t>((M + kLnBwdWarps - 1) / kLnBwdWarps, (int64_t)avb::sm_count());
   return dispatch_nc(D, [&](auto nc) {
     constexpr int NCv = decltype(nc)::value;
-    if (dx_colsum)
-      ln_bwd_kernel<NCv, true><<<blocks, 256, 3 * D * sizeof(float), avb::as_stream(stream)>>>(
+    constexpr int smem = ln_bwd_smem<NCv>();
+    auto launch = [&](auto kern, float* dsum) {
+      if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(kern), smem, "ln_bwd smem attr")) return e;
+      kern<<<blocks, 32 * kLnBwdWarps, smem, avb::as_stream(stream)>>>(
           reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
-          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, dx_colsum, M, D, accumulate);
-    else
-      ln_bwd_kernel<NCv, false><<<blocks, 256, 3 * D * sizeof(float), avb::as_stream(stream)>>>(
-          reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
-          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, nullptr, M, D, accumulate);
-    return avb::launch_status("avb_layernorm_bwd");
+          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, dsum, M, D, accumulate);
+      return avb::launch_status("avb_layernorm_bwd");
+    };
+    return dx_colsum ? launch(ln_bwd_kernel<NCv, true>, dx_colsum) : launch(ln_bwd_kernel<NCv, false>, nullptr);
   });
 }
