@@ -141,7 +141,8 @@ int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t ld, int64_
 /*
  * K5: blockwise attention backward (recomputes P from lse; no N x N storage).
  *   o, dout share (ld_o, sb_o); dq, dk, dv share (ld_g, sb_g).
- *   delta:  fp32 scratch [2, B*H, Npad] (-rowsum(dO*O), -lse*log2e).
+ *   delta:  scratch of B*H*Npad*32 bytes, 16-byte aligned (per query row: bf16 hi/lo of -lse/scale and
+ *           of -rowsum(dO*O), laid out as the extension tiles of K5's S^T / dP^T MMAs).
  *   dq_acc: NULL (default) -- each key tile's dQ contribution is reduce-added (TMA, bf16 add) straight
  *           into the zeroed bf16 dq rows; or fp32 scratch [B, N, H, 64] -- contributions accumulate in
  *           fp32 and one convert kernel writes dq (one bf16 rounding instead of one per key tile).

@@ -6,7 +6,8 @@
 //
 // Layout: Q/K/V/O are [B, N, H, 64] bf16 views with row stride `ld` and batch stride `sb`
 // (elements), e.g. the packed QKV GEMM output [B*N, 3*H*64] with q=qkv, k=qkv+D, v=qkv+2D.
-// LSE / delta are fp32 [B*H, Npad], Npad = roundup(N, 128).
+// LSE is fp32 [B*H, Npad], Npad = roundup(N, 128); the backward's statistics travel as per-query-tile
+// extension tiles of the S^T / dP^T MMAs (kExtTile, 32 bytes per row).
 //
 // Forward (K4), one CTA per (two 128-query tiles, head, clip), 2 CTAs per SM (~100 KB smem, 256 TMEM
 // columns each), 320 threads:
@@ -17,14 +18,16 @@
 //           exp2 (2 of 8 pairs on the FMA pipe), bf16 P_g packed over the consumed S_g columns, lazy
 //           (> 2^8) rescale of O_g in TMEM; O / LSE written at the end.
 // Backward (K5), persistent, one CTA per SM walking (128-key tile, head, clip) items, 704 threads:
-//   warp 21 MMA: dV += P^T dO, S^T = K Q^T (next step), dK += dS^T Q, dP^T = V dO^T (next step),
-//           dQ = dS K -- K and V live in TMEM as the A operands of S^T / dP^T;
-//   warp 20 TMA: K/V per item, Q/dO/-lse*log2e/-delta through a 3-stage ring;
+//   warp 21 MMA: dV += P^T dO, S^T = K Q^T - lse/scale (next step), dK += dS^T Q,
+//           dP^T = V dO^T - delta (next step), dQ = dS K -- K and V live in TMEM as the A operands of
+//           S^T / dP^T, the statistics enter as a fifth K step (see kExtTile);
+//   warp 20 TMA: K/V per item, Q/dO/extension tile (-lse/scale, -delta) through a 3-stage ring;
 //   warps 0-15 (quadrant = w & 3 -> key rows, chunk = w >> 2 -> 32 queries): P^T = exp2(...) over the
 //           S^T chunk (TMEM), then dS^T = P^T (dP^T - delta) over the dP^T chunk (TMEM) and into a
 //           128B-swizzled smem tile (dQ's A operand), P kept in registers between the two;
-//   warps 16-19 drain: dQ TMEM -> fp32 smem staging -> TMA reduce-add into the fp32 accumulator; at
-//           an item's end dK / dV TMEM -> bf16 -> TMA stores.  A tiny kernel converts dQ to bf16.
+//   warps 16-19 drain: dQ TMEM -> bf16 smem staging -> TMA reduce-add into the bf16 dq rows (or fp32
+//           staging into an fp32 accumulator + a convert kernel, fp32_dq); at an item's end dK / dV
+//           TMEM -> bf16 -> TMA stores.
 #include "tc_common.cuh"
 
 #include <cstdlib>
@@ -381,8 +384,7 @@ __global__ void __launch_bounds__(320, 2)
 struct BwdArgs {
   int B, H, N, Npad;
   float scale, scale_log2;
-  const float* nlse2;     // -lse * log2(e)   [B*H, Npad] (written by the pre kernel)
-  const float* ndelta;    // -rowsum(dO * O)  [B*H, Npad]
+  const uint8_t* ext;     // [B*H][Npad/128] 4 KB K-extension tiles (written by the pre kernel), see kExt*
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   int64_t ld_g, sb_g;     // strides of dk/dv
@@ -395,17 +397,29 @@ struct BwdArgs {
                           // accumulator (+ a convert kernel)
 };
 
+// The per-query softmax statistics ride inside the MMAs instead of being loaded by every compute
+// warp: each S^T / dP^T MMA gets a fifth K=16 step against a per-query-tile "extension" tile
+//   ext[q][0..1]  = bf16 hi/lo of -lse_q/scale   (so S'^T = S^T - lse/scale, and the compute warps
+//   ext[q][8..9]  = bf16 hi/lo of -delta_q        form P = exp2(S' * scale*log2e) with one FMUL2)
+//   (all other columns 0)                         (dP'^T = dP^T - delta, dS = P * dP')
+// whose A operand is a constant key-side tile with ones in columns 0-1 (S) or 8-9 (dP).  The hi/lo
+// split keeps the folded terms to ~2^-17 relative.  Tiles use the canonical no-swizzle K-major layout
+// (core matrices of 8 rows x 16 B; byte (q, k) at (q/8)*256 + (k/8)*128 + (q%8)*16 + (k%8)*2).
+constexpr int kExtTile = 4096;     // one [128 queries x 16] bf16 extension tile
+constexpr int kOnesBytes = 6144;   // 16 row groups x [zeros | (1,1,0..) | zeros] core matrices (384 B apart)
+
 // smem (dynamic base must be 1 KB aligned; checked): all 128B-swizzled bf16 tiles first.
 // dS^T is the only tile the compute warps stage in smem (A operand of dK and, seen MN-major, of
-// dQ); once dK/dQ of a step have completed, its buffer doubles as the fp32 staging of that
-// step's dQ drain.
+// dQ); once dK/dQ of a step have completed, its buffer doubles as the staging of that step's dQ
+// drain.
 constexpr int B_QD_STAGES = 3;
 constexpr int B_SK = 0, B_SV = 16384;
 constexpr int B_SQD = 32768;                               // 3 stages x (Q 16K + dO 16K)
 constexpr int B_SDS = B_SQD + B_QD_STAGES * 32768;         // 2 buffers x dS^T 32K (then dQ staging)
-constexpr int B_SLD = B_SDS + 2 * 32768;                   // 3 stages x (lse 512 + delta 512)
-constexpr int B_SK2 = B_SLD + B_QD_STAGES * 1024;           // second K buffer (next work item)
-constexpr int B_BAR = B_SK2 + 16384;
+constexpr int B_SEXT = B_SDS + 2 * 32768;                  // 3 stages x extension tile 4K
+constexpr int B_SK2 = B_SEXT + B_QD_STAGES * kExtTile;     // second K buffer (next work item)
+constexpr int B_SONE = B_SK2 + 16384;                      // constant ones tiles (A of the fifth K step)
+constexpr int B_BAR = B_SONE + kOnesBytes;
 constexpr int B_SMEM = B_BAR + 256;
 static_assert(B_SK2 % 1024 == 0, "attn bwd K2 alignment");
 static_assert(B_SMEM <= 232448, "attn bwd smem");
@@ -417,6 +431,9 @@ constexpr int kBwdDrain = 4;                 // dQ drain warps: one per TMEM lan
 constexpr int kBwdPolyFrom = AVB_BWD_POLY_FROM; // pairs e >= this (of 4) take the FMA-pipe exp2: 1 of 4
                                                 // (same-box sweep 1/2/3/4: 1.94 / 1.80 / 1.75 / 1.79 ms)
 constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
+#ifndef AVB_BWD_DS_BF16X2
+#define AVB_BWD_DS_BF16X2 1
+#endif
 
 #ifdef AVB_ATTN_TRACE_HOOKS
 #define BWD_TRACE(ev, ii)                                                                       \
@@ -462,7 +479,7 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
 //   dS group (warps 8-15): dS^T = P^T (dP^T - delta) -> bf16 over dP^T (TMEM) and into smem
 //   drain warps 16-19: dQ_g TMEM -> 128B-swizzled fp32 staging (the dS^T_g buffer) -> TMA reduce-add;
 //                      after an item's last step, its dK / dV TMEM -> bf16 global
-//   warp 20 TMA (K, V per item; Q/dO/-lse/-delta 3-stage ring), warp 21 MMA.
+//   warp 20 TMA (K, V per item; Q/dO/extension 3-stage ring), warp 21 MMA.
 struct BwdItem {
   int kt, h, b, i0, nq;
 };
@@ -489,7 +506,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   uint8_t* sV = smem + B_SV;
   uint8_t* sQD = smem + B_SQD;
   uint8_t* sDS = smem + B_SDS;
-  float* sLD = reinterpret_cast<float*>(smem + B_SLD);
+  uint8_t* sEXT = smem + B_SEXT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
   uint64_t* kv_full = bars + 0;                  // per item: K_it, V_it in smem
   uint64_t* qd_full = bars + 1;                  // [3]
@@ -509,6 +526,11 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stride = gridDim.x;
   constexpr int kDrain0 = kBwdCompute, kTMA = kBwdCompute + kBwdDrain, kMMA = kTMA + 1;
+  for (int i = threadIdx.x; i < kOnesBytes / 16; i += blockDim.x) {   // 16-byte rows of core matrices
+    const bool one = ((i >> 3) % 3) == 1;   // middle core matrix of each 8-row group: (1, 1, 0, ..., 0)
+    *reinterpret_cast<uint4*>(smem + B_SONE + 16 * i) = make_uint4(one ? 0x3F803F80u : 0u, 0u, 0u, 0u);
+  }
+  tc::fence_proxy_async();   // generic-proxy writes -> read by tcgen05.mma (async proxy) after the sync below
 
   if (warp == kTMA && lane == 0) {
     BWD_TRACE(13, 0);
@@ -561,18 +583,13 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         for (int ii = 0; ii < t.nq; ++ii, ++g) {
           const int i = t.i0 + ii, st = g % B_QD_STAGES;
           if (g >= B_QD_STAGES) tc::mbar_wait(&qd_empty[st], ((g / B_QD_STAGES) - 1) & 1);
-          tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + 1024);
+          tc::mbar_arrive_expect_tx(&qd_full[st], 32768 + kExtTile);
           tc::tma_load_3d(sQD + st * 32768, &tmQ, &qd_full[st], t.h * HD, i * BT, t.b);
           tc::tma_load_3d(sQD + st * 32768 + 16384, &tmdO, &qd_full[st], t.h * HD, i * BT, t.b);
-          const float* gl = a.nlse2 + bh * a.Npad + i * BT;
-          const float* gd = a.ndelta + bh * a.Npad + i * BT;
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                           smem_u32(sLD + st * 256)),
-                       "l"(gl), "r"(smem_u32(&qd_full[st]))
-                       : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                           smem_u32(sLD + st * 256 + 128)),
-                       "l"(gd), "r"(smem_u32(&qd_full[st]))
+          const uint8_t* ge = a.ext + (bh * (a.Npad / BT) + i) * (int64_t)kExtTile;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(sEXT + st * kExtTile)),
+                       "l"(ge), "n"(kExtTile), "r"(smem_u32(&qd_full[st]))
                        : "memory");
         }
       }
@@ -582,7 +599,9 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
       constexpr uint32_t idSS = tc::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
       constexpr uint32_t idG = tc::idesc_bf16_f32(128, 64, 0, 1);    // dV (A = P^T in TMEM), dK: B (dO / Q) MN-major
       constexpr uint32_t idQ = tc::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS (MN-major view), B = K MN-major
-      auto issue_s = [&](int gg) {      // S_gg^T = K Q_gg^T, K (A) from TMEM
+      const uint64_t dOneS = tc::sdesc_noswz(smem_u32(smem + B_SONE) + 128, 128, 384);   // columns 0-1 = 1
+      const uint64_t dOneD = tc::sdesc_noswz(smem_u32(smem + B_SONE), 128, 384);         // columns 8-9 = 1
+      auto issue_s = [&](int gg) {      // S'_gg^T = K Q_gg^T - lse/scale, K (A) from TMEM
         const int st = gg % B_QD_STAGES;
         tc::mbar_wait(&qd_full[st], (gg / B_QD_STAGES) & 1);
         tc::tc_fence_after();
@@ -590,13 +609,16 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           tc::umma_f16_ts_w(tST, tK + 8 * kk, tc::sdesc_sw128(aQ + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_f16_ss_w(tST, dOneS, tc::sdesc_noswz(smem_u32(sEXT + st * kExtTile), 128, 256), idSS, 1u);
         tc::umma_commit_w(s_full);
       };
-      auto issue_dp = [&](int gg) {     // dP_gg^T = V dO_gg^T, V (A) from TMEM (qd_full(gg) already observed)
-        const uint32_t aDO = smem_u32(sQD + (gg % B_QD_STAGES) * 32768) + 16384;
+      auto issue_dp = [&](int gg) {     // dP'_gg^T = V dO_gg^T - delta, V (A) from TMEM (qd_full(gg) already observed)
+        const int st = gg % B_QD_STAGES;
+        const uint32_t aDO = smem_u32(sQD + st * 32768) + 16384;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           tc::umma_f16_ts_w(tDPT, tV + 8 * kk, tc::sdesc_sw128(aDO + kk * 32, 16, 1024), idSS, kk > 0);
+        tc::umma_f16_ss_w(tDPT, dOneD, tc::sdesc_noswz(smem_u32(sEXT + st * kExtTile), 128, 256), idSS, 1u);
         tc::umma_commit_w(dp_full);
       };
       int g = 0, it = 0;
@@ -856,11 +878,9 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           BWD_TRACE_NS(15, g);
         }
         // ---- P^T for this chunk
-        tc::mbar_wait(s_full, g & 1);
-        tc::mbar_wait(&qd_full[st], (g / B_QD_STAGES) & 1);  // -lse*log2e and -delta landed
+        tc::mbar_wait(s_full, g & 1);   // (the statistics arrive inside S'^T / dP'^T: no smem reads here)
         tc::tc_fence_after();
         if (warp == 0) BWD_TRACE(5, g);
-        const float* sl = sLD + st * 256 + c * 32;
         const bool edge = (q0 + c * 32 + 32 > a.N) || (kv0 + quad * 32 + 32 > a.N) ||
                           (a.causal && q0 + c * 32 < kv0 + quad * 32 + 32);
         uint32_t pk[16];
@@ -878,14 +898,10 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
             constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float4 l0 = *reinterpret_cast<const float4*>(sl + u * 8);
-              const float4 l1 = *reinterpret_cast<const float4*>(sl + u * 8 + 4);
-              const float2 nl[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                    make_float2(l1.z, l1.w)};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
-                const float2 arg = f2fma(sv, sl2, nl[e]);       // S*scale*log2e - lse*log2e
+                const float2 arg = f2mul(sv, sl2);       // (S - lse/scale)*scale*log2e
                 float2 p = BWD_DBG(16) ? arg : (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
                 if (EDGE) {
                   const int qi = q0 + c * 32 + u * 8 + 2 * e;
@@ -916,7 +932,6 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         if (g >= 2) tc::mbar_wait(&stage_free[g & 1], ((g - 2) >> 1) & 1);  // dQ_{g-2} staging read out
         uint8_t* ds_t = sDS + (g & 1) * 32768;
         {
-          const float* sd = sLD + st * 256 + 128 + c * 32;
           uint32_t rp[32], dsk[16];
           if (BWD_DBG(4)) {
 #pragma unroll
@@ -928,17 +943,21 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
           if (warp == 0) BWD_TRACE(19, g);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float4 d0 = *reinterpret_cast<const float4*>(sd + u * 8);
-            const float4 d1 = *reinterpret_cast<const float4*>(sd + u * 8 + 4);
-            const float2 nd[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w), make_float2(d1.x, d1.y),
-                                  make_float2(d1.z, d1.w)};
             uint4 wv;
             uint32_t* wp = &wv.x;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 dp = make_float2(__uint_as_float(rp[u * 8 + 2 * e]), __uint_as_float(rp[u * 8 + 2 * e + 1]));
-              const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]), f2add(dp, nd[e]));  // P (dP - delta)
+#if AVB_BWD_DS_BF16X2
+              // P (dP - delta) as one bf16x2 multiply of the packed P and the packed dP' (delta folded
+              // into the MMA): 2 instructions per pair instead of unpack x2 + FMUL2 + pack
+              uint32_t dsp;
+              asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(dsp) : "r"(pk[u * 4 + e]), "r"(pack_bf16x2(dp.x, dp.y)));
+              wp[e] = dsp;
+#else
+              const float2 ds = f2mul(unpack_bf16x2(pk[u * 4 + e]), dp);  // P (dP - delta): delta folded into the MMA
               wp[e] = pack_bf16x2(ds.x, ds.y);
+#endif
               dsk[u * 4 + e] = wp[e];
             }
             if (!BWD_DBG(2)) st_sw128(ds_t, row, c * 4 + u, wv);   // dQ's A operand (read MN-major from smem)
@@ -964,11 +983,24 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
   }
 }
 
-// ndelta[b,h,n] = -sum_d dO*O and nlse2[b,h,n] = -lse*log2(e) (fp32, padded rows), both in the
-// caller's delta workspace; also zeroes the dQ accumulator rows.
+// Extension tiles (see kExtTile): row n of (b, h) gets bf16 hi/lo of -lse/scale in columns 0-1 and of
+// -rowsum(dO*O) in columns 8-9, zeros elsewhere (padded rows [N, Npad): all zero, so masked elements
+// stay finite); also zeroes the dQ accumulator rows.
+__device__ __forceinline__ void ext_row(uint8_t* ext, int64_t bh, int Npad, int n, float x, float y) {
+  uint8_t* t = ext + (bh * (Npad / BT) + n / BT) * (int64_t)kExtTile;
+  const int q = n % BT;
+  uint8_t* r = t + (q >> 3) * 256 + (q & 7) * 16;
+  const __nv_bfloat16 xh = __float2bfloat16_rn(x), yh = __float2bfloat16_rn(y);
+  const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh)), yl = __float2bfloat16_rn(y - __bfloat162float(yh));
+  const uint32_t px = (uint32_t)__bfloat16_as_ushort(xh) | ((uint32_t)__bfloat16_as_ushort(xl) << 16);
+  const uint32_t py = (uint32_t)__bfloat16_as_ushort(yh) | ((uint32_t)__bfloat16_as_ushort(yl) << 16);
+  *reinterpret_cast<uint4*>(r) = make_uint4(px, 0u, 0u, 0u);         // k 0..7
+  *reinterpret_cast<uint4*>(r + 128) = make_uint4(py, 0u, 0u, 0u);   // k 8..15
+}
+
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t ld_o, int64_t sb_o,
                                     const __nv_bfloat16* __restrict__ dout, int64_t ld_do, int64_t sb_do,
-                                    const float* __restrict__ lse, float* __restrict__ delta,
+                                    const float* __restrict__ lse, uint8_t* __restrict__ ext, float inv_scale,
                                     float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int64_t ld_g,
                                     int64_t sb_g, int B, int H, int N, int Npad) {
   // 8 threads per (b, n, h) row of 64 elements
@@ -977,14 +1009,11 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
   const int sub = gid & 7;
   const int64_t total = (int64_t)B * N * H;
   if (item >= total) {
-    // padded rows [N, Npad) of every (b, h): delta = lse term = 0, so masked elements stay finite
     const int64_t pi = gid - total * 8;
     const int npad = Npad - N;
     if (pi < (int64_t)B * H * npad) {
       const int64_t bh = pi / npad;
-      const int64_t r = bh * Npad + N + (pi - bh * npad);
-      delta[r] = 0.f;
-      delta[(int64_t)B * H * Npad + r] = 0.f;
+      ext_row(ext, bh, Npad, N + (int)(pi - bh * npad), 0.f, 0.f);
     }
     return;
   }
@@ -1006,9 +1035,9 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
   s += __shfl_xor_sync(0xffffffff, s, 2);
   s += __shfl_xor_sync(0xffffffff, s, 4);
   if (sub == 0) {
-    const int64_t r = ((int64_t)b * H + h) * Npad + n;
-    delta[r] = -s;
-    delta[(int64_t)B * H * Npad + r] = -lse[r] * kLog2e;
+    const int64_t bh = (int64_t)b * H + h;
+    const float l = lse[bh * Npad + n];
+    ext_row(ext, bh, Npad, n, isfinite(l) ? -l * inv_scale : 0.f, -s);
   }
   if (dq_acc) {
     float4* z = reinterpret_cast<float4*>(dq_acc + item * HD + sub * 8);
@@ -1107,7 +1136,8 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
     const int64_t threads = (int64_t)B * N * H * 8 + (int64_t)B * H * (Npad - N);
     attn_bwd_pre_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(o), ld_o, sb_o, reinterpret_cast<const __nv_bfloat16*>(dout), ld_o,
-        sb_o, lse, delta, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N, Npad);
+        sb_o, lse, reinterpret_cast<uint8_t*>(delta), 1.f / softmax_scale, dq_acc, reinterpret_cast<__nv_bfloat16*>(dq),
+        ld_g, sb_g, B, H, N, Npad);
     int s = avb::launch_status("attn_bwd_pre");
     if (s) return s;
   }
@@ -1134,8 +1164,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.Npad = Npad;
   a.scale = softmax_scale;
   a.scale_log2 = softmax_scale * kLog2e;
-  a.ndelta = delta;
-  a.nlse2 = delta + (int64_t)B * H * Npad;
+  a.ext = reinterpret_cast<const uint8_t*>(delta);
   a.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   a.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   a.ld_g = ld_g;

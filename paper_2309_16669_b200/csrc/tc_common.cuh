@@ -208,6 +208,23 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   return d;
 }
 
+// Canonical no-swizzle K-major layout: core matrices of 8 rows x 16 bytes (rows 16 B apart); lbo =
+// byte step between the core matrices along K, sbo = byte step between 8-row groups along M/N.
+#ifndef AVB_NOSWZ_SWAP
+#define AVB_NOSWZ_SWAP 0
+#endif
+__device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+#if AVB_NOSWZ_SWAP
+  const uint32_t t = lbo_bytes; lbo_bytes = sbo_bytes; sbo_bytes = t;
+#endif
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version = 1 (Blackwell); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, dense.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4)                        // c_format = F32

@@ -156,7 +156,7 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
     if gq[:2] != (B, N):
         raise InputError("dq/dk/dv must match q's [B, N]")
     _, _, ld_g, sb_g = gq
-    delta = torch.empty((2, B * H, npad(N)), dtype=torch.float32, device=q.device)
+    delta = torch.empty((B * H * npad(N), 8), dtype=torch.float32, device=q.device)   # 32 B per query row
     dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device) if fp32_dq else None
     scale = 64 ** -0.5 if scale is None else float(scale)
     st = _lib.load().avb_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(),

@@ -14,6 +14,9 @@ __device__ __forceinline__ uint32_t ipack2(float a, float b) {   // round-half-u
   return __byte_perm(ua, ub, 0x7632);
 }
 
+__device__ __forceinline__ uint32_t ex2h2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+__device__ __forceinline__ uint32_t ex2b2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) xu(int iters, float seed, uint32_t* sink, long long* cyc) {
   float x[8];
@@ -29,6 +32,8 @@ __global__ void __launch_bounds__(512, 1) xu(int iters, float seed, uint32_t* si
       if (MODE == 1) { acc += cvt2(x[k], x[k + 1]); x[k] += 1e-7f; }                                // 1 F2FP
       if (MODE == 2) { x[k] = ex2(x[k]) - 1.f; x[k + 1] = ex2(x[k + 1]) - 1.f; acc += cvt2(x[k], x[k + 1]); }  // 2 MUFU + 1 F2FP
       if (MODE == 3) { x[k] = ex2(x[k]) - 1.f; x[k + 1] = ex2(x[k + 1]) - 1.f; acc += ipack2(x[k], x[k + 1]); } // 2 MUFU + int pack
+      if (MODE == 5) { uint32_t h = __float_as_uint(x[k]); h = ex2h2(h); acc += h; x[k] = __uint_as_float(h ^ 0x00010001u); }  // 1 MUFU f16x2 (2 exps)
+      if (MODE == 6) { uint32_t h = __float_as_uint(x[k]); h = ex2b2(h); acc += h; x[k] = __uint_as_float(h ^ 0x00010001u); }  // 1 MUFU bf16x2 (2 exps)
       if (MODE == 4) { acc += ipack2(x[k], x[k + 1]); x[k] += 1e-7f; }                              // int pack
     }
   }
@@ -59,5 +64,7 @@ int main() {
   run<2>("ex2 x2 + F2FP", 2, 1);
   run<3>("ex2 x2 + int pack", 2, 1);
   run<4>("int pack (IADD x2 + PRMT)", 0, 1);
+  run<5>("ex2.f16x2 (2 exps/op)", 1, 0);
+  run<6>("ex2.bf16x2 (2 exps/op)", 1, 0);
   return 0;
 }
