@@ -425,11 +425,11 @@ static_assert(B_SK2 % 1024 == 0, "attn bwd K2 alignment");
 static_assert(B_SMEM <= 232448, "attn bwd smem");
 constexpr int kBwdCompute = 16;              // compute warps: 4 per TMEM lane quadrant (one 32-query chunk each)
 constexpr int kBwdDrain = 4;                 // dQ drain warps: one per TMEM lane quadrant
-#ifndef AVB_BWD_POLY_FROM
-#define AVB_BWD_POLY_FROM 3
+#ifndef AVB_BWD_POLY8_FROM
+#define AVB_BWD_POLY8_FROM 6
 #endif
-constexpr int kBwdPolyFrom = AVB_BWD_POLY_FROM; // pairs e >= this (of 4) take the FMA-pipe exp2: 1 of 4
-                                                // (same-box sweep 1/2/3/4: 1.94 / 1.80 / 1.75 / 1.79 ms)
+constexpr int kBwdPoly8From = AVB_BWD_POLY8_FROM; // pairs with (index & 7) >= this take the FMA-pipe exp2
+                                                // (same-box sweep 4/5/6: 1.503 / 1.475 / 1.436 ms at config 4)
 constexpr int kBwdWarps = kBwdCompute + kBwdDrain + 2;
 #ifndef AVB_BWD_DS_BF16X2
 #define AVB_BWD_DS_BF16X2 1
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
               for (int e = 0; e < 4; ++e) {
                 const float2 sv = make_float2(__uint_as_float(rs[u * 8 + 2 * e]), __uint_as_float(rs[u * 8 + 2 * e + 1]));
                 const float2 arg = f2mul(sv, sl2);       // (S - lse/scale)*scale*log2e
-                float2 p = BWD_DBG(16) ? arg : (e >= kBwdPolyFrom) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                float2 p = BWD_DBG(16) ? arg : (((u * 4 + e) & 7) >= kBwdPoly8From) ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
                 if (EDGE) {
                   const int qi = q0 + c * 32 + u * 8 + 2 * e;
                   const bool ok0 = (qi < a.N) && (kvi < a.N) && (!a.causal || qi >= kvi);
