@@ -393,7 +393,39 @@ def run_feed(args, rank, world, local):
                 "reference's 'valid until next iter' contract); the device-only kernel rate is the roofline",
         "gpu_launches": args.steps,
         "clocks": clocks,
+        **({"cpu_baseline": _feed_cpu_baseline()} if (rank == 0 and world == 1 and not args.no_cpu_baseline) else {}),
     }
+
+
+def _feed_cpu_job(cores: int):
+    """The reference has no device hand-off: its CPU equivalent of "uint8 Batch.frames -> normalised
+    bf16 clips" is the normalise + cast it defers, restated in torch on all cores."""
+    import torch
+
+    from oracle import cpu_baseline as CB
+
+    torch.set_num_threads(cores)
+    fr = torch.randint(0, 256, (FEED_B, FEED_T, 3, 224, 224), dtype=torch.uint8)
+    m = torch.tensor(CB.CLIP_MEAN).view(1, 1, 3, 1, 1)
+    sd = torch.tensor(CB.CLIP_STD).view(1, 1, 3, 1, 1)
+
+    def job():
+        return ((fr.float() / 255.0 - m) / sd).permute(0, 2, 1, 3, 4).to(torch.bfloat16).contiguous()
+
+    return job
+
+
+def _feed_cpu_baseline(reps: int = 5) -> dict:
+    cores = os.cpu_count() or 1
+    job = _feed_cpu_job(cores)
+    job()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        job()
+    sec = time.perf_counter() - t0
+    return {"value": FEED_B * reps / sec, "unit": "clips/s", "cores": cores, "kind": "port",
+            "sample": f"{reps} x {FEED_B} clips of uint8 [16,3,224,224] -> (x/255 - mean)/std -> bf16 [B,3,T,H,W], "
+                      f"torch on {cores} host threads (the normalise + cast the reference defers, SPEC.md:232)"}
 
 
 def _feed_into(feeder, batches, outs):
@@ -426,19 +458,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "config": workload_config(wl, world)}
     if wl == "feed":
-        # the reference has no device hand-off: its CPU equivalent of "uint8 Batch.frames -> normalised
-        # bf16 clips" is the normalise + cast it defers, restated in torch on all cores
-        import torch
-
-        from oracle import cpu_baseline as CB
-
-        torch.set_num_threads(cores)
-        fr = torch.randint(0, 256, (FEED_B, FEED_T, 3, 224, 224), dtype=torch.uint8)
-        m = torch.tensor(CB.CLIP_MEAN).view(1, 1, 3, 1, 1)
-        sd = torch.tensor(CB.CLIP_STD).view(1, 1, 3, 1, 1)
-
-        def job():
-            return ((fr.float() / 255.0 - m) / sd).permute(0, 2, 1, 3, 4).to(torch.bfloat16).contiguous()
+        job = _feed_cpu_job(cores)
 
         for _ in range(args.warmup):
             job()
