@@ -152,14 +152,29 @@ int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_
                  float* delta, float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g,
                  int B, int H, int N, int head_dim, float softmax_scale, int causal, void* stream);
 
+/*
+ * K5, bit-reproducible: identical to avb_attn_bwd except that every 128-key tile stores its dQ
+ * contribution into its own fp32 slice of dq_part [ceil(N/128), B, N, H, 64] (16-byte aligned) and
+ * one pass sums the slices in key-tile order, so dq (like dk, dv) is the same bit pattern run to run.
+ * Costs ceil(N/128) x B*N*H*256 bytes of workspace and the extra traffic; meant for debugging.
+ */
+int avb_attn_bwd_deterministic(const void* q, const void* k, const void* v, int64_t ld, int64_t sb,
+                               const void* o, const void* dout, int64_t ld_o, int64_t sb_o, const float* lse,
+                               float* delta, float* dq_part, void* dq, void* dk, void* dv, int64_t ld_g,
+                               int64_t sb_g, int B, int H, int N, int head_dim, float softmax_scale, int causal,
+                               void* stream);
+
 /* K6: LayerNorm over rows of D (<= 1024, multiple of 8) bf16 elements, fp32 gamma/beta/stats. */
 int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma, const float* beta, void* y,
                       int64_t ldy, float* mean, float* rstd, int M, int D, float eps, void* stream);
 /* dx (=|+=) LN'(dy); dgamma/dbeta (nullable) += column reductions; dx_colsum (nullable) += column
- * sums of the resulting dx (the bias gradient of the linear layer whose output is this residual). */
+ * sums of the resulting dx (the bias gradient of the linear layer whose output is this residual).
+ * work: fp32 scratch of avb_layernorm_bwd_workspace(D) floats (per-block partials); every reduction
+ * runs in a fixed order, so the result is bit-reproducible. */
 int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, int64_t ldx, const float* gamma,
                       const float* mean, const float* rstd, void* dx, int64_t lddx, float* dgamma,
-                      float* dbeta, float* dx_colsum, int M, int D, int accumulate, void* stream);
+                      float* dbeta, float* dx_colsum, float* work, int M, int D, int accumulate, void* stream);
+int avb_layernorm_bwd_workspace(int D);
 
 /* out[n] += sum_m X[m,n] (bias gradients); X bf16 [M, ldx]. */
 int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void* stream);
@@ -172,9 +187,11 @@ int avb_colsum_accum(const void* X, int64_t ldx, int M, int N, float* out, void*
 int avb_tokens_fwd(const void* pe, const float* cls, const float* pos_s, const float* pos_t, void* x, int B,
                    int Np, int S, int D, void* stream);
 /* dpe = dx[:,1:] (nullable); dcls += sum_b dx[:,0]; dpos_s[0] += sum_b dx[:,0];
- * dpos_s[1+s] += sum_{b,t} dx[b,1+t*S+s]; dpos_t[t] += sum_{b,s} dx[b,1+t*S+s]  (each nullable) */
-int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos_s, float* dpos_t, int B, int Np, int S,
-                   int D, void* stream);
+ * dpos_s[1+s] += sum_{b,t} dx[b,1+t*S+s]; dpos_t[t] += sum_{b,s} dx[b,1+t*S+s]  (each nullable).
+ * work: fp32 scratch [Np+1, D]; all sums run in a fixed order (no atomics), so the result is
+ * bit-reproducible.  dcls / dpos_s / dpos_t / work 16-byte aligned. */
+int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos_s, float* dpos_t, float* work, int B, int Np,
+                   int S, int D, void* stream);
 
 /* Tubelet patchify of normalised clips (the nn.Module path that takes [B,3,T,H,W] input; the training
  * step gets the same rows straight from K1's tubelet layout): x bf16 contiguous [B,3,T,H,W] ->

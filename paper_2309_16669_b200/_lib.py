@@ -36,11 +36,12 @@ EXPORTS: dict[str, tuple] = {
     "avb_rrc_normalize_tubelet": (_i32, [_vp, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                          _i32, _i32, _f32p, _f32p, _i32, _i32, _i32, _i32, _vp, _vp]),
     "avb_layernorm_fwd": (_i32, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, C.c_float, _vp]),
-    "avb_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _i32,
-                                 _vp]),
+    "avb_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32,
+                                 _i32, _vp]),
+    "avb_layernorm_bwd_workspace": (_i32, [_i32]),
     "avb_colsum_accum": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "avb_tokens_fwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
-    "avb_tokens_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    "avb_tokens_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
     "avb_patchify": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "avb_xent": (_i32, [_vp, _i64, _vp, _i32, _i32, C.c_float, _vp, _vp, _i64, _vp]),
     "avb_adamw": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, _i32,
@@ -60,6 +61,8 @@ EXPORTS: dict[str, tuple] = {
                             _i32, _vp]),
     "avb_attn_bwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
                             _i64, _i32, _i32, _i32, _i32, C.c_float, _i32, _vp]),
+    "avb_attn_bwd_deterministic": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                                          _vp, _i64, _i64, _i32, _i32, _i32, _i32, C.c_float, _i32, _vp]),
 }
 
 _lock = threading.Lock()

@@ -393,6 +393,8 @@ struct BwdArgs {
   long long* trace;       // debug: per-step clock64 events of CTA 0 (AVB_ATTN_TRACE), else null
   int dbg;                // trace-build experiment flags (AVB_ATTN_DBG): 1 skip the dQ drain, 2 skip the dS smem
                           // stores, 4 skip the dS-phase TMEM ld/st, 8 skip the exp-phase TMEM ld/st, 16 no exp2
+  int dq_det;             // 1 (deterministic mode): dQ_g of key tile kt is stored (not added) into fp32 slice kt of
+                          // dq_acc [nkt][B, N, H, 64]; the convert kernel sums the slices in key-tile order
   int dq_bf16;            // 1: dQ_g (scaled) reduce-added straight into the bf16 dq view; 0: into the fp32
                           // accumulator (+ a convert kernel)
 };
@@ -818,12 +820,19 @@ __global__ void __launch_bounds__(32 * kBwdWarps, 1)
         if (lane == 0) {
           const int q0 = (t.i0 + ii) * BT + quad * 32;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-            asm volatile(
-                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tmDQ)),
-                "r"(smem_u32(stage + hh * 4096)), "r"(t.h * HD + hh * 32), "r"(q0), "r"(t.b)
-                : "memory");
+          for (int hh = 0; hh < 2; ++hh) {
+            if (a.dq_det)   // slice kt of the per-key-tile partials (z = kt * B + b)
+              asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                               reinterpret_cast<uint64_t>(&tmDQ)),
+                           "r"(smem_u32(stage + hh * 4096)), "r"(t.h * HD + hh * 32), "r"(q0), "r"(t.kt * a.B + t.b)
+                           : "memory");
+            else
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                      reinterpret_cast<uint64_t>(&tmDQ)),
+                  "r"(smem_u32(stage + hh * 4096)), "r"(t.h * HD + hh * 32), "r"(q0), "r"(t.b)
+                  : "memory");
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           tc::mbar_arrive(&stage_free[pb]);   // the buffer may take dS^T_{g+2}
@@ -1049,7 +1058,7 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, int64_t
 }
 
 __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int64_t ld,
-                                       int64_t sb, int B, int H, int N, float scale) {
+                                       int64_t sb, int B, int H, int N, float scale, int nslices, int causal) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one thread per 8 elements
   const int64_t total = (int64_t)B * N * H * 8;
   if (gid >= total) return;
@@ -1059,8 +1068,17 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ dq_acc, __nv_bf
   const int64_t bn = item / H;
   const int n = bn % N;
   const int b = bn / N;
-  const float4* s = reinterpret_cast<const float4*>(dq_acc + item * HD + sub * 8);
-  const float4 x = s[0], y = s[1];
+  // slices summed in key-tile order (deterministic mode; nslices = 1 otherwise); a causal query row n
+  // only has contributions from key tiles kt <= n / 128 (the others were never written)
+  const int64_t slice = (int64_t)B * N * H * HD;
+  const int ns = causal ? min(nslices, n / BT + 1) : nslices;
+  float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = x;
+  for (int k = 0; k < ns; ++k) {
+    const float4* s = reinterpret_cast<const float4*>(dq_acc + k * slice + item * HD + sub * 8);
+    const float4 a0 = s[0], a1 = s[1];
+    x = make_float4(x.x + a0.x, x.y + a0.y, x.z + a0.z, x.w + a0.w);
+    y = make_float4(y.x + a1.x, y.y + a1.y, y.z + a1.z, y.w + a1.w);
+  }
   uint4 v;
   v.x = pack_bf16x2(x.x * scale, x.y * scale);
   v.y = pack_bf16x2(x.z * scale, x.w * scale);
@@ -1116,10 +1134,10 @@ extern "C" int avb_attn_fwd(const void* q, const void* k, const void* v, int64_t
   return avb::launch_status("avb_attn_fwd");
 }
 
-extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb, const void* o,
-                            const void* dout, int64_t ld_o, int64_t sb_o, const float* lse, float* delta,
-                            float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g, int B, int H,
-                            int N, int head_dim, float softmax_scale, int causal, void* stream) {
+static int attn_bwd_impl(const void* q, const void* k, const void* v, int64_t ld, int64_t sb, const void* o,
+                         const void* dout, int64_t ld_o, int64_t sb_o, const float* lse, float* delta, float* dq_acc,
+                         void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g, int B, int H, int N, int head_dim,
+                         float softmax_scale, int causal, int det, void* stream) {
   AVB_CHECK_ARG(head_dim == HD, "head_dim must be 64 (got %d)", head_dim);
   AVB_CHECK_ARG(B >= 0 && H >= 1 && N >= 0, "bad attention dims");
   if (B == 0 || N == 0) return AVB_OK;
@@ -1150,9 +1168,10 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   CUtensorMap mdq, mdk, mdv;
   if ((s = make_maps(&mdk, dk, B, H, N, ld_g, sb_g, 32))) return s;   // dK / dV TMA stores: 32-row boxes
   if ((s = make_maps(&mdv, dv, B, H, N, ld_g, sb_g, 32))) return s;
-  if (dq_acc) {
-    if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B, (uint64_t)H * HD,
-                                   (uint64_t)N * H * HD, 32, 32, 1, 128)))
+  const int nkt = (N + BT - 1) / BT;
+  if (dq_acc) {   // deterministic mode: nkt slices of [B, N, H, 64] (z = kt * B + b)
+    if ((s = avb::make_tmap_3d_f32(&mdq, dq_acc, (uint64_t)H * HD, (uint64_t)N, (uint64_t)B * (det ? nkt : 1),
+                                   (uint64_t)H * HD, (uint64_t)N * H * HD, 32, 32, 1, 128)))
       return s;
   } else if ((s = make_maps(&mdq, dq, B, H, N, ld_g, sb_g, 32))) {   // bf16 dq rows, 32-row boxes
     return s;
@@ -1173,6 +1192,7 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   a.nkt = (N + BT - 1) / BT;
   a.items = B * H * a.nkt;
   a.dq_bf16 = dq_acc ? 0 : 1;
+  a.dq_det = det;
   a.trace = nullptr;
   a.dbg = 0;
 #ifdef AVB_ATTN_TRACE_HOOKS   // trace build only (scripts/trace_attn_bwd.py)
@@ -1191,6 +1211,24 @@ extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t
   if (!dq_acc) return AVB_OK;   // dQ was reduce-added in bf16 directly
   const int64_t threads = (int64_t)B * N * H * 8;
   attn_dq_convert_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-      dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N, softmax_scale);
+      dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), ld_g, sb_g, B, H, N, softmax_scale, det ? nkt : 1, causal);
   return avb::launch_status("attn_dq_convert");
+}
+
+extern "C" int avb_attn_bwd(const void* q, const void* k, const void* v, int64_t ld, int64_t sb, const void* o,
+                            const void* dout, int64_t ld_o, int64_t sb_o, const float* lse, float* delta,
+                            float* dq_acc, void* dq, void* dk, void* dv, int64_t ld_g, int64_t sb_g, int B, int H,
+                            int N, int head_dim, float softmax_scale, int causal, void* stream) {
+  return attn_bwd_impl(q, k, v, ld, sb, o, dout, ld_o, sb_o, lse, delta, dq_acc, dq, dk, dv, ld_g, sb_g, B, H, N,
+                       head_dim, softmax_scale, causal, 0, stream);
+}
+
+extern "C" int avb_attn_bwd_deterministic(const void* q, const void* k, const void* v, int64_t ld, int64_t sb,
+                                          const void* o, const void* dout, int64_t ld_o, int64_t sb_o, const float* lse,
+                                          float* delta, float* dq_part, void* dq, void* dk, void* dv, int64_t ld_g,
+                                          int64_t sb_g, int B, int H, int N, int head_dim, float softmax_scale,
+                                          int causal, void* stream) {
+  AVB_CHECK_ARG(dq_part, "deterministic attention backward needs the fp32 per-key-tile dQ workspace");
+  return attn_bwd_impl(q, k, v, ld, sb, o, dout, ld_o, sb_o, lse, delta, dq_part, dq, dk, dv, ld_g, sb_g, B, H, N,
+                       head_dim, softmax_scale, causal, 1, stream);
 }

@@ -58,7 +58,8 @@ constexpr int kLnBwdWarps = 8, kLnBwdStages = 4;   // 1 block / SM: 8 warps x 3 
 template <int NC>
 constexpr int ln_fwd_smem() { return kLnFwdWarps * kLnFwdStages * NC * 512; }
 template <int NC>
-constexpr int ln_bwd_smem() { return kLnBwdWarps * kLnBwdStages * (3 * NC * 512 + 256) + 3 * NC * 256 * 4; }
+constexpr int ln_bwd_smem() { return kLnBwdWarps * kLnBwdStages * (3 * NC * 512 + 256); }
+static_assert(kLnBwdWarps * kLnBwdStages * (3 * 512 + 256) >= kLnBwdWarps * 3 * 256 * 4, "per-warp partials fit the ring");
 
 template <int NC>
 __global__ void __launch_bounds__(32 * kLnFwdWarps) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
@@ -143,16 +144,12 @@ __global__ void __launch_bounds__(32 * kLnBwdWarps, 1) ln_bwd_kernel(const __nv_
                                                      const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, __nv_bfloat16* dx, int64_t lddx,
-                                                     float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                     float* __restrict__ dsum, int M, int D, int accumulate) {
+                                                     float* __restrict__ part, int M, int D, int accumulate) {
   constexpr int S = kLnBwdStages;
   constexpr int SLOT = 3 * NC * 32 + 16;   // uint4 per (warp, stage): x, dy, dx pieces + mean/rstd per lane
   extern __shared__ uint4 ln_ring[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint4* ring = ln_ring + warp * S * SLOT;
-  float* red = reinterpret_cast<float*>(ln_ring + kLnBwdWarps * S * SLOT);   // [3][D]: dgamma, dbeta, dx column sums
-  for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) red[i] = 0.f;
-  __syncthreads();
   bool ok[NC];
   float gm[NC][8], dg[NC][8], db[NC][8], cs[NC][8];
 #pragma unroll
@@ -232,25 +229,46 @@ __global__ void __launch_bounds__(32 * kLnBwdWarps, 1) ln_bwd_kernel(const __nv_
       }
     }
   }
+  // fixed-order reductions (bit-reproducible): each warp's column partials -> smem (over the drained
+  // ring), the block sums them warp by warp -> part[block][3][D]; ln_bwd_reduce sums the blocks in order
   cp_async_wait<0>();
+  __syncthreads();
+  float* wpart = reinterpret_cast<float*>(ln_ring);   // [warp][3][D]
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c = k * 256 + lane * 8;
     if (c < D) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        atomicAdd(&red[c + e], dg[k][e]);
-        atomicAdd(&red[D + c + e], db[k][e]);
-        if (SUM) atomicAdd(&red[2 * D + c + e], cs[k][e]);
+        wpart[(warp * 3 + 0) * D + c + e] = dg[k][e];
+        wpart[(warp * 3 + 1) * D + c + e] = db[k][e];
+        wpart[(warp * 3 + 2) * D + c + e] = SUM ? cs[k][e] : 0.f;
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
-    if (dgamma) atomicAdd(dgamma + i, red[i]);
-    if (dbeta) atomicAdd(dbeta + i, red[D + i]);
-    if (SUM) atomicAdd(dsum + i, red[2 * D + i]);
+  for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) {
+    const int j = i / D, col = i - j * D;
+    float acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < kLnBwdWarps; ++w) acc += wpart[(w * 3 + j) * D + col];
+    part[(int64_t)blockIdx.x * 3 * D + i] = acc;
   }
+}
+
+// One warp per (column, quantity): lane l sums block partials l, l+32, ... in order, then a fixed
+// xor-shuffle tree -> deterministic.  part is [nblocks][3][D]; dst = dgamma / dbeta / dsum.
+__global__ void ln_bwd_reduce_kernel(const float* __restrict__ part, int nblocks, int D, float* __restrict__ dgamma,
+                                     float* __restrict__ dbeta, float* __restrict__ dsum) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= 3 * D) return;
+  const int j = w / D, i = w - j * D;
+  float* dst = j == 0 ? dgamma : (j == 1 ? dbeta : dsum);
+  if (!dst) return;
+  float acc = 0.f;
+  for (int k = lane; k < nblocks; k += 32) acc += part[((int64_t)k * 3 + j) * D + i];
+  acc = warp_sum(acc);
+  if (lane == 0) dst[i] += acc;
 }
 
 template <typename F>
@@ -287,22 +305,29 @@ extern "C" int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma,
 
 extern "C" int avb_layernorm_bwd(const void* dy, int64_t lddy, const void* x, int64_t ldx, const float* gamma,
                                  const float* mean, const float* rstd, void* dx, int64_t lddx, float* dgamma,
-                                 float* dbeta, float* dx_colsum, int M, int D, int accumulate, void* stream) {
+                                 float* dbeta, float* dx_colsum, float* work, int M, int D, int accumulate,
+                                 void* stream) {
   AVB_CHECK_ARG(M >= 0 && D >= 8 && D <= 1024 && D % 8 == 0, "LayerNorm needs D % 8 == 0, D <= 1024");
   if (M == 0) return AVB_OK;
-  AVB_CHECK_ARG(dy && x && gamma && mean && rstd && dx, "null pointer");
+  AVB_CHECK_ARG(dy && x && gamma && mean && rstd && dx && work, "null pointer");
   AVB_CHECK_ARG(lddy % 8 == 0 && ldx % 8 == 0 && lddx % 8 == 0, "row strides must be multiples of 8");
   const int blocks = (int)std::min<int64_t>((M + kLnBwdWarps - 1) / kLnBwdWarps, (int64_t)avb::sm_count());
   return dispatch_nc(D, [&](auto nc) {
     constexpr int NCv = decltype(nc)::value;
     constexpr int smem = ln_bwd_smem<NCv>();
-    auto launch = [&](auto kern, float* dsum) {
+    auto launch = [&](auto kern) {
       if (int e = avb::ensure_kernel_attrs(reinterpret_cast<const void*>(kern), smem, "ln_bwd smem attr")) return e;
       kern<<<blocks, 32 * kLnBwdWarps, smem, avb::as_stream(stream)>>>(
           reinterpret_cast<const __nv_bfloat16*>(dy), lddy, reinterpret_cast<const __nv_bfloat16*>(x), ldx, gamma,
-          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, dgamma, dbeta, dsum, M, D, accumulate);
-      return avb::launch_status("avb_layernorm_bwd");
+          mean, rstd, reinterpret_cast<__nv_bfloat16*>(dx), lddx, work, M, D, accumulate);
+      if (int e = avb::launch_status("avb_layernorm_bwd")) return e;
+      if (!dgamma && !dbeta && !dx_colsum) return AVB_OK;
+      ln_bwd_reduce_kernel<<<(3 * D * 32 + 255) / 256, 256, 0, avb::as_stream(stream)>>>(work, blocks, D, dgamma,
+                                                                                          dbeta, dx_colsum);
+      return avb::launch_status("avb_layernorm_bwd (reduce)");
     };
-    return dx_colsum ? launch(ln_bwd_kernel<NCv, true>, dx_colsum) : launch(ln_bwd_kernel<NCv, false>, nullptr);
+    return dx_colsum ? launch(ln_bwd_kernel<NCv, true>) : launch(ln_bwd_kernel<NCv, false>);
   });
 }
+
+extern "C" int avb_layernorm_bwd_workspace(int D) { return avb::sm_count() * 3 * D; }

@@ -101,9 +101,10 @@ __global__ void tokens_fwd_kernel(const __nv_bfloat16* __restrict__ pe, const fl
 // One thread per (token n, 8 columns): acc = sum_b dx[b, n]; dpe = dx[:, 1:];
 // dcls, dpos_s[0] += acc(n = 0); dpos_s[1+s] += acc; dpos_t[t] += acc (fp32 atomics: T' resp. S
 // contributions per element, so these two small gradients are not bit-reproducible run to run).
+// Token-embedding backward in two deterministic passes (no float atomics: bit-reproducible).
+// Pass 1, one thread per (token n, 8 columns): tok[n] = sum_b dx[b, n] in clip order (and dpe = dx[:, 1:]).
 __global__ void tokens_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_bfloat16* __restrict__ dpe,
-                                  float* __restrict__ dcls, float* __restrict__ dpos_s, float* __restrict__ dpos_t,
-                                  int B, int Np, int S, int D) {
+                                  float* __restrict__ tok, int B, int Np, int D) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int per_row = D / 8;
   const int64_t total = (int64_t)(Np + 1) * per_row;
@@ -113,25 +114,57 @@ __global__ void tokens_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_bfl
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = 0; b < B; ++b) {
     float f[8];
-    const int64_t tok = (int64_t)b * (Np + 1) + n;
-    ld8f(dx + tok * D + c, f);
+    const int64_t t = (int64_t)b * (Np + 1) + n;
+    ld8f(dx + t * D + c, f);
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] += f[e];
     if (n > 0 && dpe) st8f(dpe + ((int64_t)b * Np + n - 1) * D + c, f);
   }
-  if (n == 0) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      if (dcls) dcls[c + e] += acc[e];
-      if (dpos_s) dpos_s[c + e] += acc[e];
-    }
-    return;
+  float4* o = reinterpret_cast<float4*>(tok + (int64_t)n * D + c);
+  o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+// Pass 2, one warp per (table row, 4 columns), rows = [cls/pos_s[0]] + pos_s[1..S] + pos_t[0..T'): lane l
+// sums the row's tokens l, l+32, ... in order, then a fixed xor-shuffle tree (deterministic).
+__global__ void tokens_bwd_tables_kernel(const float* __restrict__ tok, float* __restrict__ dcls,
+                                         float* __restrict__ dpos_s, float* __restrict__ dpos_t, int Np, int S, int D) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int per_row = D / 4;
+  const int Tn = Np / S;
+  if (w >= (int64_t)(1 + S + Tn) * per_row) return;
+  const int c = (int)(w % per_row) * 4;
+  const int r = (int)(w / per_row);
+  // the row's tokens: r = 0 -> {0}; r in [1, S] -> {1 + t*S + (r-1)}, t < Tn; else {1 + t*S + sp}, sp < S
+  const int cnt = r == 0 ? 1 : (r <= S ? Tn : S);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int m = lane; m < cnt; m += 32) {
+    const int n = r == 0 ? 0 : (r <= S ? 1 + m * S + (r - 1) : 1 + (r - 1 - S) * S + m);
+    const float4 v = *reinterpret_cast<const float4*>(tok + (int64_t)n * D + c);
+    acc = make_float4(acc.x + v.x, acc.y + v.y, acc.z + v.z, acc.w + v.w);
   }
-  const int t = (n - 1) / S, sp = (n - 1) - t * S;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    if (dpos_s) atomicAdd(dpos_s + (int64_t)(1 + sp) * D + c + e, acc[e]);
-    if (dpos_t) atomicAdd(dpos_t + (int64_t)t * D + c + e, acc[e]);
+  for (int o = 16; o; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  if (lane != 0) return;
+  auto upd = [&](float* dst) {
+    if (!dst) return;
+    float4* d = reinterpret_cast<float4*>(dst + c);
+    const float4 o = *d;
+    *d = make_float4(o.x + acc.x, o.y + acc.y, o.z + acc.z, o.w + acc.w);
+  };
+  if (r == 0) {   // the cls token: its own parameter and slot 0 of the spatial table
+    upd(dcls);
+    upd(dpos_s);
+  } else if (r <= S) {
+    upd(dpos_s ? dpos_s + (int64_t)r * D : nullptr);
+  } else {
+    upd(dpos_t ? dpos_t + (int64_t)(r - 1 - S) * D : nullptr);
   }
 }
 
@@ -386,17 +419,24 @@ extern "C" int avb_tokens_fwd(const void* pe, const float* cls, const float* pos
   return avb::launch_status("avb_tokens_fwd");
 }
 
-extern "C" int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos_s, float* dpos_t, int B, int Np,
-                              int S, int D, void* stream) {
+extern "C" int avb_tokens_bwd(const void* dx, void* dpe, float* dcls, float* dpos_s, float* dpos_t, float* work,
+                              int B, int Np, int S, int D, void* stream) {
   AVB_CHECK_ARG(B >= 0 && Np >= 0 && D % 8 == 0, "tokens: D must be a multiple of 8");
   AVB_CHECK_ARG(S >= 1 && Np % S == 0, "tokens: Np=%d must be a multiple of the spatial count S=%d", Np, S);
   if (B == 0) return AVB_OK;
-  AVB_CHECK_ARG(dx, "null pointer");
+  AVB_CHECK_ARG(dx && work, "null pointer");
+  AVB_CHECK_ARG((reinterpret_cast<uintptr_t>(work) & 15) == 0 && (!dcls || (reinterpret_cast<uintptr_t>(dcls) & 15) == 0) &&
+                    (!dpos_s || (reinterpret_cast<uintptr_t>(dpos_s) & 15) == 0) &&
+                    (!dpos_t || (reinterpret_cast<uintptr_t>(dpos_t) & 15) == 0),
+                "tokens_bwd: work / dcls / dpos_s / dpos_t must be 16-byte aligned");
   const int64_t total = (int64_t)(Np + 1) * (D / 8);
   tokens_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, avb::as_stream(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(dx), reinterpret_cast<__nv_bfloat16*>(dpe), dcls, dpos_s, dpos_t, B, Np,
-      S, D);
-  return avb::launch_status("avb_tokens_bwd");
+      reinterpret_cast<const __nv_bfloat16*>(dx), reinterpret_cast<__nv_bfloat16*>(dpe), work, B, Np, D);
+  if (int e = avb::launch_status("avb_tokens_bwd")) return e;
+  const int64_t total2 = (int64_t)(1 + S + Np / S) * (D / 4) * 32;   // one warp per (row, 4 columns)
+  tokens_bwd_tables_kernel<<<(unsigned)((total2 + 255) / 256), 256, 0, avb::as_stream(stream)>>>(work, dcls, dpos_s,
+                                                                                               dpos_t, Np, S, D);
+  return avb::launch_status("avb_tokens_bwd (tables)");
 }
 
 extern "C" int avb_patchify(const void* x, int B, int T, int H, int W, int tt, int th, int tw, void* dst,

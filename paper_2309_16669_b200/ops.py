@@ -127,12 +127,30 @@ def attn_fwd(q, k, v, H: int, *, scale: float | None = None, causal: bool = Fals
     return out, lse
 
 
+_DETERMINISTIC = False
+
+
+def use_deterministic_algorithms(mode: bool = True) -> None:
+    """Bit-reproducible training gradients (for debugging), like torch.use_deterministic_algorithms:
+    the attention backward stores each key tile's dQ into its own fp32 slice and sums the slices in order,
+    and the wgrad GEMMs run without split-K (one fp32 add per gradient element).  LayerNorm's column
+    reductions and the token-table gradients are fixed-order in every mode."""
+    global _DETERMINISTIC
+    _DETERMINISTIC = bool(mode)
+
+
+def are_deterministic_algorithms_enabled() -> bool:
+    return _DETERMINISTIC
+
+
 def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causal: bool = False,
-             dq=None, dk=None, dv=None, fp32_dq: bool = False):
+             dq=None, dk=None, dv=None, fp32_dq: bool = False, deterministic: bool | None = None):
     """dQ, dK, dV of blockwise attention (dq/dk/dv may be slices of one packed [B,N,3*H*64] buffer).
 
     fp32_dq=False (default): every 128-key tile's dQ contribution is reduce-added in bf16 straight into
-    dq (no fp32 accumulator, no convert pass); True: fp32 accumulation + one convert kernel."""
+    dq (no fp32 accumulator, no convert pass); True: fp32 accumulation + one convert kernel.
+    deterministic=True: every key tile stores its dQ contribution into its own fp32 slice and one pass
+    sums them in key-tile order (bit-reproducible; ceil(N/128) x the fp32 dQ size of workspace)."""
     B, N, ld, sb = _bnhd(q, "q", H)
     for t, nm in ((k, "k"), (v, "v")):
         if _bnhd(t, nm, H) != (B, N, ld, sb):
@@ -157,12 +175,17 @@ def attn_bwd(q, k, v, o, dout, lse, H: int, *, scale: float | None = None, causa
         raise InputError("dq/dk/dv must match q's [B, N]")
     _, _, ld_g, sb_g = gq
     delta = torch.empty((B * H * npad(N), 8), dtype=torch.float32, device=q.device)   # 32 B per query row
-    dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device) if fp32_dq else None
+    if deterministic is None:
+        deterministic = _DETERMINISTIC
+    if deterministic:
+        dq_acc = torch.empty((npad(N) // 128, B, N, H, 64), dtype=torch.float32, device=q.device)
+    else:
+        dq_acc = torch.empty((B, N, H, 64), dtype=torch.float32, device=q.device) if fp32_dq else None
     scale = 64 ** -0.5 if scale is None else float(scale)
-    st = _lib.load().avb_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(),
-                                  ld_o, sb_o, lse.data_ptr(), delta.data_ptr(), _ptr(dq_acc), dq.data_ptr(),
-                                  dk.data_ptr(), dv.data_ptr(), ld_g, sb_g, B, H, N, 64, scale, int(causal),
-                                  _lib.stream_ptr())
+    fn = _lib.load().avb_attn_bwd_deterministic if deterministic else _lib.load().avb_attn_bwd
+    st = fn(q.data_ptr(), k.data_ptr(), v.data_ptr(), ld, sb, o.data_ptr(), dout.data_ptr(), ld_o, sb_o,
+            lse.data_ptr(), delta.data_ptr(), _ptr(dq_acc), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ld_g, sb_g,
+            B, H, N, 64, scale, int(causal), _lib.stream_ptr())
     _lib.check(st, "attn_bwd")
     return dq, dk, dv
 
@@ -181,11 +204,14 @@ def layernorm_fwd(x, gamma, beta, eps=1e-5, out=None, mean=None, rstd=None):
 
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma=None, dbeta=None, accumulate=False, dx_colsum=None):
+    """dx (=|+=) LN'(dy); dgamma/dbeta/dx_colsum += fixed-order column reductions (bit-reproducible)."""
     M, D = x.shape
-    st = _lib.load().avb_layernorm_bwd(dy.data_ptr(), _rowmajor(dy, "dy"), x.data_ptr(), _rowmajor(x, "x"),
-                                       gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
-                                       _rowmajor(dx, "dx"), _ptr(dgamma), _ptr(dbeta), _ptr(dx_colsum), M, D,
-                                       int(accumulate), _lib.stream_ptr())
+    lib = _lib.load()
+    work = torch.empty(lib.avb_layernorm_bwd_workspace(D), dtype=torch.float32, device=x.device)
+    st = lib.avb_layernorm_bwd(dy.data_ptr(), _rowmajor(dy, "dy"), x.data_ptr(), _rowmajor(x, "x"),
+                               gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+                               _rowmajor(dx, "dx"), _ptr(dgamma), _ptr(dbeta), _ptr(dx_colsum), work.data_ptr(), M, D,
+                               int(accumulate), _lib.stream_ptr())
     _lib.check(st, "layernorm_bwd")
     return dx
 
@@ -209,9 +235,11 @@ def tokens_fwd(pe, cls, pos_s, pos_t, B, Np, out):
 
 
 def tokens_bwd(dx, dpe, dcls, dpos_s, dpos_t, B, Np, S):
+    """Token-embedding backward; fixed-order sums (bit-reproducible), fp32 [Np+1, D] scratch."""
     D = dx.shape[-1]
-    _lib.check(_lib.load().avb_tokens_bwd(dx.data_ptr(), _ptr(dpe), _ptr(dcls), _ptr(dpos_s), _ptr(dpos_t), B, Np, S,
-                                          D, _lib.stream_ptr()), "tokens_bwd")
+    work = torch.empty((Np + 1, D), dtype=torch.float32, device=dx.device)
+    _lib.check(_lib.load().avb_tokens_bwd(dx.data_ptr(), _ptr(dpe), _ptr(dcls), _ptr(dpos_s), _ptr(dpos_t),
+                                          work.data_ptr(), B, Np, S, D, _lib.stream_ptr()), "tokens_bwd")
 
 
 def patchify(x, tubelet, out=None):

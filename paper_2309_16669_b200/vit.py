@@ -187,6 +187,8 @@ def wgrad_split(m_out: int, n_out: int, k_tokens: int | None = None, sms: int = 
     The fused bias-gradient mode runs a single-buffered accumulator, so every extra work item
     per CTA pays its fp32 reduce epilogue (~35 k-block equivalents) un-overlapped.
     """
+    if ops.are_deterministic_algorithms_enabled():
+        return 1   # one fp32 add per gradient element: bit-reproducible
     if n_out > 128 and m_out > 128:   # CTA-pair GEMM: 256 x 256 tiles, one worker per SM pair
         tiles, sms = ((m_out + 255) // 256) * ((n_out + 255) // 256), sms // 2
     else:
