@@ -7,7 +7,8 @@ against public semantics it must agree with:
     tubelet embedding, PAPER.md:258-259);
   * the separable position embedding == an explicit per-token loop of PE_t[t] + PE_s[1+s] (cls: PE_s[0]);
   * clip_loss == open_clip's ClipLoss formula (scaled normalised logits, symmetric CE, mean);
-  * one pre-LN block == torch.nn.TransformerEncoderLayer(norm_first=True) with QuickGELU.
+  * one pre-LN block == torch.nn.TransformerEncoderLayer(norm_first=True) with QuickGELU;
+  * a 2-layer stack == transformers' CLIPEncoder (the CLIP ViT block AVION starts from).
 CPU only, fp64 where the comparison is exact.
 """
 
@@ -87,3 +88,41 @@ def test_block_matches_torch_encoder_layer():
         got = VO.blocks(P, x.reshape(B * N, D), B, N, D, H, 1, "enc").view(B, N, D)
     assert (got - ref).abs().max().item() < 1e-10
     assert math.isfinite(got.sum().item())
+
+
+def test_blocks_match_transformers_clip_encoder():
+    """A 2-layer stack == transformers' CLIPEncoder (pre-LN, QuickGELU): the CLIP ViT-B/16 block that
+    AVION initialises its video encoder from, an independent public implementation."""
+    from transformers.models.clip.configuration_clip import CLIPVisionConfig
+    from transformers.models.clip.modeling_clip import CLIPEncoder
+
+    torch.manual_seed(5)
+    D, H, L, B, N = 128, 2, 2, 2, 13   # head_dim 64 (the kernels' and the oracle's)
+    cfg = CLIPVisionConfig(hidden_size=D, num_attention_heads=H, intermediate_size=4 * D, num_hidden_layers=L,
+                           hidden_act="quick_gelu", attention_dropout=0.0)
+    cfg._attn_implementation = "eager"
+    enc = CLIPEncoder(cfg).to(torch.float64).eval()
+    P = {}
+    for l, layer in enumerate(enc.layers):
+        g = f"enc.blk{l}"
+        a = layer.self_attn
+        for t in (layer.layer_norm1, layer.layer_norm2, a.q_proj, a.k_proj, a.v_proj, a.out_proj, layer.mlp.fc1,
+                  layer.mlp.fc2):
+            torch.nn.init.normal_(t.weight, std=0.2 if isinstance(t, torch.nn.LayerNorm) else 0.05)
+            torch.nn.init.normal_(t.bias, std=0.05)
+            if isinstance(t, torch.nn.LayerNorm):
+                t.weight.data += 1.0
+        P.update({f"{g}.ln1.g": layer.layer_norm1.weight, f"{g}.ln1.b": layer.layer_norm1.bias,
+                  f"{g}.qkv.w": torch.cat([a.q_proj.weight, a.k_proj.weight, a.v_proj.weight]),
+                  f"{g}.qkv.b": torch.cat([a.q_proj.bias, a.k_proj.bias, a.v_proj.bias]),
+                  f"{g}.proj.w": a.out_proj.weight, f"{g}.proj.b": a.out_proj.bias,
+                  f"{g}.ln2.g": layer.layer_norm2.weight, f"{g}.ln2.b": layer.layer_norm2.bias,
+                  f"{g}.fc1.w": layer.mlp.fc1.weight, f"{g}.fc1.b": layer.mlp.fc1.bias,
+                  f"{g}.fc2.w": layer.mlp.fc2.weight, f"{g}.fc2.b": layer.mlp.fc2.bias})
+    x = torch.randn(B, N, D, dtype=torch.float64)
+    with torch.no_grad():
+        out = enc(inputs_embeds=x)
+        ref = out.last_hidden_state if hasattr(out, "last_hidden_state") else out[0]
+        got = VO.blocks(P, x.reshape(B * N, D), B, N, D, H, L, "enc").view(B, N, D)
+    # transformers' eager attention takes the softmax in fp32 even in an fp64 model: ~1e-8 differences
+    assert (got - ref).abs().max().item() < 1e-6
