@@ -505,7 +505,9 @@ struct K1v4Params {
   int fpc;         // frames per CTA
   int tpf;         // column pairs (compute lanes) per frame = ceil(Wt / 2)
   int ncomp;       // compute threads (multiple of 32); the producer warp follows
-  int slot_bytes;  // bytes per staged row (multiple of 16)
+  int slot_bytes;  // bytes per staged row (multiple of 16); planar: 3 channel sub-slots of cslot bytes
+  int cslot;       // planar input ([B,T,3,H,W] rows): bytes per channel sub-slot (multiple of 16)
+  int64_t s_c;     // planar input: channel-plane stride in bytes (a multiple of 16)
   int64_t total_bytes;
   int nband;       // output-row bands per frame group (grid.x = frame groups * nband): finer work units
                    // balance the waves (each band re-reads the <= 3 source rows its neighbour also needs)
@@ -608,6 +610,20 @@ struct K1HTap {
   }
 };
 
+// planar rows: tap K of a channel is byte K of that channel's window
+template <int NT, int K = 0>
+struct K1HTapPL {
+  template <int NW>
+  __device__ __forceinline__ static void run(const uint32_t (&s0)[NW], const uint32_t (&s1)[NW], const float2 (&wp)[NT],
+                                             float2& h) {
+    if constexpr (K < NT) {
+      const float2 f = fadd2(make_float2(k1_magic<K>(s0), k1_magic<K>(s1)), make_float2(-8388608.f, -8388608.f));
+      h = ffma2(wp[K], f, h);
+      K1HTapPL<NT, K + 1>::run(s0, s1, wp, h);
+    }
+  }
+};
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -615,10 +631,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-template <int NT, int NOPEN>
+template <int NT, int NOPEN, bool PL = false>
 __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int NW = (3 * NT + 3) / 4;
+  constexpr int NW = PL ? (NT + 3) / 4 : (3 * NT + 3) / 4;   // window words per column (one channel if planar)
+  constexpr int NCH = PL ? 3 : 1;                             // bulk copies per (row, frame)
   static_assert(NOPEN <= 3, "emission count lives in rowtab.w");
   const int tid = threadIdx.x;
   const int64_t b = blockIdx.y;
@@ -694,13 +711,13 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
     // ================= producer: one lane, one bulk copy per (source row, frame)
     if (tid != p.ncomp) return;
     const uint8_t* src_end = p.src + p.total_bytes;
-    const uint8_t* row0 = p.src + b * p.s_clip + (int64_t)t0 * p.s_t + (int64_t)y0 * p.s_h + (int64_t)x0 * 3;
+    const uint8_t* row0 = p.src + b * p.s_clip + (int64_t)t0 * p.s_t + (int64_t)y0 * p.s_h + (int64_t)x0 * (PL ? 1 : 3);
     const int nf = min(p.fpc, p.T - t0);
-    const uint32_t span = 3u * cw;
-    // first row whose rounded-up copy (of the last frame) could reach past the tensor end
+    const uint32_t span = PL ? (uint32_t)cw : 3u * cw;
+    // first row whose rounded-up copy (of the last frame / channel) could reach past the tensor end
     int tail_y = ye;
     {
-      const uint8_t* last = row0 + (int64_t)(nf - 1) * p.s_t;
+      const uint8_t* last = row0 + (int64_t)(nf - 1) * p.s_t + (PL ? 2 * p.s_c : 0);
       for (int y = ye - 1; y >= ys && last + (int64_t)y * p.s_h + span + 15 > src_end; --y) tail_y = y;
     }
     int s = 0;
@@ -712,22 +729,28 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
       if (y < tail_y) {
         uint32_t tx = 0;
         const uint8_t* a = a_row;
-        for (int f = 0; f < nf; ++f, a += p.s_t) tx += (((uint32_t)(uintptr_t)a & 15u) + span + 15u) & ~15u;
+        for (int f = 0; f < nf; ++f, a += p.s_t) tx += NCH * ((((uint32_t)(uintptr_t)a & 15u) + span + 15u) & ~15u);
         tc::mbar_arrive_expect_tx(&full[s], tx);
         a = a_row;
         for (int f = 0; f < nf; ++f, a += p.s_t) {
-          const uint32_t mis = (uint32_t)(uintptr_t)a & 15u;
-          bulk_g2s(dst + (size_t)f * p.slot_bytes, a - mis, (mis + span + 15u) & ~15u, &full[s]);
+          const uint32_t mis = (uint32_t)(uintptr_t)a & 15u;   // the same for every plane (s_c % 16 == 0)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+            bulk_g2s(dst + (size_t)f * p.slot_bytes + c * p.cslot, a + c * p.s_c - mis, (mis + span + 15u) & ~15u,
+                     &full[s]);
         }
       } else {  // bytes past the tensor end would fault: zero-filled 16-byte cp.async instead
         const uint8_t* a = a_row;
         for (int f = 0; f < nf; ++f, a += p.s_t) {
-          const uint8_t* al = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15));
-          const uint32_t nb = ((uint32_t)(a - al) + span + 15u) & ~15u;
-          for (uint32_t k = 0; k < nb; k += 16) {
-            const int64_t left = src_end - (al + k);
-            const int n = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
-            cp_async16(dst + (size_t)f * p.slot_bytes + k, n ? al + k : p.src, n);
+          for (int c = 0; c < NCH; ++c) {
+            const uint8_t* ac = a + c * p.s_c;
+            const uint8_t* al = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(ac) & ~uintptr_t(15));
+            const uint32_t nb = ((uint32_t)(ac - al) + span + 15u) & ~15u;
+            for (uint32_t k = 0; k < nb; k += 16) {
+              const int64_t left = src_end - (al + k);
+              const int n = left >= 16 ? 16 : (left > 0 ? (int)left : 0);
+              cp_async16(dst + (size_t)f * p.slot_bytes + c * p.cslot + k, n ? al + k : p.src, n);
+            }
           }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
@@ -756,8 +779,8 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
     else lo1 = lo0;
 #pragma unroll
     for (int k = 0; k < NT; ++k) wp[k] = make_float2(w0[k], w1[k]);
-    o0 = 3 * lo0;
-    o1 = 3 * lo1;
+    o0 = (PL ? 1 : 3) * lo0;
+    o1 = (PL ? 1 : 3) * lo1;
   }
   // output: element offset obase + rowoff(row) + c * cstride (32-bit within a clip, all layouts)
   int64_t obase;
@@ -792,7 +815,7 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
   uint8_t* dbase = reinterpret_cast<uint8_t*>(p.dst) + obase * (bf16 ? 2 : 4);
   // low bits of each row's global address (its misalignment inside the 16-byte-aligned copy)
   uint32_t alo = (uint32_t)reinterpret_cast<uintptr_t>(p.src + b * p.s_clip + (int64_t)(active ? t : t0) * p.s_t +
-                                                       (int64_t)(y0 + ys) * p.s_h + (int64_t)x0 * 3);
+                                                       (int64_t)(y0 + ys) * p.s_h + (int64_t)x0 * (PL ? 1 : 3));
   const uint32_t sh_lo = (uint32_t)p.s_h;
   const uint8_t* slot = ring + (size_t)(active ? f : 0) * p.slot_bytes;
   const uint8_t* slot0 = slot;
@@ -823,12 +846,22 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
     float2 h[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     {
       const int mis = (int)(alo & 15u);
-      uint32_t s0[NW], s1[NW];
-      k1_window<NW>(slot, mis + o0, s0);
-      k1_window<NW>(slot, mis + o1, s1);
-      K1HTap<NT, 0>::run(s0, s1, wp, h[0]);
-      K1HTap<NT, 1>::run(s0, s1, wp, h[1]);
-      K1HTap<NT, 2>::run(s0, s1, wp, h[2]);
+      if constexpr (PL) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          uint32_t s0[NW], s1[NW];
+          k1_window<NW>(slot + c * p.cslot, mis + o0, s0);
+          k1_window<NW>(slot + c * p.cslot, mis + o1, s1);
+          K1HTapPL<NT>::run(s0, s1, wp, h[c]);
+        }
+      } else {
+        uint32_t s0[NW], s1[NW];
+        k1_window<NW>(slot, mis + o0, s0);
+        k1_window<NW>(slot, mis + o1, s1);
+        K1HTap<NT, 0>::run(s0, s1, wp, h[0]);
+        K1HTap<NT, 1>::run(s0, s1, wp, h[1]);
+        K1HTap<NT, 2>::run(s0, s1, wp, h[2]);
+      }
     }
     tc::mbar_arrive(&empty[s]);
     alo += sh_lo;
@@ -1106,9 +1139,12 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
   // v4: streaming kernel for interleaved RGB downscales (every config-2 crop).  With host boxes
   //     the tap envelope is exact; with device-only boxes it is the worst case over every
   //     downscale crop and a complement launch of v2 covers any upscale clip.
+  //     Planar rows ([B,T,3,H,W], the reference Batch layout) take the same kernel with one bulk copy
+  //     per channel plane when the planes are 16-byte aligned and the boxes are on the host.
   bool v4_done = false, v4_partial = false;
-  if (p.fast && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && force == AVB_K1_PATH_AUTO && Ht <= H && Wt <= W && Wt <= 448 && T <= 65535 &&
-      B <= 65535 && 3LL * T * Ht * Wt < (1LL << 31)) {
+  const bool pl = !p.fast && s_w == 1 && s_c % 16 == 0 && s_c >= W && boxes_host != nullptr;
+  if ((p.fast || pl) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && force == AVB_K1_PATH_AUTO && Ht <= H &&
+      Wt <= W && Wt <= 448 && T <= 65535 && B <= 65535 && 3LL * T * Ht * Wt < (1LL << 31)) {
     int nt = 0, nopen = 0, cw_max = W;
     bool ok = true;
     if (boxes_host) {
@@ -1122,7 +1158,7 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
     if (ok && nt <= 8 && nopen <= 3) {
       const int NT = nt <= 4 ? 4 : nt <= 5 ? 5 : nt <= 6 ? 6 : 8;
       const int NOPEN = nopen <= 2 ? 2 : 3;
-      const int NW = (3 * NT + 3) / 4;
+      const int NW = pl ? (NT + 3) / 4 : (3 * NT + 3) / 4;
       K1v4Params q;
       q.src = src; q.s_clip = s_clip; q.s_t = s_t; q.s_h = s_h;
       q.T = T; q.H = H; q.W = W; q.Ht = Ht; q.Wt = Wt;
@@ -1135,9 +1171,12 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
       if (const char* e = getenv("AVB_K1_FPC")) q.fpc = std::max(1, std::min(T, atoi(e)));
 #endif
       q.ncomp = ((q.fpc * q.tpf + 31) / 32) * 32;
-      // a window read ends <= 15 (misalignment) + 3*cw + 4*(NW+1) bytes into the slot
-      q.slot_bytes = ((3 * cw_max + 4 * (NW + 1) + 15 + 15) / 16) * 16;
-      q.total_bytes = (B - 1) * s_clip + (int64_t)(T - 1) * s_t + (int64_t)(H - 1) * s_h + (int64_t)W * 3;
+      // a window read ends <= 15 (misalignment) + 3*cw (planar: cw per channel) + 4*(NW+1) bytes into the slot
+      q.s_c = s_c;
+      q.cslot = pl ? ((cw_max + 4 * (NW + 1) + 15 + 15) / 16) * 16 : 0;
+      q.slot_bytes = pl ? 3 * q.cslot : ((3 * cw_max + 4 * (NW + 1) + 15 + 15) / 16) * 16;
+      q.total_bytes = (B - 1) * s_clip + (int64_t)(T - 1) * s_t + (int64_t)(H - 1) * s_h +
+                      (pl ? 2 * s_c + (int64_t)W : (int64_t)W * 3);
       const size_t smem4 = sizeof(uint64_t) * 2 * V4_RS + sizeof(float4) * (size_t)H +
                            (size_t)V4_RS * q.fpc * q.slot_bytes;
       if (smem4 <= 200 * 1024) {
@@ -1159,6 +1198,13 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
         };
         auto by_nt = [&](auto nopen_c) {
           constexpr int NO = decltype(nopen_c)::value;
+          if (pl) {
+            if (NT == 4) launch(k1v4_kernel<4, NO, true>);
+            else if (NT == 5) launch(k1v4_kernel<5, NO, true>);
+            else if (NT == 6) launch(k1v4_kernel<6, NO, true>);
+            else launch(k1v4_kernel<8, NO, true>);
+            return;
+          }
           if (NT == 4) launch(k1v4_kernel<4, NO>);
           else if (NT == 5) launch(k1v4_kernel<5, NO>);
           else if (NT == 6) launch(k1v4_kernel<6, NO>);

@@ -45,5 +45,5 @@ for _ in range(5):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
-res["planar_generic"] = {"ms": ms, "GBs": TR.algorithmic_bytes(boxes, 16, (224, 224), 2) / ms / 1e6}
+res["planar"] = {"ms": ms, "GBs": TR.algorithmic_bytes(boxes, 16, (224, 224), 2) / ms / 1e6}
 print(json.dumps(res))

@@ -86,6 +86,47 @@ def test_generic_strides_reference_batch_layout():
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
 
 
+@pytest.mark.parametrize("layout", ["cthw", "tubelet"])
+def test_planar_v4_config2_boxes(layout):
+    """Reference-layout [B,T,3,H,W] clips with host boxes (downscales, 16-byte-aligned planes) stream
+    through v4 with one bulk copy per channel plane: same tolerances as the interleaved path, and the
+    same values as the forced generic kernel."""
+    B, Tn = 4, 4
+    fr = frames_u8(B, Tn, 320, 568, seed=21)
+    planar = fr.permute(0, 1, 4, 2, 3).contiguous().cuda()                   # [B,T,3,H,W]
+    boxes, flips = CFG2[:B, :4], CFG2[:B, 4]
+    ref = O.transform_batch(fr.numpy(), boxes, flips)                       # [B,3,T,224,224]
+    kw = dict(channels_last=False, crops_host=boxes, layout=layout)
+    if layout == "tubelet":   # [B, T/2, 14, 14, 3, 2, 16, 16] -> rows (t', py, px), features (c, dt, y, x)
+        kw["tubelet"] = (2, 16, 16)
+        ref = ref.reshape(B, 3, Tn // 2, 2, 14, 16, 14, 16).transpose(0, 2, 4, 6, 1, 3, 5, 7).reshape(-1, 1536)
+    o32 = T.transform(planar, boxes, flips, out_dtype=torch.float32, **kw).cpu().numpy()
+    o16 = T.transform(planar, boxes, flips, **kw).float().cpu().numpy()
+    assert np.abs(o32 - ref).max() <= 1e-3
+    assert np.all(np.abs(o16 - ref) <= bf16_ulp(ref) + 1e-6)
+    from paper_2309_16669_b200 import _lib
+    with _Path(_lib.AVB_K1_PATH_GENERIC):
+        g32 = T.transform(planar, boxes, flips, out_dtype=torch.float32, **kw).cpu().numpy()
+    assert np.abs(o32 - g32).max() <= 2e-5
+
+
+def test_planar_v4_tensor_end_and_unaligned_planes():
+    """Planar clip whose last channel row ends at the tensor end (zero-filled tail copies), and planes
+    that are not 16-byte aligned (generic fallback) -- both against the oracle."""
+    fr = frames_u8(1, 2, 230, 304, seed=22)                                 # plane 69920 B = 16 * 4370
+    b2 = np.asarray([[80, 6, 224, 224]], dtype=np.int32)
+    planar = fr.permute(0, 1, 4, 2, 3).contiguous()
+    out = T.transform(planar.cuda(), b2, [1], channels_last=False, crops_host=b2, out_dtype=torch.float32)
+    ref = O.transform_batch(fr.numpy(), b2, np.asarray([1]))
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+    fr2 = frames_u8(2, 2, 231, 301, seed=23)                                # plane 69531 B: unaligned
+    b3 = np.asarray([[0, 0, 300, 230], [40, 3, 250, 228]], dtype=np.int32)
+    pl2 = fr2.permute(0, 1, 4, 2, 3).contiguous()
+    out = T.transform(pl2.cuda(), b3, [0, 1], channels_last=False, crops_host=b3, out_dtype=torch.float32)
+    ref = O.transform_batch(fr2.numpy(), b3, np.asarray([0, 1]))
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3
+
+
 @pytest.mark.parametrize("H,W,Ht,Wt,box", [(40, 50, 97, 131, (3, 2, 41, 33)),   # upscale, odd Wt
                                            (33, 47, 33, 47, (0, 0, 47, 33)),    # identity, odd
                                            (9, 9, 1, 1, (0, 0, 9, 9)),          # to 1 pixel
