@@ -31,7 +31,7 @@ for layout, shape in (("cthw", (B, 3, 16, 224, 224)), ("tubelet", (B * 8 * 14 * 
     ms = e0.elapsed_time(e1) / 20
     algo = TR.algorithmic_bytes(boxes, 16, (224, 224), 2)
     res[layout] = {"ms": ms, "GBs": algo / ms / 1e6}
-# the reference loader's planar layout [B,T,3,H,W] with crops (the generic any-stride path)
+# the reference loader's planar layout [B,T,3,H,W] with crops (v4 with one bulk copy per channel plane)
 planar = fr.permute(0, 1, 4, 2, 3).contiguous()
 out = torch.empty((B, 3, 16, 224, 224), dtype=torch.bfloat16, device="cuda")
 kw = dict(layout="cthw", crops_host=boxes, validate=False, channels_last=False)
