@@ -52,8 +52,22 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr int kLnFwdWarps = 8, kLnFwdStages = 4;   // 4 blocks / SM: 32 warps x 3 rows in flight
-constexpr int kLnBwdWarps = 8, kLnBwdStages = 4;   // 1 block / SM: 8 warps x 3 rows (x, dy, dx) in flight
+#ifndef AVB_LN_FWD_STAGES
+#define AVB_LN_FWD_STAGES 4
+#endif
+#ifndef AVB_LN_FWD_BLOCKS
+#define AVB_LN_FWD_BLOCKS 4
+#endif
+// same-box sweep at config 4 (bwd warps x stages): 8x4 0.122 ms, 12x3 0.112, 16x2 0.112, 6x5 0.155;
+// fwd (stages x blocks/SM): 4x4 0.0647, 6x4 0.0651, 3x6 0.0669, 8x3 0.0725
+#ifndef AVB_LN_BWD_WARPS
+#define AVB_LN_BWD_WARPS 12
+#endif
+#ifndef AVB_LN_BWD_STAGES
+#define AVB_LN_BWD_STAGES 3
+#endif
+constexpr int kLnFwdWarps = 8, kLnFwdStages = AVB_LN_FWD_STAGES;   // AVB_LN_FWD_BLOCKS blocks / SM
+constexpr int kLnBwdWarps = AVB_LN_BWD_WARPS, kLnBwdStages = AVB_LN_BWD_STAGES;   // 1 block / SM
 
 template <int NC>
 constexpr int ln_fwd_smem() { return kLnFwdWarps * kLnFwdStages * NC * 512; }
@@ -290,7 +304,7 @@ extern "C" int avb_layernorm_fwd(const void* x, int64_t ldx, const float* gamma,
   if (M == 0) return AVB_OK;
   AVB_CHECK_ARG(x && gamma && beta && y && mean && rstd, "null pointer");
   AVB_CHECK_ARG(ldx % 8 == 0 && ldy % 8 == 0, "row strides must be multiples of 8");
-  const int blocks = (int)std::min<int64_t>((M + kLnFwdWarps - 1) / kLnFwdWarps, (int64_t)avb::sm_count() * 4);
+  const int blocks = (int)std::min<int64_t>((M + kLnFwdWarps - 1) / kLnFwdWarps, (int64_t)avb::sm_count() * AVB_LN_FWD_BLOCKS);
   return dispatch_nc(D, [&](auto nc) {
     constexpr int NCv = decltype(nc)::value;
     constexpr int smem = ln_fwd_smem<NCv>();
