@@ -146,6 +146,12 @@ def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("AVB_BENCH_SHARED_GPU") and world > 1:
+        # debug only (exercises the N-rank code path on a 1-GPU box): every rank on cuda:0 over gloo;
+        # the numbers are not a scaling measurement
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return rank, world, 0
     if world > torch.cuda.device_count():
         raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
     if world > 1:
