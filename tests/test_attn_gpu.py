@@ -81,6 +81,26 @@ def test_bwd(B, N, H, causal):
         assert rel(got.reshape(B, N, H, 64), ref) < 2e-2
 
 
+@pytest.mark.parametrize("scale", [3.0, 6.0])
+@pytest.mark.parametrize("causal", [False, True])
+def test_bwd_large_dynamic_range(scale, causal):
+    """Peaked softmax (scores up to ~+-150, lse/scale ~ 10^3): the statistics folded into K5's MMAs as
+    bf16 hi/lo pairs (-lse/scale, -delta) must keep the gradients at the 2e-2 bar."""
+    B, N, H = 2, 785, 2
+    qkv = packed(B, N, H, seed=31, scale=scale)
+    q, k, v = (qkv[:, :, i].contiguous() for i in range(3))
+    D = H * 64
+    o, lse = ops.attn_fwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), H, causal=causal)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    do = torch.randn(B, N, D, generator=g, device="cuda").to(torch.bfloat16)
+    dq, dk, dv = ops.attn_bwd(q.view(B, N, D), k.view(B, N, D), v.view(B, N, D), o, do, lse, H, causal=causal)
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    ro, _ = ref_attn(qf, kf, vf, 0.125, causal)
+    ro.backward(do.float().view(B, N, H, 64))
+    for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
+        assert rel(got.reshape(B, N, H, 64), ref) < 2e-2
+
+
 @pytest.mark.parametrize("causal", [False, True])
 def test_fwd_large_dynamic_range(causal):
     """Scores growing along the key axis force deferred rescales and the > 2^64 recompute path."""
