@@ -187,8 +187,20 @@ __device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// The epilogue's "accumulator drained" arrival on the pair leader's barrier.  Relaxed: what it
+// publishes is only that this warp's tcgen05.ld of the accumulator completed (tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync precede it); a .release.cluster arrive would also drain every
+// outstanding generic memory operation (MEMBAR.ALL.CTA + MEMBAR.ALL.GPU + ERRBAR in SASS), which
+// ncu showed as the epilogue warps' top stall (11 % of samples) in the heavy-epilogue GEMMs.
+#ifndef AVB_GEMM_RELAXED_TEMPTY
+#define AVB_GEMM_RELAXED_TEMPTY 1
+#endif
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+#if AVB_GEMM_RELAXED_TEMPTY
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
 }
 // TMA 2D load into this CTA's smem, completion (tx bytes) signalled on an mbarrier of the pair leader
 __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1) {
