@@ -246,7 +246,7 @@ __device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap*
     q.y = pack_bf16x2(v[u * 8 + 2], v[u * 8 + 3]);
     q.z = pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]);
     q.w = pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]);
-    *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ sw) << 4)) = q;
+    st_shared_v4(smem_u32(stg) + lane * 64 + ((u ^ sw) << 4), q);
   }
   tc::fence_proxy_async();
   __syncwarp();
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int sw = (lane >> 1) & 3;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const uint4 q = *reinterpret_cast<const uint4*>(src + ((u ^ sw) << 4));
+            const uint4 q = ld_shared_v4(smem_u32(src) + ((u ^ sw) << 4));
             const __nv_bfloat162* hq = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
