@@ -259,6 +259,44 @@ __device__ __forceinline__ void tma_store_chunk(uint8_t* stg, const CUtensorMap*
   }
 }
 
+// Both outputs of a BIAS_GELU chunk (pre-activation and activation) staged together: one
+// proxy fence and one bulk-group for the two TMA stores.
+template <int PENDING>
+__device__ __forceinline__ void tma_store_chunk2(uint8_t* stg0, const CUtensorMap* map0, const float (&v0)[32],
+                                                 uint8_t* stg1, const CUtensorMap* map1, const float (&v1)[32],
+                                                 int lane, int col, int row0) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(PENDING) : "memory");
+  __syncwarp();
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint4 q0, q1;
+    q0.x = pack_bf16x2(v0[u * 8 + 0], v0[u * 8 + 1]);
+    q0.y = pack_bf16x2(v0[u * 8 + 2], v0[u * 8 + 3]);
+    q0.z = pack_bf16x2(v0[u * 8 + 4], v0[u * 8 + 5]);
+    q0.w = pack_bf16x2(v0[u * 8 + 6], v0[u * 8 + 7]);
+    q1.x = pack_bf16x2(v1[u * 8 + 0], v1[u * 8 + 1]);
+    q1.y = pack_bf16x2(v1[u * 8 + 2], v1[u * 8 + 3]);
+    q1.z = pack_bf16x2(v1[u * 8 + 4], v1[u * 8 + 5]);
+    q1.w = pack_bf16x2(v1[u * 8 + 6], v1[u * 8 + 7]);
+    st_shared_v4(smem_u32(stg0) + lane * 64 + ((u ^ sw) << 4), q0);
+    st_shared_v4(smem_u32(stg1) + lane * 64 + ((u ^ sw) << 4), q1);
+  }
+  tc::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map0)),
+                 "r"(smem_u32(stg0)), "r"(col), "r"(row0)
+                 : "memory");
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map1)),
+                 "r"(smem_u32(stg1)), "r"(col), "r"(row0)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EK, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -534,6 +572,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) v[j] += xa[j];
           }
         } else if (a.epi == AVB_EPI_BIAS_GELU) {
+          if (EK == 2 && SS % 2 == 0 && a.tma_out) {   // both outputs in one staged group
+#pragma unroll
+            for (int j = 0; j < 32; ++j) xa[j] = tc::quick_gelu(v[j]);
+            tma_store_chunk2<SS / 2 - 1>(stg + sbuf * 2048, &tmX, v, stg + ((sbuf + 1) % SS) * 2048, &tmC, xa, lane,
+                                         col, row0);
+            sbuf = (sbuf + 2) % SS;
+            continue;
+          }
           if (a.tma_out) {
             tma_store_chunk<SS - 1>(stg + sbuf * 2048, &tmX, lane, v, col, row0);
             sbuf = (sbuf + 1) % SS;
