@@ -856,9 +856,10 @@ extern "C" int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, 
   // aux / store rings so TMA latency is covered while the epilogue streams 32-column chunks
   const bool heavy = BN == 256 && a_major == 0 && (g.tma_aux || (g.tma_out && epilogue == AVB_EPI_BIAS_GELU)) &&
                      !knob("AVB_GEMM_NO_HEAVY");
-  // aux-reading epilogues: CTA pairs only when the mainloop is long enough to hide the aux stream
-  // (same-box: fc2 fwd + residual, K = 3072: 1208 -> 1355 TFLOP/s; K = 768 shapes 2-4 % slower)
-  if (pair && (!(heavy && g.tma_aux) || K >= 1536 || knob("AVB_GEMM_PAIR_AUX"))) {
+  // aux-reading epilogues run as CTA pairs too: with the staging on st.shared and the relaxed
+  // accumulator-empty arrival, the K = 768 shapes gained (same box: fc2 dgrad + dGELU 961 -> 996,
+  // proj fwd + residual 962 -> 1031 TFLOP/s; round 1, before those fixes, they were 2-4 % slower)
+  if (pair && !knob("AVB_GEMM_NO_PAIR_AUX")) {
     g.num_m = (M + 2 * BM - 1) / (2 * BM);
     if (heavy && g.tma_aux) {
       if (b_major == 0) return launch<256, false, false, 1, true>(ta, tb, tcm, tx, g, st);
