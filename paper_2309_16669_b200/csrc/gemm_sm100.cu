@@ -69,12 +69,31 @@ struct Cfg {
 #ifndef AVB_GEMM_PAIR_SSLOTS0
 #define AVB_GEMM_PAIR_SSLOTS0 4
 #endif
+// heavy-epilogue pair rings (stages / store slots / aux slots; same-box sweep with the pair-aux
+// change: EK1 4/2/3 + EK2 5/4 (default) vs EK1 5/2/2 + EK2 4/6 vs EK1 4/3/3: defaults best or within noise)
+#ifndef AVB_GEMM_PAIR_STAGES1
+#define AVB_GEMM_PAIR_STAGES1 4
+#endif
+#ifndef AVB_GEMM_SSLOTS1
+#define AVB_GEMM_SSLOTS1 2
+#endif
+#ifndef AVB_GEMM_XSLOTS1
+#define AVB_GEMM_XSLOTS1 3
+#endif
+#ifndef AVB_GEMM_PAIR_STAGES2
+#define AVB_GEMM_PAIR_STAGES2 5
+#endif
+#ifndef AVB_GEMM_SSLOTS2
+#define AVB_GEMM_SSLOTS2 4
+#endif
   static constexpr int STAGES =
-      PAIR ? (EK == 0 ? AVB_GEMM_PAIR_STAGES0 : (EK == 1 ? 4 : 5)) : ((BN == 256) ? (EK ? 3 : 4) : 6);
+      PAIR ? (EK == 0 ? AVB_GEMM_PAIR_STAGES0 : (EK == 1 ? AVB_GEMM_PAIR_STAGES1 : AVB_GEMM_PAIR_STAGES2))
+           : ((BN == 256) ? (EK ? 3 : 4) : 6);
   // EK 0: plain; 1: bf16 aux read (residual / GELU pre-activation); 2: second bf16 output (BIAS_GELU)
-  static constexpr int SSLOTS =
-      EK == 0 ? (PAIR ? AVB_GEMM_PAIR_SSLOTS0 : 2) : (EK == 1 ? 2 : 4);  // TMA-store staging slots per epilogue warp
-  static constexpr int XSLOTS = EK == 1 ? 3 : 1;                   // TMA-load aux ring slots per epilogue warp
+  static constexpr int SSLOTS =   // TMA-store staging slots per epilogue warp
+      EK == 0 ? (PAIR ? AVB_GEMM_PAIR_SSLOTS0 : 2)
+              : (EK == 1 ? (PAIR ? AVB_GEMM_SSLOTS1 : 2) : (PAIR ? AVB_GEMM_SSLOTS2 : 4));
+  static constexpr int XSLOTS = EK == 1 ? (PAIR ? AVB_GEMM_XSLOTS1 : 3) : 1;   // TMA-load aux ring slots per epilogue warp
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_BYTES = (SSLOTS + (EK == 1 ? XSLOTS : 0)) * kEpiWarps * 2048;  // 2 KB slots per epilogue warp
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
