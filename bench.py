@@ -155,6 +155,10 @@ def dist_setup(n_gpus: int):
     if world > torch.cuda.device_count():
         raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
     if world > 1:
+        # communicator lines show the N ranks; NCCL's log goes to stderr so that rank 0's stdout stays
+        # exactly one JSON line (NCCL writes INFO lines to stdout unless NCCL_DEBUG_FILE is set)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -565,7 +569,8 @@ def _relaunch(args) -> None:
     port = s.getsockname()[1]
     s.close()
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")          # communicator lines show the N ranks
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator lines show the N ranks (on stderr)
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
     os.execvpe(sys.executable, cmd, env)
