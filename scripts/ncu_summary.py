@@ -24,7 +24,7 @@ keys = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("smsp__inst_executed_pipe_xu.sum", "XU (MUFU) instructions"),
 ]
-for v in rows[2:]:
+for v in rows[2:]:   # every matching launch of the report (e.g. the three GEMM epilogue variants)
     d = dict(zip(h, v))
     if name not in d.get("Kernel Name", ""):
         continue
@@ -35,4 +35,3 @@ for v in rows[2:]:
     tensor = [k for k in h if "tensor" in k and "pct" in k]
     for k in tensor[:6]:
         print(f"  {k[:60]:60s} {d[k]}")
-    break
