@@ -2,33 +2,54 @@
 // Pre-LN ViT blocks (no reference code).
 //
 // One warp per row; lane l owns columns {l*8 + k*256 + 0..7}, k < NC = ceil(D/256), so every
-// access is a 16-byte vector.  Rows are kept as packed bf16 (4 registers per 8 columns) and
-// re-expanded on use, so a warp keeps two rows in flight.  The backward fuses the residual-
-// stream accumulation (dx += LN'(dy)) and reduces dgamma/dbeta per block in shared memory before
-// one atomic per column per block.
+// access is a 16-byte vector.  Inputs stream through a per-lane cp.async ring (rows prefetched
+// S-1 ahead, see below); gamma/beta live in registers as fp32 pairs and the math runs on packed
+// f32x2 instructions.  The backward fuses the residual-stream accumulation (dx += LN'(dy)); its
+// dgamma/dbeta (and the optional dx column sums) are reduced in a fixed order -- warp partials,
+// block partials, then the blocks in order -- so they are bit-reproducible.
 #include "common.cuh"
 
 #include <algorithm>
 
 namespace {
 
-__device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float2 v = __bfloat1622float2(h[e]);
-    f[2 * e] = v.x;
-    f[2 * e + 1] = v.y;
-  }
+// packed fp32 pairs (FFMA2 / FADD2 / FMUL2): half the FP instructions of the scalar forms
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return r;
 }
-__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ void unpack8x2(const uint4& q, float2 (&f)[4]) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) f[e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+}
+__device__ __forceinline__ uint4 pack8x2(const float2 (&f)[4]) {
   uint4 q;
-  q.x = pack_bf16x2(f[0], f[1]);
-  q.y = pack_bf16x2(f[2], f[3]);
-  q.z = pack_bf16x2(f[4], f[5]);
-  q.w = pack_bf16x2(f[6], f[7]);
+  q.x = pack_bf16x2(f[0].x, f[0].y);
+  q.y = pack_bf16x2(f[1].x, f[1].y);
+  q.z = pack_bf16x2(f[2].x, f[2].y);
+  q.w = pack_bf16x2(f[3].x, f[3].y);
   return q;
 }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
@@ -56,17 +77,18 @@ __device__ __forceinline__ void cp_async_wait() {
 #define AVB_LN_FWD_STAGES 4
 #endif
 #ifndef AVB_LN_FWD_BLOCKS
-#define AVB_LN_FWD_BLOCKS 4
+#define AVB_LN_FWD_BLOCKS 2   // 98 registers (gamma/beta pairs in registers): 2 blocks/SM, no spills
 #endif
 // same-box sweep at config 4 (bwd warps x stages): 8x4 0.122 ms, 12x3 0.112, 16x2 0.112, 6x5 0.155;
-// fwd (stages x blocks/SM): 4x4 0.0647, 6x4 0.0651, 3x6 0.0669, 8x3 0.0725
+// fwd (stages x blocks/SM, before the f32x2 rewrite): 4x4 0.0647, 6x4 0.0651, 3x6 0.0669, 8x3 0.0725;
+// with f32x2 math (blocks/SM bound): 2: 0.0606, 3 (80 regs + spills): 0.0657, 4 (64 regs + spills): 0.0799
 #ifndef AVB_LN_BWD_WARPS
 #define AVB_LN_BWD_WARPS 12
 #endif
 #ifndef AVB_LN_BWD_STAGES
 #define AVB_LN_BWD_STAGES 3
 #endif
-constexpr int kLnFwdWarps = 8, kLnFwdStages = AVB_LN_FWD_STAGES;   // AVB_LN_FWD_BLOCKS blocks / SM
+constexpr int kLnFwdWarps = 8, kLnFwdStages = AVB_LN_FWD_STAGES;   // AVB_LN_FWD_BLOCKS blocks / SM (launch bound)
 constexpr int kLnBwdWarps = AVB_LN_BWD_WARPS, kLnBwdStages = AVB_LN_BWD_STAGES;   // 1 block / SM
 
 template <int NC>
@@ -76,7 +98,7 @@ constexpr int ln_bwd_smem() { return kLnBwdWarps * kLnBwdStages * (3 * NC * 512 
 static_assert(kLnBwdWarps * kLnBwdStages * (3 * 512 + 256) >= kLnBwdWarps * 3 * 256 * 4, "per-warp partials fit the ring");
 
 template <int NC>
-__global__ void __launch_bounds__(32 * kLnFwdWarps) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(32 * kLnFwdWarps, AVB_LN_FWD_BLOCKS) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ gamma, const float* __restrict__ beta,
                                                      __nv_bfloat16* __restrict__ y, int64_t ldy, float* __restrict__ mean,
                                                      float* __restrict__ rstd, int M, int D, float eps) {
@@ -86,15 +108,15 @@ __global__ void __launch_bounds__(32 * kLnFwdWarps) ln_fwd_kernel(const __nv_bfl
   uint4* ring = ln_ring + warp * S * NC * 32 + lane;
   const int64_t nw = (int64_t)gridDim.x * kLnFwdWarps;
   bool ok[NC];
-  float gg[NC][8], bb[NC][8];
+  float2 gg[NC][4], bb[NC][4];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c = k * 256 + lane * 8;
     ok[k] = c < D;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      gg[k][e] = ok[k] ? __ldg(gamma + c + e) : 0.f;
-      bb[k][e] = ok[k] ? __ldg(beta + c + e) : 0.f;
+    for (int e = 0; e < 4; ++e) {
+      gg[k][e] = ok[k] ? make_float2(__ldg(gamma + c + 2 * e), __ldg(gamma + c + 2 * e + 1)) : make_float2(0.f, 0.f);
+      bb[k][e] = ok[k] ? make_float2(__ldg(beta + c + 2 * e), __ldg(beta + c + 2 * e + 1)) : make_float2(0.f, 0.f);
     }
   }
   auto issue = [&](int64_t row, int s) {
@@ -114,36 +136,38 @@ __global__ void __launch_bounds__(32 * kLnFwdWarps) ln_fwd_kernel(const __nv_bfl
     uint4 raw[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) raw[k] = ok[k] ? ring[(s * NC + k) * 32] : make_uint4(0, 0, 0, 0);
-    float sum = 0.f;
+    float2 sum = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
-      float f[8];
-      unpack8(raw[k], f);
+      float2 f[4];
+      unpack8x2(raw[k], f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) sum += f[e];
+      for (int e = 0; e < 4; ++e) sum = f2add(sum, f[e]);
     }
-    const float mu = warp_sum(sum) / D;
-    float q = 0.f;
+    const float mu = warp_sum(sum.x + sum.y) / D;
+    const float2 nmu = make_float2(-mu, -mu);
+    float2 q = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      float f[8];
-      unpack8(raw[k], f);
+      float2 f[4];
+      unpack8x2(raw[k], f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = f[e] - mu;
-        q += d * d;
+      for (int e = 0; e < 4; ++e) {
+        const float2 d = f2add(f[e], nmu);
+        q = f2fma(d, d, q);
       }
     }
-    const float rs = rsqrtf(warp_sum(q) / D + eps);
+    const float rs = rsqrtf(warp_sum(q.x + q.y) / D + eps);
+    const float2 rs2 = make_float2(rs, rs), nmr2 = make_float2(-mu * rs, -mu * rs);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      float f[8];
-      unpack8(raw[k], f);
+      float2 f[4];
+      unpack8x2(raw[k], f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gg[k][e] + bb[k][e];
-      *reinterpret_cast<uint4*>(y + row * ldy + k * 256 + lane * 8) = pack8(f);
+      for (int e = 0; e < 4; ++e) f[e] = f2fma(f2fma(f[e], rs2, nmr2), gg[k][e], bb[k][e]);   // (x - mu) rs g + b
+      *reinterpret_cast<uint4*>(y + row * ldy + k * 256 + lane * 8) = pack8x2(f);
     }
     if (lane == 0) {
       mean[row] = mu;
@@ -165,15 +189,15 @@ __global__ void __launch_bounds__(32 * kLnBwdWarps, 1) ln_bwd_kernel(const __nv_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint4* ring = ln_ring + warp * S * SLOT;
   bool ok[NC];
-  float gm[NC][8], dg[NC][8], db[NC][8], cs[NC][8];
+  float2 gm[NC][4], dg[NC][4], db[NC][4], cs[NC][4];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c = k * 256 + lane * 8;
     ok[k] = c < D;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      gm[k][e] = ok[k] ? __ldg(gamma + c + e) : 0.f;
-      dg[k][e] = db[k][e] = cs[k][e] = 0.f;
+    for (int e = 0; e < 4; ++e) {
+      gm[k][e] = ok[k] ? make_float2(__ldg(gamma + c + 2 * e), __ldg(gamma + c + 2 * e + 1)) : make_float2(0.f, 0.f);
+      dg[k][e] = db[k][e] = cs[k][e] = make_float2(0.f, 0.f);
     }
   }
   const int64_t nw = (int64_t)gridDim.x * kLnBwdWarps;
@@ -202,44 +226,46 @@ __global__ void __launch_bounds__(32 * kLnBwdWarps, 1) ln_bwd_kernel(const __nv_
     cp_async_wait<S - 1>();
     const uint4* slot = ring + s * SLOT;
     const float2 st = reinterpret_cast<const float2*>(slot + 3 * NC * 32)[lane];
-    const float mu = st.x, rs = st.y;
-    float s1 = 0.f, s2 = 0.f;
+    const float2 rs2 = make_float2(st.y, st.y), nmr2 = make_float2(-st.x * st.y, -st.x * st.y);   // xh = x rs - mu rs
+    float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      float xv[8], dv[8];
-      unpack8(slot[k * 32 + lane], xv);
-      unpack8(slot[(NC + k) * 32 + lane], dv);
+      float2 xv[4], dv[4];
+      unpack8x2(slot[k * 32 + lane], xv);
+      unpack8x2(slot[(NC + k) * 32 + lane], dv);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float xh = (xv[e] - mu) * rs;
-        const float g = dv[e] * gm[k][e];
-        s1 += g;
-        s2 += g * xh;
-        dg[k][e] += dv[e] * xh;
-        db[k][e] += dv[e];
+      for (int e = 0; e < 4; ++e) {
+        const float2 xh = f2fma(xv[e], rs2, nmr2);
+        const float2 g = f2mul(dv[e], gm[k][e]);
+        s1 = f2add(s1, g);
+        s2 = f2fma(g, xh, s2);
+        dg[k][e] = f2fma(dv[e], xh, dg[k][e]);
+        db[k][e] = f2add(db[k][e], dv[e]);
       }
     }
-    const float m1 = warp_sum(s1) / D, m2 = warp_sum(s2) / D;
+    const float m1 = warp_sum(s1.x + s1.y) / D, m2 = warp_sum(s2.x + s2.y) / D;
+    const float2 nm1 = make_float2(-m1, -m1), nm2 = make_float2(-m2, -m2);
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       if (!ok[k]) continue;
-      float xv[8], dv[8], pv[8], o[8];
-      unpack8(slot[k * 32 + lane], xv);
-      unpack8(slot[(NC + k) * 32 + lane], dv);
-      unpack8(slot[(2 * NC + k) * 32 + lane], pv);   // zero-filled when !accumulate
+      float2 xv[4], dv[4], pv[4], o[4];
+      unpack8x2(slot[k * 32 + lane], xv);
+      unpack8x2(slot[(NC + k) * 32 + lane], dv);
+      unpack8x2(slot[(2 * NC + k) * 32 + lane], pv);   // zero-filled when !accumulate
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float xh = (xv[e] - mu) * rs;
-        o[e] = rs * (dv[e] * gm[k][e] - m1 - xh * m2) + pv[e];
+      for (int e = 0; e < 4; ++e) {   // rs (dy gamma - m1 - xh m2) + dx_prev
+        const float2 xh = f2fma(xv[e], rs2, nmr2);
+        const float2 t = f2fma(xh, nm2, f2fma(dv[e], gm[k][e], nm1));
+        o[e] = f2fma(t, rs2, pv[e]);
       }
-      const uint4 q = pack8(o);
+      const uint4 q = pack8x2(o);
       *reinterpret_cast<uint4*>(dx + row * lddx + k * 256 + lane * 8) = q;
       if (SUM) {
-        float ob[8];
-        unpack8(q, ob);   // sum what was stored (bf16), like a separate column-sum pass would
+        float2 ob[4];
+        unpack8x2(q, ob);   // sum what was stored (bf16), like a separate column-sum pass would
 #pragma unroll
-        for (int e = 0; e < 8; ++e) cs[k][e] += ob[e];
+        for (int e = 0; e < 4; ++e) cs[k][e] = f2add(cs[k][e], ob[e]);
       }
     }
   }
@@ -253,10 +279,10 @@ __global__ void __launch_bounds__(32 * kLnBwdWarps, 1) ln_bwd_kernel(const __nv_
     const int c = k * 256 + lane * 8;
     if (c < D) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        wpart[(warp * 3 + 0) * D + c + e] = dg[k][e];
-        wpart[(warp * 3 + 1) * D + c + e] = db[k][e];
-        wpart[(warp * 3 + 2) * D + c + e] = SUM ? cs[k][e] : 0.f;
+      for (int e = 0; e < 4; ++e) {
+        *reinterpret_cast<float2*>(&wpart[(warp * 3 + 0) * D + c + 2 * e]) = dg[k][e];
+        *reinterpret_cast<float2*>(&wpart[(warp * 3 + 1) * D + c + 2 * e]) = db[k][e];
+        *reinterpret_cast<float2*>(&wpart[(warp * 3 + 2) * D + c + 2 * e]) = SUM ? cs[k][e] : make_float2(0.f, 0.f);
       }
     }
   }
