@@ -567,17 +567,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (col >= a.N) continue;
         float v[32];
+        // the element-wise epilogue math runs on f32x2 pairs (FFMA2 / FMUL2 / FADD2)
+        auto pr = [](float (&w)[32], int j) -> float2 { return make_float2(w[j], w[j + 1]); };
+        auto pw = [](float (&w)[32], int j, float2 p) { w[j] = p.x; w[j + 1] = p.y; };
+        const float2 alpha2 = make_float2(a.alpha, a.alpha);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * a.alpha;
+        for (int j = 0; j < 32; j += 2)
+          pw(v, j, tc::f2mul(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), alpha2));
         if (a.bias) {
           if (col + 32 <= a.N && a.vec_ok) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + col + j));
-              v[j] += bb.x;
-              v[j + 1] += bb.y;
-              v[j + 2] += bb.z;
-              v[j + 3] += bb.w;
+              pw(v, j, tc::f2add(pr(v, j), make_float2(bb.x, bb.y)));
+              pw(v, j + 2, tc::f2add(pr(v, j + 2), make_float2(bb.z, bb.w)));
             }
           } else {
 #pragma unroll
@@ -588,12 +591,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (a.aux) {
             if (!tma_aux) load_aux_chunk(a, a.aux, row, col, xa);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += xa[j];
+            for (int j = 0; j < 32; j += 2) pw(v, j, tc::f2add(pr(v, j), pr(xa, j)));
           }
         } else if (a.epi == AVB_EPI_BIAS_GELU) {
           if (EK == 2 && SS % 2 == 0 && a.tma_out) {   // both outputs in one staged group
 #pragma unroll
-            for (int j = 0; j < 32; ++j) xa[j] = tc::quick_gelu(v[j]);
+            for (int j = 0; j < 32; j += 2) pw(xa, j, tc::quick_gelu2(pr(v, j)));
             tma_store_chunk2<SS / 2 - 1>(stg + sbuf * 2048, &tmX, v, stg + ((sbuf + 1) % SS) * 2048, &tmC, xa, lane,
                                          col, row0);
             sbuf = (sbuf + 2) % SS;
@@ -606,11 +609,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             store_aux_chunk(a, row, col, v);
           }
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = tc::quick_gelu(v[j]);
+          for (int j = 0; j < 32; j += 2) pw(v, j, tc::quick_gelu2(pr(v, j)));
         } else if (a.epi == AVB_EPI_DGELU) {
           if (!tma_aux) load_aux_chunk(a, a.aux, row, col, xa);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= tc::quick_gelu_grad(xa[j]);
+          for (int j = 0; j < 32; j += 2) pw(v, j, tc::f2mul(pr(v, j), tc::quick_gelu_grad2(pr(xa, j))));
         }
         if (a.tma_out) {
           tma_store_chunk<SS - 1>(stg + sbuf * 2048, &tmC, lane, v, col, row0);

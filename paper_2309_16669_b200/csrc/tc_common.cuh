@@ -252,6 +252,43 @@ __device__ __forceinline__ float tanh_approx(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// packed fp32 pairs (FFMA2 / FADD2 / FMUL2)
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return r;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
+}
+// QuickGELU and its derivative on a pair (the same formulas as the scalar forms below)
+__device__ __forceinline__ float2 quick_gelu2(float2 x) {
+  const float2 a = f2mul(x, make_float2(0.851f, 0.851f));
+  const float2 s = f2fma(make_float2(tanh_approx(a.x), tanh_approx(a.y)), make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+  return f2mul(x, s);
+}
+__device__ __forceinline__ float2 quick_gelu_grad2(float2 x) {
+  const float2 a = f2mul(x, make_float2(0.851f, 0.851f));
+  const float2 s = f2fma(make_float2(tanh_approx(a.x), tanh_approx(a.y)), make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+  const float2 xs = f2mul(f2mul(x, make_float2(1.702f, 1.702f)), s);            // 1.702 x s
+  const float2 oms = f2fma(s, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));   // 1 - s
+  return f2fma(xs, oms, s);
+}
+
 __device__ __forceinline__ float quick_gelu(float x) {
   const float s = fmaf(0.5f, tanh_approx(0.851f * x), 0.5f);
   return x * s;
