@@ -922,57 +922,83 @@ __global__ void __launch_bounds__(256, 4) k1v4_kernel(const K1v4Params p) {
 // planar Batch.frames layout [B,T,3,Ht,Wt] (loader.py:99-116).  Full-frame boxes at identity scale
 // reduce K1 to flip + normalize + cast + re-layout: one thread per 16 pixels of one channel row,
 // one 16-byte load, two 16-byte bf16 stores (16 output columns are contiguous in every layout).
+// Each thread moves kIdU chunks spaced one grid apart: all kIdU 16-byte loads are issued before the
+// first store (HBM needs ~40 KB in flight per SM; one chunk per thread left it latency-bound at 65 %),
+// and the chunk -> (clip, frame, channel, row, column) decode runs in 32-bit arithmetic (IDX = uint32_t)
+// whenever the chunk count allows (the 64-bit divisions were most of the instructions).
+#ifndef AVB_K1_ID_U
+#define AVB_K1_ID_U 4
+#endif
+constexpr int kIdU = AVB_K1_ID_U;
+template <typename IDX>
 __global__ void __launch_bounds__(256) k1_identity_kernel(const K1Params p, int64_t nchunks) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= nchunks) return;
-  const int cpr = p.Wt >> 4;                        // 16-pixel chunks per row
-  const int xc = (int)(gid % cpr);
-  int64_t r = gid / cpr;                            // ((b*T + t)*3 + c)*Ht + y
-  const int y = (int)(r % p.Ht);
-  r /= p.Ht;
-  const int c = (int)(r % 3);
-  r /= 3;
-  const int t = (int)(r % p.T);
-  const int64_t b = r / p.T;
-  const bool flip = p.flips ? (p.flips[b] != 0) : false;
-  const int x0 = flip ? p.Wt - 16 * (xc + 1) : 16 * xc;   // source chunk (mirrored when flipped)
-  const uint8_t* src = p.src + b * p.s_clip + (int64_t)t * p.s_t + (int64_t)c * p.s_c + (int64_t)y * p.s_h + x0;
-  uint4 v = *reinterpret_cast<const uint4*>(src);
-  if (flip) {  // reverse the 16 bytes
-    const uint32_t w0 = __byte_perm(v.w, 0, 0x0123), w1 = __byte_perm(v.z, 0, 0x0123),
-                   w2 = __byte_perm(v.y, 0, 0x0123), w3 = __byte_perm(v.x, 0, 0x0123);
-    v = make_uint4(w0, w1, w2, w3);
-  }
-  const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-  const float sc = p.scale[c], bi = p.bias[c];
-  float f[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) f[k] = fmaf((float)((wd[k >> 2] >> (8 * (k & 3))) & 0xffu), sc, bi);
-  const int j = 16 * xc;
-  int64_t o;
+  const IDX n = (IDX)nchunks;
+  const IDX stride = (IDX)gridDim.x * blockDim.x;
+  const IDX cpr = (IDX)(p.Wt >> 4);                 // 16-pixel chunks per row
   const int64_t plane = (int64_t)p.Ht * p.Wt;
-  if (p.out_layout == AVB_LAYOUT_CTHW) {
-    o = ((b * 3 + c) * p.T + t) * plane + (int64_t)y * p.Wt + j;
-  } else if (p.out_layout == AVB_LAYOUT_TCHW) {
-    o = ((b * p.T + t) * 3 + c) * plane + (int64_t)y * p.Wt + j;
-  } else {
-    const int npy = p.Ht / p.tph, npx = p.Wt / p.tpw;
-    const int64_t Np = (int64_t)(p.T / p.tt) * npy * npx;
-    const int F = 3 * p.tt * p.tph * p.tpw;
-    o = (b * Np + ((int64_t)(t / p.tt) * npy + y / p.tph) * npx + j / p.tpw) * F +
-        ((c * p.tt + t % p.tt) * p.tph + y % p.tph) * p.tpw + j % p.tpw;
-  }
-  if (p.out_dtype == AVB_DTYPE_BF16) {
-    uint4 lo, hi;
-    lo.x = pack_bf16x2(f[0], f[1]); lo.y = pack_bf16x2(f[2], f[3]); lo.z = pack_bf16x2(f[4], f[5]); lo.w = pack_bf16x2(f[6], f[7]);
-    hi.x = pack_bf16x2(f[8], f[9]); hi.y = pack_bf16x2(f[10], f[11]); hi.z = pack_bf16x2(f[12], f[13]); hi.w = pack_bf16x2(f[14], f[15]);
-    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.dst) + o);
-    d[0] = lo;
-    d[1] = hi;
-  } else {
-    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.dst) + o);
+  for (IDX g0 = (IDX)blockIdx.x * blockDim.x + threadIdx.x; g0 < n; g0 += stride * kIdU) {
+    uint4 v[kIdU];
+    int64_t o[kIdU];
+    int cf[kIdU];                                   // channel | flip << 2; -1: past the end
 #pragma unroll
-    for (int k = 0; k < 4; ++k) d[k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+    for (int u = 0; u < kIdU; ++u) {
+      const IDX gid = g0 + (IDX)u * stride;
+      cf[u] = -1;
+      if (gid >= n) continue;
+      IDX r = gid / cpr;
+      const int xc = (int)(gid - r * cpr);
+      const IDX r2 = r / (IDX)p.Ht;                 // ((b*T + t)*3 + c)*Ht + y
+      const int y = (int)(r - r2 * (IDX)p.Ht);
+      const IDX r3 = r2 / 3u;
+      const int c = (int)(r2 - r3 * 3u);
+      const IDX bb = r3 / (IDX)p.T;
+      const int t = (int)(r3 - bb * (IDX)p.T);
+      const int64_t b = (int64_t)bb;
+      const bool flip = p.flips ? (p.flips[b] != 0) : false;
+      const int x0 = flip ? p.Wt - 16 * (xc + 1) : 16 * xc;   // source chunk (mirrored when flipped)
+      const uint8_t* src = p.src + b * p.s_clip + (int64_t)t * p.s_t + (int64_t)c * p.s_c + (int64_t)y * p.s_h + x0;
+      v[u] = __ldg(reinterpret_cast<const uint4*>(src));
+      cf[u] = c | (flip ? 4 : 0);
+      const int j = 16 * xc;
+      if (p.out_layout == AVB_LAYOUT_CTHW) {
+        o[u] = ((b * 3 + c) * p.T + t) * plane + (int64_t)y * p.Wt + j;
+      } else if (p.out_layout == AVB_LAYOUT_TCHW) {
+        o[u] = ((b * p.T + t) * 3 + c) * plane + (int64_t)y * p.Wt + j;
+      } else {
+        const int npy = p.Ht / p.tph, npx = p.Wt / p.tpw;
+        const int64_t Np = (int64_t)(p.T / p.tt) * npy * npx;
+        const int F = 3 * p.tt * p.tph * p.tpw;
+        o[u] = (b * Np + ((int64_t)(t / p.tt) * npy + y / p.tph) * npx + j / p.tpw) * F +
+               ((c * p.tt + t % p.tt) * p.tph + y % p.tph) * p.tpw + j % p.tpw;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kIdU; ++u) {
+      if (cf[u] < 0) continue;
+      const int c = cf[u] & 3;
+      uint4 w = v[u];
+      if (cf[u] & 4) {  // reverse the 16 bytes
+        w = make_uint4(__byte_perm(w.w, 0, 0x0123), __byte_perm(w.z, 0, 0x0123), __byte_perm(w.y, 0, 0x0123),
+                       __byte_perm(w.x, 0, 0x0123));
+      }
+      const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+      const float sc = p.scale[c], bi = p.bias[c];
+      float f[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) f[k] = fmaf((float)((wd[k >> 2] >> (8 * (k & 3))) & 0xffu), sc, bi);
+      if (p.out_dtype == AVB_DTYPE_BF16) {
+        uint4 lo, hi;
+        lo.x = pack_bf16x2(f[0], f[1]); lo.y = pack_bf16x2(f[2], f[3]); lo.z = pack_bf16x2(f[4], f[5]); lo.w = pack_bf16x2(f[6], f[7]);
+        hi.x = pack_bf16x2(f[8], f[9]); hi.y = pack_bf16x2(f[10], f[11]); hi.z = pack_bf16x2(f[12], f[13]); hi.w = pack_bf16x2(f[14], f[15]);
+        uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.dst) + o[u]);
+        d[0] = lo;
+        d[1] = hi;
+      } else {
+        float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.dst) + o[u]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+      }
+    }
   }
 }
 
@@ -1132,7 +1158,11 @@ static int rrc_normalize_impl(const uint8_t* src, int64_t B, int T, int H, int W
               boxes_host[4 * i + 3] == H;
     if (ident) {
       const int64_t nchunks = B * (int64_t)T * 3 * Ht * (Wt / 16);
-      k1_identity_kernel<<<(unsigned)((nchunks + 255) / 256), 256, 0, avb::as_stream(stream)>>>(p, nchunks);
+      const int64_t blocks = std::min<int64_t>((nchunks + 256 * kIdU - 1) / (256 * kIdU), 65535LL * 1024);
+      if (nchunks < (1LL << 31) - 256LL * kIdU * 2)
+        k1_identity_kernel<uint32_t><<<(unsigned)blocks, 256, 0, avb::as_stream(stream)>>>(p, nchunks);
+      else
+        k1_identity_kernel<uint64_t><<<(unsigned)blocks, 256, 0, avb::as_stream(stream)>>>(p, nchunks);
       return avb::launch_status("avb_rrc_normalize (identity)");
     }
   }
