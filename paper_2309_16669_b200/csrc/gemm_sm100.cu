@@ -24,6 +24,7 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <atomic>
 
 #include <stdlib.h>
 #include <string.h>
@@ -680,17 +681,21 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcm,
   cfg.attrs = attr2;
   cfg.numAttrs = 1;
   // persistent pairs: as many as can be co-resident (a TPC with a harvested SM hosts no pair)
-  static int max_pairs = 0;
-  if (max_pairs == 0) {
+  // (per device and kernel instantiation; a benign race between threads computes the same value)
+  static std::atomic<int> max_pairs_dev[64];
+  int dev = 0;
+  (void)cudaGetDevice(&dev);
+  std::atomic<int>& max_pairs = max_pairs_dev[dev & 63];
+  if (max_pairs.load(std::memory_order_relaxed) == 0) {
     cfg.gridDim = dim3(avb::sm_count(), 1, 1);
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) {
       (void)cudaGetLastError();
       n = avb::sm_count() / 2;
     }
-    max_pairs = n;
+    max_pairs.store(n, std::memory_order_relaxed);
   }
-  const int pairs = std::min(total, max_pairs);
+  const int pairs = std::min(total, max_pairs.load(std::memory_order_relaxed));
   cfg.gridDim = dim3(2 * pairs, 1, 1);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tx, a);
   if (e != cudaSuccess) return avb::cuda_status(e, "avb_gemm (pair launch)");
