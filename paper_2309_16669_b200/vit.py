@@ -266,9 +266,13 @@ class TransformerStack:
         for l in reversed(range(self.L)):
             g = f"{P}.blk{l}"
             x, h1, mu1, rs1, qkv, o2, lse, x2, h2, mu2, rs2, pre, a = saved[l]
-            # fc2: x3 = x2 + a W2^T + b2
+            # fc2: x3 = x2 + a W2^T + b2.  Bias gradients that are column sums of the residual-stream
+            # gradient dx come out of the LayerNorm backward that produced dx (fixed-order, nearly free
+            # there; as an extra N=16 MMA per K step they cost the wgrad GEMM 12-16 %): fc2.b of block l
+            # from block l+1's ln1 backward, proj.b from this block's ln2 backward.  Only the top
+            # block's fc2.b (dx from the caller) uses the GEMM row sums.
             ops.gemm(dx, a, a_mn=True, b_mn=True, out=s.g(f"{g}.fc2.w"), epilogue=ops.EPI_F32_ACCUM,
-                     split_k=wgrad_split(D, Hd, M), a_rowsum=s.g(f"{g}.fc2.b"))
+                     split_k=wgrad_split(D, Hd, M), a_rowsum=s.g(f"{g}.fc2.b") if l == self.L - 1 else None)
             dpre = ops.gemm(dx, s.w(f"{g}.fc2.w"), b_mn=True, epilogue=ops.EPI_DGELU, aux=pre)
             # fc1: pre = h2 W1^T + b1
             ops.gemm(dpre, h2, a_mn=True, b_mn=True, out=s.g(f"{g}.fc1.w"), epilogue=ops.EPI_F32_ACCUM,
@@ -276,11 +280,11 @@ class TransformerStack:
             dh2 = ops.gemm(dpre, s.w(f"{g}.fc1.w"), b_mn=True)
             del dpre
             ops.layernorm_bwd(dh2, x2, s.p(f"{g}.ln2.g"), mu2, rs2, dx, s.g(f"{g}.ln2.g"), s.g(f"{g}.ln2.b"),
-                              accumulate=True)
+                              accumulate=True, dx_colsum=s.g(f"{g}.proj.b"))
             del dh2
-            # proj: x2 = x + o Wo^T + bo
+            # proj: x2 = x + o Wo^T + bo (bias gradient: the column sums above)
             ops.gemm(dx, o2, a_mn=True, b_mn=True, out=s.g(f"{g}.proj.w"), epilogue=ops.EPI_F32_ACCUM,
-                     split_k=wgrad_split(D, D, M), a_rowsum=s.g(f"{g}.proj.b"))
+                     split_k=wgrad_split(D, D, M))
             do = ops.gemm(dx, s.w(f"{g}.proj.w"), b_mn=True)
             q3 = qkv.view(B, N, 3 * D)
             dqkv = torch.empty((M, 3 * D), dtype=torch.bfloat16, device=dev)
@@ -293,7 +297,7 @@ class TransformerStack:
             dh1 = ops.gemm(dqkv, s.w(f"{g}.qkv.w"), b_mn=True)
             del dqkv
             ops.layernorm_bwd(dh1, x, s.p(f"{g}.ln1.g"), mu1, rs1, dx, s.g(f"{g}.ln1.g"), s.g(f"{g}.ln1.b"),
-                              accumulate=True)
+                              accumulate=True, dx_colsum=s.g(f"{P}.blk{l - 1}.fc2.b") if l > 0 else None)
             del dh1
             saved[l] = None
             if on_layer_done is not None:

@@ -91,7 +91,8 @@ def test_odd_n_unaligned_head():
 
 
 @pytest.mark.parametrize("Mtok,Nout,Kin,splits", [(100416 // 8, 768, 3072, 2), (12552, 3072, 768, 2),
-                                                  (1000, 200, 136, 1), (777, 2304, 768, 5), (64, 3808, 768, 1)])
+                                                  (1000, 200, 136, 1), (777, 2304, 768, 5), (64, 3808, 768, 1),
+                                                  (256, 512, 3072, 2)])   # more n-tiles than K blocks per split
 def test_wgrad_rowsum_bias_grad(Mtok, Nout, Kin, splits):
     # fused bias gradient: a_rowsum[n] += sum_tokens dY[token, n] alongside dW = dY^T X
     dY, X = mk(Mtok, Nout, seed=16), mk(Mtok, Kin, seed=17)
