@@ -458,7 +458,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
         const int acc = rs_mode ? 0 : (it & 1);
         const uint32_t acc_phase = rs_mode ? (it & 1) : ((it >> 1) & 1);
-        const bool do_rs = rs_mode && (t % a.num_n) == 0;   // row sums once per row block (n-tile 0)
+        // row sums: with split-K, n-tile r of a row block sums the r-th of num_n contiguous parts of the
+        // unit's K blocks (the launch waits for its slowest tile; n-tile 0 alone took +12-19 %) and adds
+        // its partial sums atomically.  Without split-K (deterministic mode) n-tile 0 sums them all.
+        const int rs_n = t % a.num_n, rs_len = kb1 - kb0;
+        const int rs_lo = a.splits > 1 ? kb0 + (int)((int64_t)rs_len * rs_n / a.num_n) : (rs_n == 0 ? kb0 : kb1);
+        const int rs_hi = a.splits > 1 ? kb0 + (int)((int64_t)rs_len * (rs_n + 1) / a.num_n) : kb1;
         tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
@@ -469,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // descriptors differ only in the start-address field (bits 0-13, 16-byte units)
           const uint64_t soff = (uint64_t)((stage * C::STAGE_BYTES) >> 4);
 #pragma unroll
+          const bool do_rs = rs_mode && kb >= rs_lo && kb < rs_hi;
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t da = da0 + soff + (uint64_t)((A_MN ? k * 2048 : k * 32) >> 4);
             const uint64_t db = db0 + soff + (uint64_t)((B_MN ? k * 2048 : k * 32) >> 4);
@@ -476,13 +482,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_f16_ss_cg2_w(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
               if (do_rs)   // ones tile: each CTA supplies 8 of the 16 B rows (all ones)
                 umma_f16_ss_cg2_w(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
-                                (kb > kb0 || k > 0) ? 1u : 0u);
+                                (kb > rs_lo || k > 0) ? 1u : 0u);
               continue;
             }
             tc::umma_f16_ss_w(d_tmem, da, db, C::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
             if (do_rs)
               tc::umma_f16_ss_w(tmem + BN, da, tc::sdesc_sw128(ones_u32 + k * 32, 16, 1024), C::IDESC_RS,
-                              (kb > kb0 || k > 0) ? 1u : 0u);
+                              (kb > rs_lo || k > 0) ? 1u : 0u);
           }
           if (PAIR) umma_commit_pair_w(&empty[stage]); else tc::umma_commit_w(&empty[stage]);
           if (++stage == C::STAGES) {
@@ -527,7 +533,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tc_fence_after();
       const int row = row0 + lane;
       const uint32_t tbase = tmem + acc * BN + tlane + eh * (BN / 2);
-      if (rs_mode && eh == 0 && (mn % a.num_n) == 0) {
+      bool has_rs = false;
+      if (rs_mode && eh == 0) {   // the MMA warp's rs_lo < rs_hi for this tile
+        const int split = t / (a.num_m * a.num_n);
+        const int kb0 = split * a.kb_per_split, kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        const int rn = mn % a.num_n, len = kb1 - kb0;
+        has_rs = a.splits > 1 ? ((int64_t)len * (rn + 1) / a.num_n > (int64_t)len * rn / a.num_n) : rn == 0;
+      }
+      if (has_rs) {
         uint32_t rs;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(rs) : "r"(tmem + BN + tlane));
         tc::tmem_ld_wait();
