@@ -120,7 +120,9 @@ int avb_rrc_taps(int crop, int tgt, int32_t* lo_dev, int32_t* hi_dev, float* w_d
  * and wgrad (both MN-major, EPI_F32_ACCUM, split_k over the token dimension).
  *   a_rowsum: fp32 [M] or NULL (fp32 epilogues only): a_rowsum[m] += sum_k A[m,k], unscaled --
  *   for a wgrad (A = dY^T) that is the bias gradient, computed on the tensor cores from the
- *   A tiles already in shared memory instead of a second pass over dY.
+ *   A tiles already in shared memory instead of a second pass over dY.  With split_k > 1 the
+ *   n-tiles of a row block each sum a contiguous part of the K range and add atomically (order
+ *   not fixed); with split_k == 1 one tile adds each row once (bit-reproducible).
  */
 int avb_gemm(const void* A, int64_t lda, int a_major, const void* B, int64_t ldb, int b_major,
              void* C, int64_t ldc, int M, int N, int K, int epilogue, const float* bias,
